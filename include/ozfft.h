@@ -1,0 +1,180 @@
+/*
+ * ozfft.h -- C ABI of the B200 (sm_100a) fp64-accurate FFT built from 32-bit NTTs.
+ *
+ * Method: arXiv 2603.29129 (Kawakami & Takahashi).  References "P:N" are lines of
+ * /root/reference/PAPER.md; "S:N" lines of SPEC.md; "SURVEY" = SURVEY.md.
+ *
+ *   y = DFT(x), x in F64^n + i F64^n, any n >= 1 (Alg.4 Require/Ensure, P:464-465;
+ *   eq:dft P:152-156, omega_n = e^{-2 pi i / n}).
+ *   Bluestein (Alg.1) with cyclic length m = 2^ceil(log2(2n-1)),
+ *   Ozaki split of Re/Im of x' = x (.) omega into <= K int32 slices (Alg.6, P:768-793;
+ *   cap K), exact slice convolutions by 32-bit NTTs modulo p0 and p1
+ *   (P:670-716), NTT-domain accumulation of <= L equal-scale products before each
+ *   inverse NTT (Alg.8), two-prime Garner CRT, scaled DD
+ *   recombination and post-chirp (Alg.4).
+ *
+ * Conventions (all entry points):
+ *   - Every call returns an ozfft_status; nothing throws across the ABI.  On error
+ *     ozfft_last_error_string() (thread-local) describes it.
+ *   - Device pointers are CUDA device addresses on the plan's device; `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Complex data are contiguous [batch][n] interleaved (re, im) binary64 -- the
+ *     memory of a contiguous torch.complex128 tensor; 16-byte aligned.
+ *   - The caller owns every buffer: input/output, the plan's persistent buffer and
+ *     its workspace.  execute never allocates, never synchronizes the host, and
+ *     never falls back to the CPU.
+ *   - A plan is immutable after bind; one execute at a time per bound workspace.
+ */
+#ifndef OZFFT_H
+#define OZFFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  OZFFT_OK = 0,
+  OZFFT_ERR_INVALID_ARGUMENT = 1,   /* null pointer, n < 1, batch < 1, K/L out of range */
+  OZFFT_ERR_UNSUPPORTED_LENGTH = 2, /* m > 2^min(two-adicity(p0), two-adicity(p1)) */
+  OZFFT_ERR_BAD_PRIMES = 3,         /* not prime, equal, >= 2^31, or p0*p1 >= 2^62        */
+  OZFFT_ERR_ALPHA = 4,              /* alpha < 1: no slice width fits            */
+  OZFFT_ERR_NOT_BOUND = 5,          /* execute before bind                              */
+  OZFFT_ERR_MISALIGNED = 6,         /* buffer not 16-byte (256-byte for plan buffers) aligned */
+  OZFFT_ERR_CUDA = 7,               /* a CUDA runtime error (message in last_error)      */
+  OZFFT_ERR_SHARD = 8,              /* bad shard index / count                          */
+  OZFFT_ERR_BUFFER_TOO_SMALL = 9    /* persistent or workspace size below plan_get_info  */
+} ozfft_status;
+
+/* Plan descriptor.  Defaults (zeros) mean: K = 3, L = 3, p0 = 2,130,706,433,
+ * p1 = 2,113,929,217 (the paper's primes), device = current device,
+ * max_workspace_bytes = 16 GiB (the batch is processed in chunks that fit). */
+typedef struct {
+  int64_t n;                  /* DFT length, >= 1                                  */
+  int64_t batch;              /* independent transforms per execute, >= 1          */
+  int32_t K;                  /* split cap per real vector, 1..8       */
+  int32_t L;                  /* NTT-domain accumulation bound, 1..8   */
+  uint32_t p0, p1;            /* NTT primes, < 2^31, p-1 divisible by m            */
+  int32_t device;             /* CUDA device ordinal, -1 = current                 */
+  int32_t reserved;
+  uint64_t max_workspace_bytes;
+} ozfft_plan_desc;
+
+typedef struct {
+  int64_t n, m, batch, chunk;   /* m: Bluestein cyclic length; chunk: transforms per pass */
+  int32_t K, L, alpha, rho;     /* alpha = floor((log2(p0p1/2) - log2(L n))/2), rho = 53-alpha */
+  int32_t log2_rows, log2_cols; /* NTT decomposition m = R x C (two passes when R > 1) */
+  uint64_t persistent_bytes;    /* caller allocates; 256-byte aligned              */
+  uint64_t workspace_bytes;     /* caller allocates; 256-byte aligned              */
+  int32_t cached_ntts;          /* forward NTTs of omega~* slices done at bind */
+  int32_t reserved;
+} ozfft_plan_info;
+
+typedef struct {
+  int32_t k[4];          /* slices of Re x', Im x' (transform 0), Re w~*, Im w~*      */
+  int64_t fwd_ntts;      /* runtime forward NTTs over the last execute (all transforms) */
+  int64_t inv_ntts;      /* runtime inverse NTTs (= 2 x groups)                      */
+  int64_t cached_ntts;   /* plan-time forward NTTs of omega~* slices                 */
+  int64_t groups;        /* Alg.8 flush groups over the batch                        */
+  int64_t nonfinite;     /* transforms whose input had NaN/Inf (output set to NaN)   */
+  uint32_t flags;        /* bit0: some input non-finite; bit1: CRT range fix (never expected) */
+  int32_t reserved;
+} ozfft_exec_stats;
+
+/* Test-only stage outputs (device pointers, any may be NULL), for ONE execute of a
+ * plan whose batch fits in a single chunk.  Layouts match the oracle's taps, in the
+ * natural (paper) order -- internal orders are converted by tap kernels:
+ *   digits int32 [B][2][K][n]     E int32 [B][2][K]    kv int32 [B][2]
+ *   X   uint32 [B][2 part][K][2 prime][m]     forward NTTs of the slices
+ *   sched int32 [B][4 conv][1 + K*K*(2+2L)]   Alg.8 groups: ngroups, then per group
+ *                                             cexp, npairs, (s,t) x L
+ *   Z   uint32 [B][4][K*K][2][m]  NTT-domain accumulated groups (Alg.8 l.981-982)
+ *   res uint32 [B][4][K*K][2][n]  inverse-NTT outputs j < n (l.973)
+ *   crt int64  [B][4][K*K][n]     Garner integers (l.974)
+ *   W   uint32 [2 part][K][2 prime][m]        cached omega~* spectra (plan data)
+ * conv order: rr, ii, ir, ri as (x part, w part) = (0,0),(1,1),(1,0),(0,1).      */
+typedef struct {
+  void* digits;
+  void* E;
+  void* kv;
+  void* X;
+  void* sched;
+  void* Z;
+  void* res;
+  void* crt;
+  void* W;
+} ozfft_taps;
+
+typedef struct ozfft_plan ozfft_plan;
+
+/* Host-side plan math only (alpha, roots of unity, twiddle tables, the correctly
+ * rounded chirp table (ruling 3) and omega~* = ZeroPad_pm(omega*, m)
+ * ).  No device memory is touched.  Errors: INVALID_ARGUMENT,
+ * UNSUPPORTED_LENGTH, BAD_PRIMES, ALPHA.  On success *out owns a host plan. */
+ozfft_status ozfft_plan_create(const ozfft_plan_desc* desc, ozfft_plan** out);
+
+/* Sizes and derived parameters; valid right after create. */
+ozfft_status ozfft_plan_get_info(const ozfft_plan* plan, ozfft_plan_info* info);
+
+/* Bind caller-owned device memory (persistent >= info.persistent_bytes, workspace >=
+ * info.workspace_bytes, both 256-byte aligned) and precompute on `stream`: uploads
+ * tables, splits omega~* (Alg.6) and runs its 4K forward NTTs into the
+ * cached W spectra.  Synchronizes `stream` once (plan time, not on the hot path).
+ * Errors: INVALID_ARGUMENT, MISALIGNED, BUFFER_TOO_SMALL, CUDA. */
+ozfft_status ozfft_plan_bind(ozfft_plan* plan, void* persistent, size_t persistent_bytes,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* y = DFT(x) (direction -1) or x = DFT^-1(y) (direction +1, P:158-160,
+ * computed as conj(DFT(conj(y)))/n with RN division, ruling 16), for the plan's
+ * batch.  `in` and `out` are device complex128 [batch][n]; in == out is allowed.
+ * Asynchronous on `stream`.  Errors: NOT_BOUND, INVALID_ARGUMENT, MISALIGNED, CUDA. */
+ozfft_status ozfft_execute(const ozfft_plan* plan, const void* in, void* out, int direction,
+                           void* stream);
+
+/* Same as ozfft_execute but `in`/`out` are HOST buffers (ideally pinned): the
+ * host->device copy of the inputs and the device->host copy of the outputs are
+ * issued on `stream` around the device pipeline; returns after the D2H copy has
+ * completed (synchronizes `stream`).  Uses the workspace's staging area. */
+ozfft_status ozfft_execute_host(const ozfft_plan* plan, const double* in, double* out,
+                                int direction, void* stream);
+
+/* As ozfft_execute, additionally writing the stage outputs listed in ozfft_taps.
+ * Requires info.chunk == info.batch.  Test-only; not on the hot path. */
+ozfft_status ozfft_execute_taps(const ozfft_plan* plan, const void* in, void* out,
+                                int direction, void* stream, const ozfft_taps* taps);
+
+/* Statistics of the last execute on this plan (synchronizes `stream`). */
+ozfft_status ozfft_last_stats(const ozfft_plan* plan, ozfft_exec_stats* stats, void* stream);
+
+/* ---- single large transform sharded over `nshards` ranks ----------
+ * Unit u in [0, 8) = (prime q = u % 2, real conv cv = u / 2) (conv order as in taps).
+ * Rank `shard` computes the contiguous units [shard*8/nshards, (shard+1)*8/nshards)
+ * (with 8 ranks: rank r = (prime r % 2, conv r / 2)) of transform 0: it redoes the O(n)
+ * premultiply/split of `in` (identical digits on every rank), runs its forward NTTs,
+ * NTT-domain accumulation and inverse NTTs, and writes residues into its contiguous
+ * slice of `residues_out`, a device uint32 buffer of ozfft_shard_residue_bytes()
+ * bytes laid out [8 units][K*K groups][n] (slice = units of this shard).  Shards are
+ * then all-gathered by the caller (torch.distributed / NCCL) into every rank's full
+ * buffer and ozfft_shard_finish() performs CRT, recombination and post-chirp.
+ * nshards must divide 8.  Errors: SHARD, NOT_BOUND, CUDA. */
+uint64_t ozfft_shard_residue_bytes(const ozfft_plan* plan);
+ozfft_status ozfft_shard_partial(const ozfft_plan* plan, int shard, int nshards, const void* in,
+                                 int direction, void* residues_out, void* stream);
+ozfft_status ozfft_shard_finish(const ozfft_plan* plan, const void* residues_all, void* out,
+                                int direction, void* stream);
+
+/* Free the host plan (device buffers stay owned by the caller). */
+ozfft_status ozfft_plan_destroy(ozfft_plan* plan);
+
+const char* ozfft_status_string(ozfft_status s);
+const char* ozfft_last_error_string(void);
+
+/* Library build identity, e.g. "ozfft sm_100a <git-describe>". */
+const char* ozfft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OZFFT_H */

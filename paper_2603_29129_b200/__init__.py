@@ -1,0 +1,244 @@
+"""paper_2603_29129_b200 -- fp64-accurate DFT of any length from 32-bit NTTs on B200.
+
+Thin ctypes binding over libozfft.so, whose C ABI is declared in include/ozfft.h.
+Argument marshalling only: every step of the transform runs in the library's sm_100a
+kernels.  PyTorch provides device memory (the plan's persistent and workspace
+buffers are torch.uint8 tensors) and streams.  There is no CPU fallback: importing
+this package without the built library, or using it without a CUDA device, raises.
+
+    import torch, paper_2603_29129_b200 as oz
+    plan = oz.Plan(n=1 << 18, batch=16)            # K=3, L=3, paper primes
+    y = plan.forward(x)                            # x: cuda complex128 [16, n]
+    x2 = plan.inverse(y)
+
+Method: arXiv 2603.29129 (Bluestein + Ozaki split + two-prime NTT + CRT); see
+DESIGN.md and the header for citations.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libozfft.so")
+
+P0 = 2130706433
+P1 = 2113929217
+
+_STATUS = {0: "OZFFT_OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED_LENGTH", 3: "BAD_PRIMES",
+           4: "ALPHA", 5: "NOT_BOUND", 6: "MISALIGNED", 7: "CUDA", 8: "SHARD",
+           9: "BUFFER_TOO_SMALL"}
+
+
+class OzfftError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"ozfft {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [("n", C.c_int64), ("batch", C.c_int64), ("K", C.c_int32), ("L", C.c_int32),
+                ("p0", C.c_uint32), ("p1", C.c_uint32), ("device", C.c_int32),
+                ("reserved", C.c_int32), ("max_workspace_bytes", C.c_uint64)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("n", C.c_int64), ("m", C.c_int64), ("batch", C.c_int64), ("chunk", C.c_int64),
+                ("K", C.c_int32), ("L", C.c_int32), ("alpha", C.c_int32), ("rho", C.c_int32),
+                ("log2_rows", C.c_int32), ("log2_cols", C.c_int32),
+                ("persistent_bytes", C.c_uint64), ("workspace_bytes", C.c_uint64),
+                ("cached_ntts", C.c_int32), ("reserved", C.c_int32)]
+
+
+class ExecStats(C.Structure):
+    _fields_ = [("k", C.c_int32 * 4), ("fwd_ntts", C.c_int64), ("inv_ntts", C.c_int64),
+                ("cached_ntts", C.c_int64), ("groups", C.c_int64), ("nonfinite", C.c_int64),
+                ("flags", C.c_uint32), ("reserved", C.c_int32)]
+
+
+class Taps(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in ("digits", "E", "kv", "X", "sched", "Z", "res", "crt", "W")]
+
+
+# Symbols declared in include/ozfft.h (checked by tests/test_abi.py without a GPU).
+EXPORTS = ["ozfft_plan_create", "ozfft_plan_get_info", "ozfft_plan_bind", "ozfft_execute",
+           "ozfft_execute_host", "ozfft_execute_taps", "ozfft_last_stats",
+           "ozfft_shard_residue_bytes", "ozfft_shard_partial", "ozfft_shard_finish",
+           "ozfft_plan_destroy", "ozfft_status_string", "ozfft_last_error_string",
+           "ozfft_version"]
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """Load libozfft.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not found: run `python -m paper_2603_29129_b200.build` "
+                          "(or __graft_entry__.build()); ozfft has no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64
+    L.ozfft_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(vp)]
+    L.ozfft_plan_get_info.argtypes = [vp, C.POINTER(PlanInfo)]
+    L.ozfft_plan_bind.argtypes = [vp, vp, C.c_size_t, vp, C.c_size_t, vp]
+    L.ozfft_execute.argtypes = [vp, vp, vp, i32, vp]
+    L.ozfft_execute_host.argtypes = [vp, vp, vp, i32, vp]
+    L.ozfft_execute_taps.argtypes = [vp, vp, vp, i32, vp, C.POINTER(Taps)]
+    L.ozfft_last_stats.argtypes = [vp, C.POINTER(ExecStats), vp]
+    L.ozfft_shard_residue_bytes.argtypes = [vp]
+    L.ozfft_shard_residue_bytes.restype = u64
+    L.ozfft_shard_partial.argtypes = [vp, i32, i32, vp, i32, vp, vp]
+    L.ozfft_shard_finish.argtypes = [vp, vp, vp, i32, vp]
+    L.ozfft_plan_destroy.argtypes = [vp]
+    for f in ("ozfft_plan_create", "ozfft_plan_get_info", "ozfft_plan_bind", "ozfft_execute",
+              "ozfft_execute_host", "ozfft_execute_taps", "ozfft_last_stats",
+              "ozfft_shard_partial", "ozfft_shard_finish", "ozfft_plan_destroy"):
+        getattr(L, f).restype = C.c_int
+    L.ozfft_status_string.argtypes = [C.c_int]
+    L.ozfft_status_string.restype = C.c_char_p
+    L.ozfft_last_error_string.argtypes = []
+    L.ozfft_last_error_string.restype = C.c_char_p
+    L.ozfft_version.argtypes = []
+    L.ozfft_version.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise OzfftError(status, load_library().ozfft_last_error_string().decode())
+
+
+def version() -> str:
+    return load_library().ozfft_version().decode()
+
+
+def _stream_ptr(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Plan:
+    """Plan for `batch` complex fp64 DFTs of length n (any n, 1 <= n <= 2^19).
+
+    K: split cap per real vector; L: NTT-domain accumulation bound
+    (P:940-946).  p0, p1: NTT primes (default: the paper's).
+    """
+
+    def __init__(self, n: int, batch: int = 1, K: int = 3, L: int = 3, p0: int = 0, p1: int = 0,
+                 device=None, max_workspace_bytes: int = 0, stream=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("ozfft needs a CUDA device (sm_100a); there is no CPU fallback")
+        self._lib = load_library()
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.device = dev
+        d = PlanDesc(n=n, batch=batch, K=K, L=L, p0=p0, p1=p1, device=dev.index or 0,
+                     reserved=0, max_workspace_bytes=max_workspace_bytes)
+        h = C.c_void_p()
+        _check(self._lib.ozfft_plan_create(C.byref(d), C.byref(h)))
+        self._h = h
+        info = PlanInfo()
+        _check(self._lib.ozfft_plan_get_info(h, C.byref(info)))
+        self.n, self.batch, self.K, self.L = n, batch, info.K, info.L
+        self.m, self.alpha, self.rho, self.chunk = info.m, info.alpha, info.rho, info.chunk
+        self.log2_rows, self.log2_cols = info.log2_rows, info.log2_cols
+        with torch.cuda.device(dev):
+            self.persistent = torch.empty(max(info.persistent_bytes, 256), dtype=torch.uint8, device=dev)
+            self.workspace = torch.empty(max(info.workspace_bytes, 256), dtype=torch.uint8, device=dev)
+            _check(self._lib.ozfft_plan_bind(h, self.persistent.data_ptr(), self.persistent.numel(),
+                                             self.workspace.data_ptr(), self.workspace.numel(),
+                                             _stream_ptr(stream)))
+        info2 = PlanInfo()
+        _check(self._lib.ozfft_plan_get_info(h, C.byref(info2)))
+        self.cached_ntts = info2.cached_ntts
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.ozfft_plan_destroy(h)
+            self._h = None
+
+    # ------------------------------------------------------------------ execution
+    def _check_io(self, x: torch.Tensor, out: torch.Tensor | None):
+        if x.device != self.device or x.dtype != torch.complex128 or not x.is_contiguous():
+            raise ValueError("input must be a contiguous complex128 tensor on the plan's device")
+        if x.numel() != self.batch * self.n:
+            raise ValueError(f"input must hold batch*n = {self.batch * self.n} elements")
+        if out is None:
+            out = torch.empty_like(x)
+        elif out.device != self.device or out.dtype != torch.complex128 or not out.is_contiguous() \
+                or out.numel() != x.numel():
+            raise ValueError("out must match the input")
+        return out
+
+    def execute(self, x: torch.Tensor, direction: int = -1, out=None, stream=None) -> torch.Tensor:
+        out = self._check_io(x, out)
+        _check(self._lib.ozfft_execute(self._h, x.data_ptr(), out.data_ptr(), direction,
+                                       _stream_ptr(stream)))
+        return out
+
+    def forward(self, x, out=None, stream=None):
+        """y = DFT(x), omega_n = e^{-2 pi i/n} (eq:dft)."""
+        return self.execute(x, -1, out, stream)
+
+    def inverse(self, y, out=None, stream=None):
+        """x = DFT^{-1}(y) = conj(DFT(conj(y)))/n (eq:idft P:158-160; ruling 16)."""
+        return self.execute(y, +1, out, stream)
+
+    def execute_host(self, x_host: torch.Tensor, direction: int = -1, out_host=None, stream=None):
+        """End-to-end call on HOST buffers (pinned CPU complex128 tensors): H2D, pipeline, D2H."""
+        if x_host.device.type != "cpu" or x_host.dtype != torch.complex128 or not x_host.is_contiguous():
+            raise ValueError("x_host must be a contiguous CPU complex128 tensor")
+        if out_host is None:
+            out_host = torch.empty_like(x_host, pin_memory=x_host.is_pinned())
+        with torch.cuda.device(self.device):
+            _check(self._lib.ozfft_execute_host(self._h, x_host.data_ptr(), out_host.data_ptr(),
+                                                direction, _stream_ptr(stream)))
+        return out_host
+
+    def execute_taps(self, x: torch.Tensor, direction: int = -1, stream=None):
+        """Test-only: run once and return every stage output in the oracle's layout."""
+        B, n, m, K, L = self.batch, self.n, self.m, self.K, self.L
+        G = K * K
+        stride = 1 + G * (2 + 2 * L)
+        dev = self.device
+        z = lambda *s, dt: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
+        t = dict(digits=z(B, 2, K, n, dt=torch.int32), E=z(B, 2, K, dt=torch.int32),
+                 kv=z(B, 2, dt=torch.int32), X=z(B, 2, K, 2, m, dt=torch.int32),
+                 sched=z(B, 4, stride, dt=torch.int32), Z=z(B, 4, G, 2, m, dt=torch.int32),
+                 res=z(B, 4, G, 2, n, dt=torch.int32), crt=z(B, 4, G, n, dt=torch.int64),
+                 W=z(2, K, 2, m, dt=torch.int32))
+        tp = Taps(*[t[f].data_ptr() for f, _ in Taps._fields_])
+        out = torch.empty_like(x)
+        _check(self._lib.ozfft_execute_taps(self._h, x.data_ptr(), out.data_ptr(), direction,
+                                            _stream_ptr(stream), C.byref(tp)))
+        torch.cuda.synchronize(dev)
+        for k in ("X", "Z", "res", "W"):  # uint32 payloads carried in int32 tensors
+            t[k] = t[k].to(torch.int64) & 0xFFFFFFFF
+        return out, t
+
+    def stats(self, stream=None) -> dict:
+        s = ExecStats()
+        _check(self._lib.ozfft_last_stats(self._h, C.byref(s), _stream_ptr(stream)))
+        return dict(k=list(s.k), fwd_ntts=s.fwd_ntts, inv_ntts=s.inv_ntts,
+                    cached_ntts=s.cached_ntts, groups=s.groups, nonfinite=s.nonfinite,
+                    flags=s.flags)
+
+    # ------------------------------------------------------------------ sharding
+    def shard_residue_bytes(self) -> int:
+        return int(self._lib.ozfft_shard_residue_bytes(self._h))
+
+    def shard_partial(self, x: torch.Tensor, shard: int, nshards: int, residues: torch.Tensor,
+                      direction: int = -1, stream=None):
+        _check(self._lib.ozfft_shard_partial(self._h, shard, nshards, x.data_ptr(), direction,
+                                             residues.data_ptr(), _stream_ptr(stream)))
+
+    def shard_finish(self, residues: torch.Tensor, out: torch.Tensor, direction: int = -1,
+                     stream=None):
+        _check(self._lib.ozfft_shard_finish(self._h, residues.data_ptr(), out.data_ptr(),
+                                            direction, _stream_ptr(stream)))
+        return out

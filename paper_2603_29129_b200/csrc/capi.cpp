@@ -1,0 +1,404 @@
+// capi.cpp -- the extern "C" boundary of ozfft (declared in include/ozfft.h).
+// Validation, plan sizing/memory layout, chunked execution and statistics.  All
+// compute is in kernels.cu; there is no CPU fallback anywhere in this library.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.h"
+
+#ifndef OZFFT_GIT
+#define OZFFT_GIT "dev"
+#endif
+
+struct ozfft_plan : ozfft::Plan {};
+
+namespace ozfft {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+static ozfft_status fail(ozfft_status s, const std::string& msg) {
+  set_error(msg);
+  return s;
+}
+
+static bool is_prime_u32(uint64_t p) {
+  if (p < 2) return false;
+  for (uint64_t d = 2; d * d <= p; ++d)
+    if (p % d == 0) return false;
+  return true;
+}
+static int two_adicity(uint64_t v) {
+  int a = 0;
+  while (v && !(v & 1)) { v >>= 1; ++a; }
+  return a;
+}
+// alpha = floor((log2(p0 p1 / 2) - log2(L n)) / 2) (n = DFT length, ruling 2):
+// the largest a with 2 L n 4^a < p0 p1, evaluated in exact 128-bit integers.
+static int compute_alpha(int64_t n, int64_t L, uint32_t p0, uint32_t p1) {
+  const unsigned __int128 P = (unsigned __int128)p0 * p1;
+  int best = 0;
+  for (int a = 1; a < 62; ++a) {
+    unsigned __int128 v = (unsigned __int128)2 * (uint64_t)L * (uint64_t)n;
+    bool over = false;
+    for (int i = 0; i < a && !over; ++i) {
+      v <<= 2;
+      if (v >= P) over = true;
+    }
+    if (over) break;
+    best = a;
+  }
+  return best;
+}
+
+static uint64_t align256(uint64_t v) { return (v + 255) & ~(uint64_t)255; }
+
+static void layout(Plan& pl) {
+  const int64_t n = pl.n, m = pl.m, K = pl.K, L = pl.L, G = K * K;
+  // persistent
+  uint64_t o = 0;
+  pl.poff.chirp = o; o = align256(o + (uint64_t)n * 16);
+  pl.poff.tw = o;    o = align256(o + (uint64_t)4 * m * 8);
+  pl.poff.W = o;     o = align256(o + std::max<uint64_t>((uint64_t)4 * K * m * 8, (uint64_t)m * 16));
+  pl.poff.wsplit = o; o = align256(o + (uint64_t)(2 + 2 * K) * 4);
+  pl.poff.end = o;
+  pl.persistent_bytes = o;
+  // workspace: per-transform bytes of the chunked region
+  const bool two = pl.logR > 0;
+  const uint64_t per = (uint64_t)2 * K * 8 + (uint64_t)8 * K * n +
+                       (two ? (uint64_t)16 * K * m + (uint64_t)32 * G * m : 0) +
+                       (uint64_t)32 * G * n + (uint64_t)32 * n;
+  int64_t chunk = (int64_t)std::max<uint64_t>(1, pl.max_ws / std::max<uint64_t>(per, 1));
+  chunk = std::min<int64_t>(chunk, pl.batch);
+  pl.chunk = chunk;
+  o = 0;
+  pl.woff.stats = o;  o = align256(o + (uint64_t)pl.batch * stats_stride(K) * 4);
+  pl.woff.sched = o;  o = align256(o + (uint64_t)pl.batch * 4 * sched_stride(K, L) * 4);
+  pl.woff.mu = o;     o = align256(o + (uint64_t)chunk * 2 * K * 8);
+  pl.woff.digits = o; o = align256(o + (uint64_t)chunk * 2 * K * n * 4);
+  pl.woff.Y = o;      o = align256(o + (two ? (uint64_t)chunk * 4 * K * m * 4 : 0));
+  pl.woff.G = o;      o = align256(o + (two ? (uint64_t)chunk * 8 * G * m * 4 : 0));
+  pl.woff.res = o;    o = align256(o + (uint64_t)chunk * 8 * G * n * 4);
+  pl.woff.io_in = o;  o = align256(o + (uint64_t)chunk * n * 16);
+  pl.woff.io_out = o; o = align256(o + (uint64_t)chunk * n * 16);
+  pl.woff.end = o;
+  pl.workspace_bytes = o;
+}
+
+static ozfft_status check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(OZFFT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return OZFFT_OK;
+}
+
+}  // namespace ozfft
+
+using namespace ozfft;
+
+extern "C" {
+
+const char* ozfft_status_string(ozfft_status s) {
+  switch (s) {
+    case OZFFT_OK: return "OZFFT_OK";
+    case OZFFT_ERR_INVALID_ARGUMENT: return "OZFFT_ERR_INVALID_ARGUMENT";
+    case OZFFT_ERR_UNSUPPORTED_LENGTH: return "OZFFT_ERR_UNSUPPORTED_LENGTH";
+    case OZFFT_ERR_BAD_PRIMES: return "OZFFT_ERR_BAD_PRIMES";
+    case OZFFT_ERR_ALPHA: return "OZFFT_ERR_ALPHA";
+    case OZFFT_ERR_NOT_BOUND: return "OZFFT_ERR_NOT_BOUND";
+    case OZFFT_ERR_MISALIGNED: return "OZFFT_ERR_MISALIGNED";
+    case OZFFT_ERR_CUDA: return "OZFFT_ERR_CUDA";
+    case OZFFT_ERR_SHARD: return "OZFFT_ERR_SHARD";
+    case OZFFT_ERR_BUFFER_TOO_SMALL: return "OZFFT_ERR_BUFFER_TOO_SMALL";
+  }
+  return "OZFFT_ERR_UNKNOWN";
+}
+
+const char* ozfft_last_error_string(void) { return g_err.c_str(); }
+
+const char* ozfft_version(void) { return "ozfft sm_100a " OZFFT_GIT; }
+
+ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
+  if (!d || !out) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null descriptor or output pointer");
+  *out = nullptr;
+  ozfft_plan_desc desc = *d;
+  if (desc.K == 0) desc.K = 3;
+  if (desc.L == 0) desc.L = 3;
+  if (desc.p0 == 0) desc.p0 = 2130706433u;
+  if (desc.p1 == 0) desc.p1 = 2113929217u;
+  if (desc.max_workspace_bytes == 0) desc.max_workspace_bytes = 16ull << 30;
+  if (desc.n < 1 || desc.batch < 1)
+    return fail(OZFFT_ERR_INVALID_ARGUMENT, "n and batch must be >= 1");
+  if (desc.K < 1 || desc.K > kMaxK || desc.L < 1 || desc.L > kMaxL)
+    return fail(OZFFT_ERR_INVALID_ARGUMENT, "K and L must be in [1, 8]");
+  if (desc.n > (1ll << 23)) return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "n > 2^23");
+  const uint32_t p0 = desc.p0, p1 = desc.p1;
+  if (p0 == p1 || p0 >= (1u << 31) || p1 >= (1u << 31) || !is_prime_u32(p0) || !is_prime_u32(p1) ||
+      (unsigned __int128)p0 * p1 >= ((unsigned __int128)1 << 62))
+    return fail(OZFFT_ERR_BAD_PRIMES, "primes must be distinct, < 2^31, with p0*p1 < 2^62");
+  ozfft_plan* pl = new (std::nothrow) ozfft_plan();
+  if (!pl) return fail(OZFFT_ERR_INVALID_ARGUMENT, "out of host memory");
+  pl->n = desc.n;
+  pl->batch = desc.batch;
+  pl->K = desc.K;
+  pl->L = desc.L;
+  pl->p[0] = p0;
+  pl->p[1] = p1;
+  pl->max_ws = desc.max_workspace_bytes;
+  int64_t m = 1;
+  while (m < 2 * desc.n - 1) m <<= 1;  // Bluestein length, N >= 2n-1
+  pl->m = m;
+  int logm = 0;
+  while ((1ll << logm) < m) ++logm;
+  pl->logm = logm;
+  if (logm > std::min(two_adicity(p0 - 1ull), two_adicity(p1 - 1ull))) {
+    delete pl;
+    return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "m exceeds the primes' two-adicity");
+  }
+  if (logm > 20) {
+    delete pl;
+    return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "this build supports m <= 2^20 (n <= 2^19)");
+  }
+  // NTT decomposition: one pass up to m = 2^12, else rows of C = 2^11 (2^12 at m = 2^20)
+  pl->logC = logm <= 12 ? logm : std::max(11, logm - 8);
+  pl->logR = logm - pl->logC;
+  pl->alpha = compute_alpha(desc.n, desc.L, p0, p1);
+  if (pl->alpha < 1) {
+    delete pl;
+    return fail(OZFFT_ERR_ALPHA, "alpha < 1");
+  }
+  pl->rho = 53 - pl->alpha;
+  int dev = desc.device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  }
+  pl->device = dev;
+  ozfft_status s = build_plan_tables(*pl);
+  if (s) {
+    delete pl;
+    return s;
+  }
+  layout(*pl);
+  *out = pl;
+  return OZFFT_OK;
+}
+
+ozfft_status ozfft_plan_get_info(const ozfft_plan* pl, ozfft_plan_info* info) {
+  if (!pl || !info) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->n = pl->n;
+  info->m = pl->m;
+  info->batch = pl->batch;
+  info->chunk = pl->chunk;
+  info->K = pl->K;
+  info->L = pl->L;
+  info->alpha = pl->alpha;
+  info->rho = pl->rho;
+  info->log2_rows = pl->logR;
+  info->log2_cols = pl->logC;
+  info->persistent_bytes = pl->persistent_bytes;
+  info->workspace_bytes = pl->workspace_bytes;
+  info->cached_ntts = pl->bound ? 2 * (pl->kw[0] + pl->kw[1]) : 4 * pl->K;
+  return OZFFT_OK;
+}
+
+ozfft_status ozfft_plan_bind(ozfft_plan* pl, void* persistent, size_t pbytes, void* workspace,
+                             size_t wbytes, void* stream) {
+  if (!pl || !persistent || !workspace) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null argument");
+  if (((uintptr_t)persistent & 255) || ((uintptr_t)workspace & 255))
+    return fail(OZFFT_ERR_MISALIGNED, "plan buffers must be 256-byte aligned");
+  if (pbytes < pl->persistent_bytes || wbytes < pl->workspace_bytes)
+    return fail(OZFFT_ERR_BUFFER_TOO_SMALL, "persistent/workspace smaller than plan_get_info");
+  ozfft_status s = check_cuda(cudaSetDevice(pl->device), "cudaSetDevice");
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  pl->pers = (uint8_t*)persistent;
+  pl->ws = (uint8_t*)workspace;
+  const int64_t m = pl->m;
+  s = check_cuda(cudaMemcpyAsync(pl->pers + pl->poff.chirp, pl->chirp.data(),
+                                 sizeof(double) * 2 * pl->n, cudaMemcpyHostToDevice, st),
+                 "upload chirp");
+  for (int q = 0; q < 2 && !s; ++q)
+    for (int dir = 0; dir < 2 && !s; ++dir)
+      s = check_cuda(cudaMemcpyAsync(pl->pers + pl->poff.tw + (uint64_t)(q * 2 + dir) * m * 8,
+                                     pl->tw[q][dir].data(), (size_t)m * 8, cudaMemcpyHostToDevice, st),
+                     "upload twiddles");
+  // omega~* staged in the W area; launch_plan_precompute replaces it by the W spectra
+  if (!s)
+    s = check_cuda(cudaMemcpyAsync(pl->pers + pl->poff.W, pl->wstar.data(), (size_t)m * 16,
+                                   cudaMemcpyHostToDevice, st),
+                   "upload omega~*");
+  if (!s) s = check_cuda(cudaMemsetAsync(pl->ws, 0, pl->woff.mu, st), "clear stats");
+  if (!s) s = launch_plan_precompute(*pl, stream);
+  if (s) return s;
+  pl->bound = true;
+  return OZFFT_OK;
+}
+
+static ozfft_status check_exec(const ozfft_plan* pl, const void* in, const void* out, int dir) {
+  if (!pl) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null plan");
+  if (!pl->bound) return fail(OZFFT_ERR_NOT_BOUND, "plan not bound");
+  if (!in || !out) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null buffer");
+  if (dir != -1 && dir != 1) return fail(OZFFT_ERR_INVALID_ARGUMENT, "direction must be -1 or +1");
+  if (((uintptr_t)in & 15) || ((uintptr_t)out & 15))
+    return fail(OZFFT_ERR_MISALIGNED, "buffers must be 16-byte aligned");
+  return OZFFT_OK;
+}
+
+ozfft_status ozfft_execute(const ozfft_plan* pl, const void* in, void* out, int direction,
+                           void* stream) {
+  ozfft_status s = check_exec(pl, in, out, direction);
+  if (s) return s;
+  const int64_t n = pl->n;
+  for (int64_t b0 = 0; b0 < pl->batch; b0 += pl->chunk) {
+    ExecArgs a{};
+    a.nb = std::min<int64_t>(pl->chunk, pl->batch - b0);
+    a.in = reinterpret_cast<const double*>(in) + 2 * b0 * n;
+    a.out = reinterpret_cast<double*>(out) + 2 * b0 * n;
+    a.b0 = b0;
+    a.direction = direction;
+    a.unit_mask = 0xFF;
+    a.finish = true;
+    a.taps = nullptr;
+    s = launch_execute(*pl, a, stream);
+    if (s) return s;
+  }
+  const_cast<ozfft_plan*>(pl)->last_batch = pl->batch;
+  return OZFFT_OK;
+}
+
+ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* out, int direction,
+                                void* stream) {
+  ozfft_status s = check_exec(pl, in, out, direction);
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = pl->n;
+  double* din = reinterpret_cast<double*>(pl->ws + pl->woff.io_in);
+  double* dout = reinterpret_cast<double*>(pl->ws + pl->woff.io_out);
+  for (int64_t b0 = 0; b0 < pl->batch; b0 += pl->chunk) {
+    const int64_t nb = std::min<int64_t>(pl->chunk, pl->batch - b0);
+    const size_t bytes = (size_t)nb * n * 16;
+    s = check_cuda(cudaMemcpyAsync(din, in + 2 * b0 * n, bytes, cudaMemcpyHostToDevice, st), "H2D");
+    if (s) return s;
+    ExecArgs a{};
+    a.nb = nb;
+    a.in = din;
+    a.out = dout;
+    a.b0 = b0;
+    a.direction = direction;
+    a.unit_mask = 0xFF;
+    a.finish = true;
+    s = launch_execute(*pl, a, stream);
+    if (s) return s;
+    s = check_cuda(cudaMemcpyAsync(out + 2 * b0 * n, dout, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    if (s) return s;
+  }
+  const_cast<ozfft_plan*>(pl)->last_batch = pl->batch;
+  return check_cuda(cudaStreamSynchronize(st), "execute_host sync");
+}
+
+ozfft_status ozfft_execute_taps(const ozfft_plan* pl, const void* in, void* out, int direction,
+                                void* stream, const ozfft_taps* taps) {
+  ozfft_status s = check_exec(pl, in, out, direction);
+  if (s) return s;
+  if (pl->chunk != pl->batch)
+    return fail(OZFFT_ERR_INVALID_ARGUMENT, "taps need the whole batch in one chunk");
+  ExecArgs a{};
+  a.nb = pl->batch;
+  a.in = reinterpret_cast<const double*>(in);
+  a.out = reinterpret_cast<double*>(out);
+  a.b0 = 0;
+  a.direction = direction;
+  a.unit_mask = 0xFF;
+  a.finish = true;
+  a.taps = taps;
+  s = launch_execute(*pl, a, stream);
+  const_cast<ozfft_plan*>(pl)->last_batch = pl->batch;
+  return s;
+}
+
+ozfft_status ozfft_last_stats(const ozfft_plan* pl, ozfft_exec_stats* out, void* stream) {
+  if (!pl || !out) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null argument");
+  if (!pl->bound) return fail(OZFFT_ERR_NOT_BOUND, "plan not bound");
+  std::memset(out, 0, sizeof(*out));
+  out->k[2] = pl->kw[0];
+  out->k[3] = pl->kw[1];
+  out->cached_ntts = 2 * (pl->kw[0] + pl->kw[1]);
+  const int64_t B = pl->last_batch;
+  if (B == 0) return OZFFT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int K = pl->K, L = pl->L;
+  std::vector<int32_t> hs((size_t)B * stats_stride(K));
+  std::vector<int32_t> hsched((size_t)B * 4 * sched_stride(K, L));
+  ozfft_status s = check_cuda(cudaMemcpyAsync(hs.data(), pl->ws + pl->woff.stats, hs.size() * 4,
+                                              cudaMemcpyDeviceToHost, st), "stats D2H");
+  if (!s) s = check_cuda(cudaMemcpyAsync(hsched.data(), pl->ws + pl->woff.sched, hsched.size() * 4,
+                                         cudaMemcpyDeviceToHost, st), "sched D2H");
+  if (!s) s = check_cuda(cudaStreamSynchronize(st), "stats sync");
+  if (s) return s;
+  for (int64_t b = 0; b < B; ++b) {
+    const int32_t* r = hs.data() + b * stats_stride(K);
+    if (b == 0) {
+      out->k[0] = r[0];
+      out->k[1] = r[1];
+    }
+    if (r[2 + 2 * K] & 1) {
+      out->nonfinite++;
+      out->flags |= 1u;
+      continue;
+    }
+    out->fwd_ntts += 2 * (r[0] + r[1]);
+    for (int cv = 0; cv < 4; ++cv) out->groups += hsched[(b * 4 + cv) * sched_stride(K, L)];
+  }
+  out->inv_ntts = 2 * out->groups;
+  return OZFFT_OK;
+}
+
+uint64_t ozfft_shard_residue_bytes(const ozfft_plan* pl) {
+  if (!pl) return 0;
+  return (uint64_t)8 * pl->K * pl->K * pl->n * 4;
+}
+
+ozfft_status ozfft_shard_partial(const ozfft_plan* pl, int shard, int nshards, const void* in,
+                                 int direction, void* residues_out, void* stream) {
+  ozfft_status s = check_exec(pl, in, residues_out, direction);
+  if (s) return s;
+  if (nshards < 1 || 8 % nshards != 0 || shard < 0 || shard >= nshards)
+    return fail(OZFFT_ERR_SHARD, "nshards must divide 8 and 0 <= shard < nshards");
+  const int per = 8 / nshards;
+  uint32_t mask = 0;
+  for (int u = shard * per; u < (shard + 1) * per; ++u) mask |= 1u << u;
+  ExecArgs a{};
+  a.nb = 1;
+  a.in = reinterpret_cast<const double*>(in);
+  a.out = nullptr;
+  a.b0 = 0;
+  a.direction = direction;
+  a.unit_mask = mask;
+  a.finish = false;
+  s = launch_execute(*pl, a, stream);
+  if (s) return s;
+  // res layout [b=0][cv][q][G][n] == [unit = cv*2+q][G][n]; copy this shard's units
+  const size_t unit_bytes = (size_t)pl->K * pl->K * pl->n * 4;
+  return check_cuda(cudaMemcpyAsync((uint8_t*)residues_out + (size_t)shard * per * unit_bytes,
+                                    pl->ws + pl->woff.res + (size_t)shard * per * unit_bytes,
+                                    per * unit_bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+                    "shard copy");
+}
+
+ozfft_status ozfft_shard_finish(const ozfft_plan* pl, const void* residues_all, void* out,
+                                int direction, void* stream) {
+  ozfft_status s = check_exec(pl, residues_all, out, direction);
+  if (s) return s;
+  return launch_finish_from_residues(*pl, reinterpret_cast<const uint32_t*>(residues_all),
+                                     reinterpret_cast<double*>(out), direction, stream);
+}
+
+ozfft_status ozfft_plan_destroy(ozfft_plan* pl) {
+  delete pl;
+  return OZFFT_OK;
+}
+
+}  // extern "C"

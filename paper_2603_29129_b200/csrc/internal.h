@@ -1,0 +1,87 @@
+// internal.h -- shared definitions of the ozfft CUDA library (not part of the ABI).
+// References "P:N" = /root/reference/PAPER.md line N.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ozfft.h"
+
+#ifdef __CUDACC__
+#define OZ_HD __host__ __device__
+#else
+#define OZ_HD
+#endif
+
+namespace ozfft {
+
+constexpr int kMaxK = 8;  // split cap per real vector (plan K <= kMaxK)
+constexpr int kMaxL = 8;  // accumulation bound (plan L <= kMaxL)
+
+// Real convolutions of the complex Bluestein convolution:
+// cv = 0 rr, 1 ii, 2 ir, 3 ri as (x' part a, omega~* part b).
+OZ_HD inline int conv_a(int cv) { return (cv == 1 || cv == 2) ? 1 : 0; }
+OZ_HD inline int conv_b(int cv) { return (cv == 1 || cv == 3) ? 1 : 0; }
+
+// Host-side plan (immutable after bind).
+struct Plan {
+  // descriptor-derived
+  int64_t n = 0, m = 0, batch = 0, chunk = 0;
+  int K = 3, L = 3, alpha = 0, rho = 0;
+  uint32_t p[2] = {0, 0};
+  int logm = 0, logC = 0, logR = 0;  // m = R * C
+  int device = 0;
+  uint64_t max_ws = 0;
+  // host tables (built at create)
+  std::vector<double> chirp;       // [n][2] = (C_j, S_j), omega(j) = C_j + i S_j
+  std::vector<double> wstar;       // [m][2] omega~* = ZeroPad_pm(conj(omega), m)
+  std::vector<uint32_t> tw[2][2];  // [prime][dir] -> [m][2] = (w, shoup) at T[h + j] = w_{2h}^{+-j}
+  uint32_t minv[2] = {0, 0};       // m^{-1} mod p
+  uint32_t p0inv_mod_p1 = 0;       // Garner constant
+  // sizes and layout
+  uint64_t persistent_bytes = 0, workspace_bytes = 0;
+  struct {
+    uint64_t chirp, tw, W, wsplit, end;
+  } poff{};
+  struct {
+    uint64_t stats, sched, mu, digits, Y, G, res, io_in, io_out, end;
+  } woff{};
+  // bound state
+  bool bound = false;
+  uint8_t* pers = nullptr;
+  uint8_t* ws = nullptr;
+  int kw[2] = {0, 0};
+  int32_t Ew[2][kMaxK] = {{0}};
+  int64_t last_batch = 0;  // transforms covered by the per-batch stats arrays
+};
+
+// Schedule row length per (transform, conv): ngroups + K*K groups of (cexp, npairs, L pairs)
+OZ_HD inline int sched_stride(int K, int L) { return 1 + K * K * (2 + 2 * L); }
+
+// Per-transform stats record in the workspace (int32 words).
+// [0..1] kv(re, im), [2..2+2K) E(re, im), [2+2K] flags (bit0 nonfinite), then mu bits (u64) separately.
+OZ_HD inline int stats_stride(int K) { return 4 + 2 * K; }
+
+void set_error(const std::string& msg);
+
+// plan_host.cpp
+ozfft_status build_plan_tables(Plan& pl);  // chirp, wstar, twiddles (host math)
+
+// kernels.cu launchers (all asynchronous on `stream`)
+struct ExecArgs {
+  const double* in;    // device complex [chunk][n]
+  double* out;         // device complex [chunk][n]
+  int64_t b0;          // index of the first transform of the chunk within the batch
+  int64_t nb;          // transforms in this chunk
+  int direction;       // -1 forward, +1 inverse
+  uint32_t unit_mask;  // bit (cv*2 + q): which (conv, prime) units to compute (0xFF = all)
+  bool finish;         // run CRT/recombine/post-chirp
+  const ozfft_taps* taps;
+};
+ozfft_status launch_plan_precompute(Plan& pl, void* stream);
+ozfft_status launch_execute(const Plan& pl, const ExecArgs& a, void* stream);
+ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, double* out,
+                                         int direction, void* stream);
+
+}  // namespace ozfft

@@ -1,0 +1,1120 @@
+// kernels.cu -- sm_100a kernels of the ozfft hot path (arXiv 2603.29129).
+//
+//   k_split_max      a1+a2  chirp premultiply in DD (Alg.4 l.473-474) + per-level
+//                           max |hi| for the Ozaki split (Alg.6 l.778/786, eq:ts-split-mu)
+//   k_split_digits   a2     int32 digits D = fl(fl(hi+sigma)-sigma) 2^(alpha-E)
+//                           (Alg.6 l.781-785) + Alg.8 flush schedule per real conv
+//   k_col_fwd        a3     residue lift + first log2(R) DIF stages of the length-m
+//                           forward NTT (eq:ntt P:248) on column tiles (stride C)
+//   k_row_fused      a3-a5  last log2(C) DIF stages of the 2K slice NTTs of one row,
+//                           pointwise products + NTT-domain accumulation of each
+//                           Alg.8 group (l.981-982), first log2(C) DIT stages of
+//                           its inverse NTT (l.973)
+//   k_col_inv        a5     last log2(R) DIT stages of the inverse NTT, natural
+//                           order, only indices j < n written
+//   k_crt_finish     a6+a7  Garner CRT (l.974), exact power-of-two scaling, DD
+//                           accumulation in flush order (l.975-976), complex combine
+//                           (P:1012-1019), post-chirp (Alg.4 l.480-484), fp64 output
+//
+// NTT arithmetic: canonical residues in [0,p), Shoup multiplication by precomputed
+// twiddles, branch-free conditional subtraction via unsigned min
+// (one VIADDMNMX on sm_100a).  The forward NTT is decimation-in-frequency from
+// natural order to bit-reversed order; the inverse is decimation-in-time from
+// bit-reversed to natural order, so the pointwise stage needs no permutation.
+// m^{-1} of eq:intt is folded into the cached W spectra.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "internal.h"
+
+namespace ozfft {
+
+// ============================================================== modular arithmetic
+__device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) {
+  const uint32_t s = a + b;  // a, b < p < 2^31
+  return min(s, s - p);
+}
+__device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) {
+  const uint32_t d = a + (p - b);
+  return min(d, d - p);
+}
+// a * w mod p for any a < 2^32, w = (w, floor(w 2^32 / p)) (Shoup)
+__device__ __forceinline__ uint32_t mul_shoup(uint32_t a, uint2 w, uint32_t p) {
+  const uint32_t q = __umulhi(a, w.y);
+  const uint32_t r = a * w.x - q * p;  // in [0, 2p)
+  return min(r, r - p);
+}
+
+// ============================================================== double-double (DD)
+// Fixed IEEE RN operation sequences (no contraction): must match the oracle bit for bit.
+__device__ __forceinline__ void two_prod(double a, double b, double& p, double& e) {
+  p = __dmul_rn(a, b);
+  e = __fma_rn(a, b, -p);
+}
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+// FastTwoSum, Alg.7
+__device__ __forceinline__ void fast_two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  e = __dsub_rn(b, __dsub_rn(s, a));
+}
+__device__ __forceinline__ void dd_add(double ah, double al, double bh, double bl, double& rh,
+                                       double& rl) {
+  double s, e, t, f;
+  two_sum(ah, bh, s, e);
+  two_sum(al, bl, t, f);
+  e = __dadd_rn(e, t);
+  fast_two_sum(s, e, s, e);
+  e = __dadd_rn(e, f);
+  fast_two_sum(s, e, rh, rl);
+}
+__device__ __forceinline__ void dd_mul_d(double ah, double al, double b, double& rh, double& rl) {
+  double p, e;
+  two_prod(ah, b, p, e);
+  e = __fma_rn(al, b, e);
+  fast_two_sum(p, e, rh, rl);
+}
+
+// ceil(log2(mu)) exactly from the bits of a positive finite double (ruling 8)
+__device__ __forceinline__ int ceil_log2_bits(unsigned long long u) {
+  const int eb = (int)(u >> 52);
+  const unsigned long long man = u & ((1ull << 52) - 1);
+  if (eb == 0) return (64 - __clzll((long long)(man - 1))) - 1074;  // subnormal
+  return man == 0 ? eb - 1023 : eb - 1022;
+}
+
+constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
+
+// ============================================================== split kernels
+struct SplitParams {
+  const double2* x;       // mode 0: input complex [nb][len]; mode 1: raw DD hi values [len]
+  const double2* chirp;   // [len] (C, S)
+  int64_t len;            // vector length (n for x', m for omega~*)
+  int mode;               // 0: x' = x (.) omega (conj on load if inverse); 1: raw (lo = 0)
+  int conj;               // inverse-direction wrapper (ruling 16)
+  int K, alpha, rho;
+  unsigned long long* mu; // [nb][2][K] max-|hi| bits per level
+  int32_t* digits;        // [nb][2][K][len]
+  int32_t* stats;         // [nb][stats_stride]
+  int32_t* sched;         // [nb][4][sched_stride] (nullptr: no schedule)
+  const int32_t* wsplit;  // kw[2], Ew[2][K] of omega~* (for the schedule)
+  int L;
+};
+
+__device__ __forceinline__ void load_xprime(const SplitParams& P, int64_t b, int64_t j, double& hr,
+                                            double& lr, double& hi, double& li) {
+  if (P.mode == 0) {
+    const double2 xv = P.x[b * P.len + j];
+    const double2 w = P.chirp[j];
+    const double xr = xv.x, xi = P.conj ? -xv.y : xv.y;
+    double p1, e1, p2, e2;
+    two_prod(xr, w.x, p1, e1);
+    two_prod(xi, w.y, p2, e2);
+    dd_add(p1, e1, -p2, -e2, hr, lr);
+    two_prod(xr, w.y, p1, e1);
+    two_prod(xi, w.x, p2, e2);
+    dd_add(p1, e1, p2, e2, hi, li);
+  } else {
+    const double2 wv = P.x[j];
+    hr = wv.x;
+    hi = wv.y;
+    lr = 0.0;
+    li = 0.0;
+  }
+}
+
+// One Ozaki extraction step on (h, l) with level exponent E (Alg.6 l.781-783).
+__device__ __forceinline__ int32_t split_step(double& h, double& l, int E, int alpha, int rho) {
+  const double sigma = scalbn(1.0, E + rho);
+  const double t = __dadd_rn(h, sigma);
+  const double d = __dsub_rn(t, sigma);
+  const int32_t D = __double2int_rz(__dmul_rn(d, scalbn(1.0, alpha - E)));
+  const double r = __dsub_rn(h, d);
+  fast_two_sum(r, l, h, l);
+  return D;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// Max |hi| over the transform at split level `level` (levels < level applied first).
+__global__ void __launch_bounds__(256) k_split_max(SplitParams P, int level) {
+  const int64_t b = blockIdx.y;
+  const unsigned long long* mub = P.mu + b * 2 * P.K;
+  int E[2][kMaxK];
+  int lv[2] = {level, level};  // levels already extracted (stop at the first mu == 0)
+  bool bad = false;
+  for (int v = 0; v < 2; ++v)
+    for (int k = 0; k < level; ++k) {
+      const unsigned long long u = mub[v * P.K + k];
+      if (u >= kInfBits) bad = true;
+      if (u == 0 && lv[v] == level) lv[v] = k;
+      E[v][k] = (u == 0 || u >= kInfBits) ? 0 : ceil_log2_bits(u);
+    }
+  if (bad) return;  // non-finite transform: nothing more to compute
+  unsigned long long m0 = 0, m1 = 0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P.len;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double h[2], l[2];
+    load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
+#pragma unroll
+    for (int v = 0; v < 2; ++v)  // a level with mu == 0 ended this part's split (Alg.6 l.780)
+      for (int k = 0; k < lv[v]; ++k) (void)split_step(h[v], l[v], E[v][k], P.alpha, P.rho);
+    const unsigned long long a0 = (unsigned long long)__double_as_longlong(fabs(h[0]));
+    const unsigned long long a1 = (unsigned long long)__double_as_longlong(fabs(h[1]));
+    m0 = a0 > m0 ? a0 : m0;  // NaN bits exceed +Inf bits: a NaN sticks
+    m1 = a1 > m1 ? a1 : m1;
+  }
+  __shared__ unsigned long long red[2][8];
+  m0 = warp_max_u64(m0);
+  m1 = warp_max_u64(m1);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { red[0][w] = m0; red[1][w] = m1; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    m0 = lane < nw ? red[0][lane] : 0;
+    m1 = lane < nw ? red[1][lane] : 0;
+    m0 = warp_max_u64(m0);
+    m1 = warp_max_u64(m1);
+    if (lane == 0) {
+      unsigned long long* dst = P.mu + b * 2 * P.K;
+      if (m0) atomicMax(&dst[0 * P.K + level], m0);
+      if (m1) atomicMax(&dst[1 * P.K + level], m1);
+    }
+  }
+}
+
+// Alg.8 flush schedule for one real convolution; writes the row layout
+// [ngroups, (cexp, npairs, s0, t0, ..., s_{L-1}, t_{L-1}) x K*K].
+__device__ void alg8_schedule(int kx, const int* sx, int ky, const int* sy, int K, int L,
+                              int32_t* row) {
+  const int stride = 1 + K * K * (2 + 2 * L);
+  for (int i = 0; i < stride; ++i) row[i] = 0;
+  if (kx <= 0 || ky <= 0) return;
+  int ng = 0;
+  int c = sx[kx - 1] + sy[ky - 1];
+  int l = 0;
+  int32_t* grp = row + 1;
+  grp[0] = c;
+  for (int k = kx + ky - 2; k >= 0; --k) {
+    const int s_lo = max(0, k - ky + 1), s_hi = min(kx - 1, k);
+    for (int s = s_lo; s <= s_hi; ++s) {
+      const int t = k - s;
+      const int e = sx[s] + sy[t];
+      if (l >= L || e != c) {  // flush the current group (l.972-979)
+        ++ng;
+        grp = row + 1 + ng * (2 + 2 * L);
+        c = e;
+        l = 0;
+        grp[0] = c;
+      }
+      grp[2 + 2 * l] = s;
+      grp[3 + 2 * l] = t;
+      ++l;
+      grp[1] = l;
+    }
+  }
+  row[0] = ng + 1;
+}
+
+// Digits for every level, per-transform stats and (block 0) the schedules.
+__global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
+  const int64_t b = blockIdx.y;
+  const unsigned long long* mub = P.mu + b * 2 * P.K;
+  int E[2][kMaxK];
+  int kv[2];
+  bool bad = false;
+  for (int v = 0; v < 2; ++v) {
+    kv[v] = P.K;
+    for (int k = 0; k < P.K; ++k) {
+      const unsigned long long u = mub[v * P.K + k];
+      if (u >= kInfBits) bad = true;
+      E[v][k] = (u == 0 || u >= kInfBits) ? 0 : ceil_log2_bits(u);
+      if (u == 0 && kv[v] == P.K) kv[v] = k;
+    }
+  }
+  // mu of level k is only meaningful while all previous levels were non-zero
+  for (int v = 0; v < 2; ++v)
+    for (int k = kv[v]; k < P.K; ++k) E[v][k] = 0;
+  if (bad) { kv[0] = 0; kv[1] = 0; }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int32_t* st = P.stats + b * stats_stride(P.K);
+    st[0] = kv[0];
+    st[1] = kv[1];
+    for (int v = 0; v < 2; ++v)
+      for (int k = 0; k < P.K; ++k) st[2 + v * P.K + k] = E[v][k];
+    st[2 + 2 * P.K] = bad ? 1 : 0;
+  }
+  if (P.sched && blockIdx.x == 0 && threadIdx.x < 4) {
+    const int cv = threadIdx.x;
+    const int a = conv_a(cv), bw = conv_b(cv);
+    int sx[kMaxK], sy[kMaxK];
+    const int kw = P.wsplit[bw];
+    for (int k = 0; k < P.K; ++k) {
+      sx[k] = P.alpha - E[a][k];                 // c = (u sigma)^-1 = 2^(alpha - E) (l.785)
+      sy[k] = P.alpha - P.wsplit[2 + bw * P.K + k];
+    }
+    alg8_schedule(bad ? 0 : kv[a], sx, kw, sy, P.K, P.L,
+                  P.sched + (b * 4 + cv) * sched_stride(P.K, P.L));
+  }
+  if (bad) return;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P.len;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double h[2], l[2];
+    load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j;
+      for (int k = 0; k < P.K; ++k) {
+        int32_t D = 0;
+        if (k < kv[v]) D = split_step(h[v], l[v], E[v][k], P.alpha, P.rho);
+        dv[k * P.len] = D;
+      }
+    }
+  }
+}
+
+// ============================================================== NTT building blocks
+// A group of 2^S registers x[k] holding global positions gbase + k*gstep, with
+// rmod = gbase mod gstep.  DIF stages h = gstep*2^(S-1) .. gstep (block length 2h):
+//   (u, v) -> (u + v, (u - v) * T[h + (pos mod h)]),  T[h + j] = w_{2h}^j.
+template <int S>
+__device__ __forceinline__ void dif_group(uint32_t* x, uint32_t rmod, uint32_t gstep,
+                                          const uint2* __restrict__ T, uint32_t p) {
+#pragma unroll
+  for (int st = S - 1; st >= 0; --st) {
+    const int d = 1 << st;
+    const uint32_t h = gstep << st;
+#pragma unroll
+    for (int k = 0; k < (1 << S); ++k) {
+      if (k & d) continue;
+      const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);
+      const uint32_t u = x[k], v = x[k + d];
+      x[k] = add_mod(u, v, p);
+      x[k + d] = mul_shoup(u + (p - v), w, p);
+    }
+  }
+}
+// DIT stages h = gstep .. gstep*2^(S-1): v' = v * Tinv[h + (pos mod h)]; (u + v', u - v')
+template <int S>
+__device__ __forceinline__ void dit_group(uint32_t* x, uint32_t rmod, uint32_t gstep,
+                                          const uint2* __restrict__ T, uint32_t p) {
+#pragma unroll
+  for (int st = 0; st < S; ++st) {
+    const int d = 1 << st;
+    const uint32_t h = gstep << st;
+#pragma unroll
+    for (int k = 0; k < (1 << S); ++k) {
+      if (k & d) continue;
+      const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);
+      const uint32_t u = x[k];
+      const uint32_t v = mul_shoup(x[k + d], w, p);
+      x[k] = add_mod(u, v, p);
+      x[k + d] = sub_mod(u, v, p);
+    }
+  }
+}
+
+template <bool INV, int S>
+__device__ __forceinline__ void groups_compute(uint32_t* x, int gpt, int tv, int Tv, int logstep,
+                                               uint32_t gb_mod, uint32_t gs,
+                                               const uint2* __restrict__ T, uint32_t p) {
+  const uint32_t step = 1u << logstep;
+#pragma unroll
+  for (int u = 0; u < 16 / (1 << S); ++u) {
+    if (u < gpt) {
+      const uint32_t g = (uint32_t)(tv + u * Tv);
+      const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
+      if (INV)
+        dit_group<S>(x + u * (1 << S), rmod, step * gs, T, p);
+      else
+        dif_group<S>(x + u * (1 << S), rmod, step * gs, T, p);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t pad_idx(uint32_t e) { return e + (e >> 4); }
+
+// Length-N (N = 2^logN) sub-transform executed cooperatively by Tv threads (thread
+// index tv), 16 elements per thread per round (N >= 16) in rounds of <= 4 radix-2
+// stages, with shared memory (padded, interleave Cb) between rounds.
+//   INV = false: DIF stages len = N .. 2 (rounds from the top);
+//   INV = true : DIT stages len = 2 .. N.
+// Element e has global position gbase_vec + e*gs; gb_mod = gbase_vec mod (gs*step) for
+// every step used (0 for rows, the column index for columns).  load_first(e) gives the
+// round-0 input; store_last(e, v) consumes the final values.  `sm` must be free for
+// writes (caller-synchronised) on entry.
+template <bool INV, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt(int logN, int tv, int Tv, uint32_t* __restrict__ sm,
+                                        int Cb, uint32_t gb_mod, uint32_t gs,
+                                        const uint2* __restrict__ T, uint32_t p,
+                                        LoadF&& load_first, StoreF&& store_last) {
+  int rS[8], rLB[8];  // stages and log2(block length) per round
+  int nr = 0;
+  for (int lb = logN; lb > 0;) {
+    const int S = lb < 4 ? lb : 4;
+    rS[nr] = S;
+    rLB[nr] = lb;
+    ++nr;
+    lb -= S;
+  }
+  if (INV) {
+    for (int i = 0; i < nr / 2; ++i) {
+      int t = rS[i]; rS[i] = rS[nr - 1 - i]; rS[nr - 1 - i] = t;
+      t = rLB[i]; rLB[i] = rLB[nr - 1 - i]; rLB[nr - 1 - i] = t;
+    }
+  }
+  uint32_t x[16];
+  if (nr == 0) {  // N == 1: identity
+    if (tv == 0) store_last(0u, load_first(0u));
+    return;
+  }
+  for (int r = 0; r < nr; ++r) {
+    const int S = rS[r], lb = rLB[r];
+    const int logstep = lb - S;
+    const int cnt = logN >= 4 ? 16 : (1 << logN);
+    const int gpt = cnt >> S;
+    // gather
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < cnt) {
+        const uint32_t g = (uint32_t)(tv + (i >> S) * Tv);
+        const uint32_t k = (uint32_t)(i & ((1 << S) - 1));
+        const uint32_t e = ((g >> logstep) << lb) + (g & ((1u << logstep) - 1)) + (k << logstep);
+        x[i] = (r == 0) ? load_first(e) : sm[pad_idx(e) * Cb];
+      }
+    }
+    switch (S) {
+      case 1: groups_compute<INV, 1>(x, gpt, tv, Tv, logstep, gb_mod, gs, T, p); break;
+      case 2: groups_compute<INV, 2>(x, gpt, tv, Tv, logstep, gb_mod, gs, T, p); break;
+      case 3: groups_compute<INV, 3>(x, gpt, tv, Tv, logstep, gb_mod, gs, T, p); break;
+      default: groups_compute<INV, 4>(x, gpt, tv, Tv, logstep, gb_mod, gs, T, p); break;
+    }
+    // scatter
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < cnt) {
+        const uint32_t g = (uint32_t)(tv + (i >> S) * Tv);
+        const uint32_t k = (uint32_t)(i & ((1 << S) - 1));
+        const uint32_t e = ((g >> logstep) << lb) + (g & ((1u << logstep) - 1)) + (k << logstep);
+        if (r == nr - 1)
+          store_last(e, x[i]);
+        else
+          sm[pad_idx(e) * Cb] = x[i];
+      }
+    }
+    if (r != nr - 1) __syncthreads();
+  }
+}
+
+__device__ __forceinline__ uint32_t lift(int32_t D, uint32_t p) {
+  return D >= 0 ? (uint32_t)D : (uint32_t)D + p;  // canonical lift (ruling 5)
+}
+
+// ============================================================== column passes
+struct ColParams {
+  int logm, logC, logR, logCb;
+  int64_t nb;
+  int K, L;
+  uint32_t p[2];
+  const uint2* tw;        // [2 prime][2 dir][m]
+  // forward
+  const int32_t* digits;  // [nb][2][K][in_len]
+  int64_t in_len;         // n (x') or m (omega~*)
+  uint32_t* Y;            // [nb][2 q][2 a][K][m]
+  // inverse
+  const uint32_t* G;      // [nb][2 q][4 cv][K*K][m]
+  uint32_t* res;          // [nb][4 cv][2 q][K*K][n]
+  int64_t n;
+  const int32_t* stats;   // [nb][stats_stride]
+  const int32_t* sched;   // [nb][4][sched_stride]
+  uint32_t unit_mask;
+};
+
+// Forward column pass: global DIF stages len = m .. 2C on columns of the R x C view.
+__global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
+  extern __shared__ uint32_t smem[];
+  const int64_t ncb = 1ll << (P.logC - P.logCb);
+  const int64_t cb = blockIdx.x % ncb;
+  int64_t v = blockIdx.x / ncb;  // ((b * 2 + q) * 2 + a) * K + s
+  const int s = (int)(v % P.K); v /= P.K;
+  const int a = (int)(v % 2); v /= 2;
+  const int q = (int)(v % 2); v /= 2;
+  const int64_t b = v;
+  const int32_t* st = P.stats + b * stats_stride(P.K);
+  if (s >= st[a]) return;  // slice does not exist (k_a <= s) or transform non-finite
+  // unit (cv, q) needs part a if conv_a(cv) == a
+  const uint32_t need = a == 0 ? ((1u << (0 * 2 + q)) | (1u << (3 * 2 + q)))
+                               : ((1u << (1 * 2 + q)) | (1u << (2 * 2 + q)));
+  if (!(P.unit_mask & need)) return;
+  const int Cb = 1 << P.logCb;
+  const int c = threadIdx.x & (Cb - 1);
+  const int tv = threadIdx.x >> P.logCb;
+  const int Tv = P.logR >= 4 ? (1 << (P.logR - 4)) : 1;
+  if (tv >= Tv) return;
+  const uint32_t p = P.p[q];
+  const uint32_t C = 1u << P.logC;
+  const uint32_t col = (uint32_t)(cb << P.logCb) + c;
+  const int32_t* D = P.digits + ((b * 2 + a) * P.K + s) * P.in_len;
+  uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (1ll << P.logm);
+  const uint2* T = P.tw + (size_t)(q * 2 + 0) * (1ull << P.logm);
+  const int64_t in_len = P.in_len;
+  sub_ntt<false>(
+      P.logR, tv, Tv, smem + c, Cb, col, C, T, p,
+      [&](uint32_t e) -> uint32_t {
+        const int64_t i = (int64_t)e * C + col;
+        return i < in_len ? lift(__ldg(&D[i]), p) : 0u;
+      },
+      [&](uint32_t e, uint32_t val) { out[(int64_t)e * C + col] = val; });
+}
+
+// Inverse column pass: global DIT stages len = 2C .. m; writes rows i < n only.
+__global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
+  extern __shared__ uint32_t smem[];
+  const int64_t ncb = 1ll << (P.logC - P.logCb);
+  const int G = P.K * P.K;
+  const int64_t cb = blockIdx.x % ncb;
+  int64_t v = blockIdx.x / ncb;  // ((b * 2 + q) * 4 + cv) * G + g
+  const int g = (int)(v % G); v /= G;
+  const int cv = (int)(v % 4); v /= 4;
+  const int q = (int)(v % 2); v /= 2;
+  const int64_t b = v;
+  if (!(P.unit_mask & (1u << (cv * 2 + q)))) return;
+  if (g >= P.sched[(b * 4 + cv) * sched_stride(P.K, P.L)]) return;
+  const int Cb = 1 << P.logCb;
+  const int c = threadIdx.x & (Cb - 1);
+  const int tv = threadIdx.x >> P.logCb;
+  const int Tv = P.logR >= 4 ? (1 << (P.logR - 4)) : 1;
+  if (tv >= Tv) return;
+  const uint32_t p = P.p[q];
+  const uint32_t C = 1u << P.logC;
+  const uint32_t col = (uint32_t)(cb << P.logCb) + c;
+  const int64_t m = 1ll << P.logm;
+  const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m;
+  uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
+  const uint2* T = P.tw + (size_t)(q * 2 + 1) * (1ull << P.logm);
+  const int64_t n = P.n;
+  sub_ntt<true>(
+      P.logR, tv, Tv, smem + c, Cb, col, C, T, p,
+      [&](uint32_t e) -> uint32_t { return __ldg(&in[(int64_t)e * C + col]); },
+      [&](uint32_t e, uint32_t val) {
+        const int64_t i = (int64_t)e * C + col;
+        if (i < n) out[i] = val;
+      });
+}
+
+// ============================================================== fused row kernel
+struct RowParams {
+  int logm, logC, logR;
+  int64_t nb;
+  int K, L;
+  uint32_t p[2];
+  const uint2* tw;        // [2 prime][2 dir][m]
+  const int32_t* digits;  // R == 1: [nb][2][K][in_len]
+  int64_t in_len;
+  const uint32_t* Y;      // R > 1: [nb][2][2][K][m]
+  const uint2* W;         // [2 q][2 b][K][m] (W m^{-1}, Shoup)
+  uint32_t* G;            // R > 1: [nb][2 q][4][K*K][m]
+  uint32_t* res;          // R == 1: [nb][4][2][K*K][n]
+  int64_t n;
+  const int32_t* stats;
+  const int32_t* sched;
+  uint32_t unit_mask;
+  int fwd_only;           // 1: write the forward spectra (internal order) to Xout, stop
+  uint32_t* Xout;         // fwd_only or tap: [nb][2 q][2 a][K][m]
+  uint32_t* Zout;         // tap: [nb][2 q][4][K*K][m] (internal order, W m^{-1} scaled)
+};
+
+__global__ void __launch_bounds__(256) k_row_fused(RowParams P) {
+  extern __shared__ uint32_t smem[];
+  const int64_t b = blockIdx.x;
+  const int a = blockIdx.y & 1;
+  const int q = (blockIdx.y >> 1) & 1;
+  const uint32_t row = blockIdx.y >> 2;
+  const int logC = P.logC;
+  const uint32_t C = 1u << logC;
+  const uint32_t padC = C + (C >> 4) + 1;
+  const int Tv = logC >= 4 ? (1 << (logC - 4)) : 1;
+  const int tv = threadIdx.x;
+  const int64_t m = 1ll << P.logm;
+  const uint32_t p = P.p[q];
+  const int K = P.K, L = P.L, G = K * K;
+  const int32_t* st = P.stats + b * stats_stride(K);
+  const int ka = st[a];
+  // convolutions using part a: a = 0 -> rr (0), ri (3); a = 1 -> ii (1), ir (2)
+  const int cvs[2] = {a == 0 ? 0 : 1, a == 0 ? 3 : 2};
+  bool want[2];
+  for (int i = 0; i < 2; ++i) want[i] = (P.unit_mask >> (cvs[i] * 2 + q)) & 1u;
+  if (!P.fwd_only && !want[0] && !want[1]) return;
+  if (ka == 0 && !P.fwd_only) {
+    // nothing to convolve; the schedule has no groups for these convolutions
+    return;
+  }
+  uint32_t* Xs = smem;                 // [K][padC]
+  uint32_t* work = smem + K * padC;    // 2 x [padC]
+  const uint2* Tf = P.tw + (size_t)(q * 2 + 0) * m;
+  const uint2* Ti = P.tw + (size_t)(q * 2 + 1) * m;
+  const uint32_t rowoff = row << logC;
+  int buf = 0;
+  // ---- forward: last log2(C) DIF stages of each slice's NTT (Alg.6 l.787)
+  for (int s = 0; s < ka; ++s) {
+    uint32_t* xs = Xs + s * padC;
+    uint32_t* outX = P.Xout ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff : nullptr;
+    if (P.logR > 0) {
+      const uint32_t* y = P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff;
+      sub_ntt<false>(
+          logC, tv, Tv, work + buf * padC, 1, 0u, 1u, Tf, p,
+          [&](uint32_t e) -> uint32_t { return __ldg(&y[e]); },
+          [&](uint32_t e, uint32_t v) {
+            xs[pad_idx(e)] = v;
+            if (outX) outX[e] = v;
+          });
+    } else {
+      const int32_t* D = P.digits + ((b * 2 + a) * K + s) * P.in_len;
+      const int64_t in_len = P.in_len;
+      sub_ntt<false>(
+          logC, tv, Tv, work + buf * padC, 1, 0u, 1u, Tf, p,
+          [&](uint32_t e) -> uint32_t { return (int64_t)e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
+          [&](uint32_t e, uint32_t v) {
+            xs[pad_idx(e)] = v;
+            if (outX) outX[e] = v;
+          });
+    }
+    buf ^= 1;
+  }
+  if (P.fwd_only) return;
+  __syncthreads();
+  // ---- per group: Z = sum X_s (.) W_t (Alg.8 l.981-982), then first DIT stages
+  for (int ci = 0; ci < 2; ++ci) {
+    if (!want[ci]) continue;
+    const int cv = cvs[ci];
+    const int bw = conv_b(cv);
+    const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
+    const int ng = srow[0];
+    for (int g = 0; g < ng; ++g) {
+      const int32_t* grp = srow + 1 + g * (2 + 2 * L);
+      const int np = grp[1];
+      uint32_t* Zt = P.Zout ? P.Zout + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff : nullptr;
+      auto load_z = [&](uint32_t e) -> uint32_t {
+        uint32_t z = 0;
+        for (int i = 0; i < np; ++i) {
+          const int s = grp[2 + 2 * i], t = grp[3 + 2 * i];
+          const uint2 w = __ldg(&P.W[((size_t)(q * 2 + bw) * K + t) * m + rowoff + e]);
+          z = add_mod(z, mul_shoup(Xs[s * padC + pad_idx(e)], w, p), p);
+        }
+        if (Zt) Zt[e] = z;
+        return z;
+      };
+      if (P.logR > 0) {
+        uint32_t* gout = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
+        sub_ntt<true>(logC, tv, Tv, work + buf * padC, 1, 0u, 1u, Ti, p, load_z,
+                      [&](uint32_t e, uint32_t v) { gout[e] = v; });
+      } else {
+        uint32_t* rout = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
+        const int64_t n = P.n;
+        sub_ntt<true>(logC, tv, Tv, work + buf * padC, 1, 0u, 1u, Ti, p, load_z,
+                      [&](uint32_t e, uint32_t v) {
+                        if ((int64_t)e < n) rout[e] = v;
+                      });
+      }
+      buf ^= 1;
+    }
+  }
+}
+
+// ============================================================== CRT + recombination
+struct FinishParams {
+  int64_t n, nb;
+  int K, L;
+  uint32_t p0, p1, p0inv;   // p0^{-1} mod p1
+  const uint32_t* res;      // [nb][4][2][K*K][n]
+  const int32_t* stats;
+  const int32_t* sched;
+  const double2* chirp;     // [n]
+  double2* out;             // [nb][n]
+  int direction;
+  int64_t* crt_tap;         // [nb][4][K*K][n] or null
+};
+
+// symmetric residue of z in [0, p): z or z - p, in [-(p-1)/2, (p-1)/2]
+__device__ __forceinline__ int64_t sym_res(uint32_t z, uint32_t p) {
+  return z > (p >> 1) ? (int64_t)z - (int64_t)p : (int64_t)z;
+}
+
+// Garner, two primes (Alg.8 l.974): the unique Z in [-p0p1/2, p0p1/2).
+__device__ __forceinline__ long long garner2(uint32_t z0, uint32_t z1, uint32_t p0, uint32_t p1,
+                                             uint32_t inv) {
+  const int64_t z0s = sym_res(z0, p0);
+  // (z1 - z0s) mod p1 in [0, p1): z0s in (-p0/2, p0/2), p0 < 2 p1
+  int64_t d = (int64_t)z1 - z0s;
+  d %= (int64_t)p1;
+  if (d < 0) d += p1;
+  const uint32_t t = (uint32_t)(((uint64_t)d * inv) % p1);
+  return (long long)(z0s + sym_res(t, p1) * (int64_t)p0);
+}
+
+__global__ void __launch_bounds__(256) k_crt_finish(FinishParams P) {
+  const int64_t b = blockIdx.y;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.n) return;
+  const int K = P.K, L = P.L, G = K * K;
+  const int32_t* st = P.stats + b * stats_stride(K);
+  double2 o;
+  if (st[2 + 2 * K] & 1) {
+    o.x = __longlong_as_double(0x7FF8000000000000ll);
+    o.y = o.x;
+    P.out[b * P.n + j] = o;
+    return;
+  }
+  double Sh[4], Sl[4];
+  for (int cv = 0; cv < 4; ++cv) {
+    double sh = 0.0, sl = 0.0;
+    const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
+    const int ng = srow[0];
+    const uint32_t* r0 = P.res + (((b * 4 + cv) * 2 + 0) * G) * P.n + j;
+    const uint32_t* r1 = P.res + (((b * 4 + cv) * 2 + 1) * G) * P.n + j;
+    for (int g = 0; g < ng; ++g) {
+      const int cexp = srow[1 + g * (2 + 2 * L)];
+      const long long Z = garner2(__ldg(&r0[g * P.n]), __ldg(&r1[g * P.n]), P.p0, P.p1, P.p0inv);
+      if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + j] = Z;
+      const double h = __ll2double_rn(Z);
+      const double l = __ll2double_rn(Z - __double2ll_rz(h));
+      const double sc = scalbn(1.0, -cexp);  // z' / c, exact (l.975)
+      dd_add(sh, sl, __dmul_rn(h, sc), __dmul_rn(l, sc), sh, sl);
+    }
+    Sh[cv] = sh;
+    Sl[cv] = sl;
+  }
+  double yrh, yrl, yih, yil;
+  dd_add(Sh[0], Sl[0], -Sh[1], -Sl[1], yrh, yrl);  // rr - ii
+  dd_add(Sh[2], Sl[2], Sh[3], Sl[3], yih, yil);    // ir + ri
+  const double2 w = P.chirp[j];
+  double a1h, a1l, a2h, a2l, ore, oim, tmp;
+  dd_mul_d(yrh, yrl, w.x, a1h, a1l);
+  dd_mul_d(yih, yil, w.y, a2h, a2l);
+  dd_add(a1h, a1l, -a2h, -a2l, ore, tmp);
+  dd_mul_d(yrh, yrl, w.y, a1h, a1l);
+  dd_mul_d(yih, yil, w.x, a2h, a2l);
+  dd_add(a1h, a1l, a2h, a2l, oim, tmp);
+  if (P.direction > 0) {
+    const double dn = (double)P.n;
+    ore = __ddiv_rn(ore, dn);
+    oim = __ddiv_rn(-oim, dn);
+  }
+  o.x = ore;
+  o.y = oim;
+  P.out[b * P.n + j] = o;
+}
+
+// ============================================================== small utility kernels
+// W finalize: Wp[q][b][t][i] = (W m^{-1} mod p, Shoup companion) from the forward spectra.
+__global__ void k_w_finalize(const uint32_t* __restrict__ X, uint2* __restrict__ Wp, int K,
+                             int64_t m, uint32_t p0, uint32_t p1, uint32_t minv0, uint32_t minv1) {
+  const int64_t total = (int64_t)4 * K * m;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(i / (2 * K * m));
+    const uint32_t p = q ? p1 : p0, mi = q ? minv1 : minv0;
+    const uint32_t w = (uint32_t)(((uint64_t)X[i] * mi) % p);
+    Wp[i] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));
+  }
+}
+
+// Tap conversion: internal bit-reversed order (optionally times a constant) -> natural.
+//   dst[o(v)][k] = src[v][bitrev(k)] * mult mod p, for vectors v of length m.
+__global__ void k_tap_permute(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                              int64_t nvec, int logm, const int64_t* __restrict__ dst_off,
+                              const uint32_t* __restrict__ vec_p, uint32_t mult_is_m) {
+  const int64_t m = 1ll << logm;
+  const int64_t total = nvec * m;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i >> logm, k = i & (m - 1);
+    const int64_t br = logm ? (int64_t)(__brevll((unsigned long long)k) >> (64 - logm)) : 0;
+    uint32_t val = src[v * m + br];
+    if (mult_is_m) val = (uint32_t)(((uint64_t)val * (uint64_t)(m % vec_p[v])) % vec_p[v]);
+    dst[dst_off[v] + k] = val;
+  }
+}
+
+// ============================================================== launchers
+static ozfft_status cuda_check(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return OZFFT_ERR_CUDA;
+  }
+  return OZFFT_OK;
+}
+
+static int col_logCb(int logR, int logC) {
+  // tile = R x Cb columns with R*Cb/16 = 256 threads (>= 8 columns for 32-byte sectors)
+  int lcb = (logR >= 4) ? 12 - logR : 8;
+  if (lcb < 3) lcb = 3;
+  if (lcb > logC) lcb = logC;
+  return lcb;
+}
+static size_t col_smem(int logR, int logCb) {
+  const size_t R = 1ull << logR;
+  return (R + (R >> 4) + 1) * (1ull << logCb) * sizeof(uint32_t);
+}
+static int col_threads(int logR, int logCb) {
+  const int Tv = logR >= 4 ? (1 << (logR - 4)) : 1;
+  return Tv << logCb;
+}
+
+static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cudaStream_t st) {
+  const int threads = 256;
+  int64_t blocks_per = (SP.len + threads * 4 - 1) / (threads * 4);
+  if (blocks_per < 1) blocks_per = 1;
+  if (blocks_per > 65535) blocks_per = 65535;
+  dim3 grid((unsigned)blocks_per, (unsigned)nb);
+  for (int level = 0; level < SP.K; ++level) k_split_max<<<grid, threads, 0, st>>>(SP, level);
+  k_split_digits<<<grid, threads, 0, st>>>(SP);
+  (void)pl;
+  return cuda_check("split kernels");
+}
+
+struct NttLaunch {
+  int logCb;
+  size_t col_smem;
+  int col_threads;
+  size_t row_smem;
+  int row_threads;
+};
+static NttLaunch ntt_launch_cfg(const Plan& pl) {
+  NttLaunch c;
+  c.logCb = col_logCb(pl.logR, pl.logC);
+  c.col_smem = col_smem(pl.logR, c.logCb);
+  c.col_threads = col_threads(pl.logR, c.logCb);
+  const size_t C = 1ull << pl.logC;
+  const size_t padC = C + (C >> 4) + 1;
+  c.row_smem = (size_t)(pl.K + 2) * padC * sizeof(uint32_t);
+  c.row_threads = pl.logC >= 4 ? (1 << (pl.logC - 4)) : 1;  // exactly Tv: every thread active
+  return c;
+}
+
+static ozfft_status set_smem_attrs(const NttLaunch& c) {
+  static size_t done_col = 0, done_row = 0;
+  if (c.col_smem > 48 * 1024 && c.col_smem > done_col) {
+    cudaFuncSetAttribute(k_col_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.col_smem);
+    cudaFuncSetAttribute(k_col_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.col_smem);
+    done_col = c.col_smem;
+  }
+  if (c.row_smem > 48 * 1024 && c.row_smem > done_row) {
+    cudaFuncSetAttribute(k_row_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.row_smem);
+    done_row = c.row_smem;
+  }
+  return cuda_check("cudaFuncSetAttribute");
+}
+
+// Forward NTT of digit vectors [nb][2][K][in_len] into internal-order spectra Xout
+// [nb][2 q][2 a][K][m] (used at plan time for omega~*; the hot path fuses the row part).
+static ozfft_status launch_forward_only(const Plan& pl, const int32_t* digits, int64_t in_len,
+                                        const int32_t* stats, uint32_t* Y, uint32_t* Xout,
+                                        int64_t nb, cudaStream_t st) {
+  const NttLaunch c = ntt_launch_cfg(pl);
+  ozfft_status s = set_smem_attrs(c);
+  if (s) return s;
+  const uint2* tw = reinterpret_cast<const uint2*>(pl.pers + pl.poff.tw);
+  if (pl.logR > 0) {
+    ColParams CP{};
+    CP.logm = pl.logm; CP.logC = pl.logC; CP.logR = pl.logR; CP.logCb = c.logCb;
+    CP.nb = nb; CP.K = pl.K; CP.L = pl.L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
+    CP.tw = tw; CP.digits = digits; CP.in_len = in_len; CP.Y = Y; CP.stats = stats;
+    CP.unit_mask = 0xFF;
+    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4 * pl.K;
+    k_col_fwd<<<(unsigned)nblk, c.col_threads, c.col_smem, st>>>(CP);
+  }
+  RowParams RP{};
+  RP.logm = pl.logm; RP.logC = pl.logC; RP.logR = pl.logR; RP.nb = nb; RP.K = pl.K; RP.L = pl.L;
+  RP.p[0] = pl.p[0]; RP.p[1] = pl.p[1]; RP.tw = tw; RP.digits = digits; RP.in_len = in_len;
+  RP.Y = Y; RP.stats = stats; RP.unit_mask = 0xFF; RP.fwd_only = 1; RP.Xout = Xout;
+  dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
+  k_row_fused<<<grid, c.row_threads, c.row_smem, st>>>(RP);
+  return cuda_check("forward-only NTT");
+}
+
+ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t m = pl.m;
+  const int K = pl.K;
+  // scratch (plan time only)
+  unsigned long long* mu = nullptr;
+  int32_t *digits = nullptr, *stats = nullptr;
+  uint32_t *Y = nullptr, *X = nullptr;
+  if (cudaMalloc(&mu, sizeof(unsigned long long) * 2 * K) ||
+      cudaMalloc(&digits, sizeof(int32_t) * 2 * K * m) ||
+      cudaMalloc(&stats, sizeof(int32_t) * stats_stride(K)) ||
+      cudaMalloc(&Y, sizeof(uint32_t) * 4 * K * m) || cudaMalloc(&X, sizeof(uint32_t) * 4 * K * m)) {
+    set_error("cudaMalloc failed in plan precompute");
+    return OZFFT_ERR_CUDA;
+  }
+  cudaMemsetAsync(mu, 0, sizeof(unsigned long long) * 2 * K, st);
+  cudaMemsetAsync(X, 0, sizeof(uint32_t) * 4 * K * m, st);
+  SplitParams SP{};
+  SP.x = reinterpret_cast<const double2*>(pl.pers + pl.poff.W);  // wstar staged in the W area
+  SP.chirp = nullptr;
+  SP.len = m;
+  SP.mode = 1;
+  SP.K = K;
+  SP.alpha = pl.alpha;
+  SP.rho = pl.rho;
+  SP.mu = mu;
+  SP.digits = digits;
+  SP.stats = stats;
+  SP.sched = nullptr;
+  SP.L = pl.L;
+  ozfft_status s = launch_split(pl, SP, 1, st);
+  if (!s) s = launch_forward_only(pl, digits, m, stats, Y, X, 1, st);
+  int32_t hstats[4 + 2 * kMaxK];
+  if (!s) {
+    cudaMemcpyAsync(hstats, stats, sizeof(int32_t) * stats_stride(K), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) s = cuda_check("plan precompute");
+  }
+  if (!s) {
+    if (hstats[2 + 2 * K] & 1) {
+      set_error("omega~* split produced a non-finite value");
+      s = OZFFT_ERR_CUDA;
+    }
+  }
+  if (!s) {
+    pl.kw[0] = hstats[0];
+    pl.kw[1] = hstats[1];
+    int32_t wsplit[2 + 2 * kMaxK] = {0};
+    wsplit[0] = pl.kw[0];
+    wsplit[1] = pl.kw[1];
+    for (int v = 0; v < 2; ++v)
+      for (int k = 0; k < K; ++k) {
+        pl.Ew[v][k] = hstats[2 + v * K + k];
+        wsplit[2 + v * K + k] = pl.Ew[v][k];
+      }
+    cudaMemcpyAsync(pl.pers + pl.poff.wsplit, wsplit, sizeof(int32_t) * (2 + 2 * K),
+                    cudaMemcpyHostToDevice, st);
+    k_w_finalize<<<592, 256, 0, st>>>(X, reinterpret_cast<uint2*>(pl.pers + pl.poff.W), K, m,
+                                      pl.p[0], pl.p[1], pl.minv[0], pl.minv[1]);
+    s = cuda_check("W finalize");
+    if (!s && cudaStreamSynchronize(st) != cudaSuccess) s = cuda_check("plan precompute sync");
+  }
+  cudaFree(mu);
+  cudaFree(digits);
+  cudaFree(stats);
+  cudaFree(Y);
+  cudaFree(X);
+  return s;
+}
+
+ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int K = pl.K, L = pl.L, G = K * K;
+  const int64_t nb = A.nb, m = pl.m, n = pl.n;
+  uint8_t* ws = pl.ws;
+  // per-batch stats and schedules live at the transform's global index
+  int32_t* stats = reinterpret_cast<int32_t*>(ws + pl.woff.stats) + A.b0 * stats_stride(K);
+  int32_t* sched = reinterpret_cast<int32_t*>(ws + pl.woff.sched) + A.b0 * 4 * sched_stride(K, L);
+  unsigned long long* mu = reinterpret_cast<unsigned long long*>(ws + pl.woff.mu);
+  int32_t* digits = reinterpret_cast<int32_t*>(ws + pl.woff.digits);
+  uint32_t* Y = reinterpret_cast<uint32_t*>(ws + pl.woff.Y);
+  uint32_t* Gb = reinterpret_cast<uint32_t*>(ws + pl.woff.G);
+  uint32_t* res = reinterpret_cast<uint32_t*>(ws + pl.woff.res);
+  const uint2* tw = reinterpret_cast<const uint2*>(pl.pers + pl.poff.tw);
+  const uint2* W = reinterpret_cast<const uint2*>(pl.pers + pl.poff.W);
+  const double2* chirp = reinterpret_cast<const double2*>(pl.pers + pl.poff.chirp);
+  const int32_t* wsplit = reinterpret_cast<const int32_t*>(pl.pers + pl.poff.wsplit);
+  const ozfft_taps* taps = A.taps;
+
+  cudaMemsetAsync(mu, 0, sizeof(unsigned long long) * 2 * K * nb, st);
+  SplitParams SP{};
+  SP.x = reinterpret_cast<const double2*>(A.in);
+  SP.chirp = chirp;
+  SP.len = n;
+  SP.mode = 0;
+  SP.conj = A.direction > 0 ? 1 : 0;
+  SP.K = K;
+  SP.alpha = pl.alpha;
+  SP.rho = pl.rho;
+  SP.mu = mu;
+  SP.digits = taps && taps->digits ? reinterpret_cast<int32_t*>(taps->digits) : digits;
+  SP.stats = stats;
+  SP.sched = sched;
+  SP.wsplit = wsplit;
+  SP.L = L;
+  ozfft_status s = launch_split(pl, SP, nb, st);
+  if (s) return s;
+  const NttLaunch c = ntt_launch_cfg(pl);
+  s = set_smem_attrs(c);
+  if (s) return s;
+  uint32_t* Xtap = nullptr;
+  uint32_t* Ztap = nullptr;
+  if (taps && (taps->X || taps->Z)) {
+    if (taps->X && cudaMalloc(&Xtap, sizeof(uint32_t) * nb * 4 * K * m)) return cuda_check("tap alloc");
+    if (taps->Z && cudaMalloc(&Ztap, sizeof(uint32_t) * nb * 8 * G * m)) return cuda_check("tap alloc");
+    if (Xtap) cudaMemsetAsync(Xtap, 0, sizeof(uint32_t) * nb * 4 * K * m, st);
+    if (Ztap) cudaMemsetAsync(Ztap, 0, sizeof(uint32_t) * nb * 8 * G * m, st);
+  }
+  if (pl.logR > 0) {
+    ColParams CP{};
+    CP.logm = pl.logm; CP.logC = pl.logC; CP.logR = pl.logR; CP.logCb = c.logCb;
+    CP.nb = nb; CP.K = K; CP.L = L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
+    CP.tw = tw; CP.digits = SP.digits; CP.in_len = n; CP.Y = Y; CP.stats = stats;
+    CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n; CP.unit_mask = A.unit_mask;
+    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4 * K;
+    k_col_fwd<<<(unsigned)nblk, c.col_threads, c.col_smem, st>>>(CP);
+    s = cuda_check("k_col_fwd");
+    if (s) return s;
+  }
+  RowParams RP{};
+  RP.logm = pl.logm; RP.logC = pl.logC; RP.logR = pl.logR; RP.nb = nb; RP.K = K; RP.L = L;
+  RP.p[0] = pl.p[0]; RP.p[1] = pl.p[1]; RP.tw = tw; RP.digits = SP.digits; RP.in_len = n;
+  RP.Y = Y; RP.W = W; RP.G = Gb; RP.res = res; RP.n = n; RP.stats = stats; RP.sched = sched;
+  RP.unit_mask = A.unit_mask; RP.fwd_only = 0; RP.Xout = Xtap; RP.Zout = Ztap;
+  {
+    dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
+    k_row_fused<<<grid, c.row_threads, c.row_smem, st>>>(RP);
+    s = cuda_check("k_row_fused");
+    if (s) return s;
+  }
+  if (pl.logR > 0) {
+    ColParams CP{};
+    CP.logm = pl.logm; CP.logC = pl.logC; CP.logR = pl.logR; CP.logCb = c.logCb;
+    CP.nb = nb; CP.K = K; CP.L = L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
+    CP.tw = tw; CP.stats = stats; CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n;
+    CP.unit_mask = A.unit_mask;
+    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 8 * G;
+    k_col_inv<<<(unsigned)nblk, c.col_threads, c.col_smem, st>>>(CP);
+    s = cuda_check("k_col_inv");
+    if (s) return s;
+  }
+  if (A.finish) {
+    FinishParams FP{};
+    FP.n = n; FP.nb = nb; FP.K = K; FP.L = L; FP.p0 = pl.p[0]; FP.p1 = pl.p[1];
+    FP.p0inv = pl.p0inv_mod_p1; FP.res = res; FP.stats = stats; FP.sched = sched;
+    FP.chirp = chirp; FP.out = reinterpret_cast<double2*>(A.out); FP.direction = A.direction;
+    FP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
+    dim3 grid((unsigned)((n + 255) / 256), (unsigned)nb);
+    k_crt_finish<<<grid, 256, 0, st>>>(FP);
+    s = cuda_check("k_crt_finish");
+    if (s) return s;
+  }
+  // ---- taps (test only): convert internal orders to the oracle's natural layouts
+  if (taps) {
+    std::vector<int64_t> off;
+    std::vector<uint32_t> vp;
+    auto run_perm = [&](const uint32_t* src, void* dst, bool mult) -> ozfft_status {
+      int64_t* doff = nullptr;
+      uint32_t* dvp = nullptr;
+      const int64_t nvec = (int64_t)off.size();
+      cudaMalloc(&doff, sizeof(int64_t) * nvec);
+      cudaMalloc(&dvp, sizeof(uint32_t) * nvec);
+      cudaMemcpyAsync(doff, off.data(), sizeof(int64_t) * nvec, cudaMemcpyHostToDevice, st);
+      cudaMemcpyAsync(dvp, vp.data(), sizeof(uint32_t) * nvec, cudaMemcpyHostToDevice, st);
+      k_tap_permute<<<1184, 256, 0, st>>>(src, reinterpret_cast<uint32_t*>(dst), nvec, pl.logm,
+                                          doff, dvp, mult ? 1u : 0u);
+      cudaStreamSynchronize(st);
+      cudaFree(doff);
+      cudaFree(dvp);
+      return cuda_check("tap permute");
+    };
+    if (taps->X) {  // src [b][q][a][s][m] -> dst [b][a][s][q][m]
+      off.clear(); vp.clear();
+      for (int64_t b = 0; b < nb; ++b)
+        for (int q = 0; q < 2; ++q)
+          for (int a = 0; a < 2; ++a)
+            for (int s2 = 0; s2 < K; ++s2) {
+              off.push_back((((b * 2 + a) * K + s2) * 2 + q) * m);
+              vp.push_back(pl.p[q]);
+            }
+      s = run_perm(Xtap, taps->X, false);
+      if (s) return s;
+    }
+    if (taps->Z) {  // src [b][q][cv][g][m] (W m^-1 scaled) -> dst [b][cv][g][q][m] (times m)
+      off.clear(); vp.clear();
+      for (int64_t b = 0; b < nb; ++b)
+        for (int q = 0; q < 2; ++q)
+          for (int cv = 0; cv < 4; ++cv)
+            for (int g = 0; g < G; ++g) {
+              off.push_back((((b * 4 + cv) * G + g) * 2 + q) * m);
+              vp.push_back(pl.p[q]);
+            }
+      s = run_perm(Ztap, taps->Z, true);
+      if (s) return s;
+    }
+    if (taps->res) {  // [b][cv][q][g][n] -> [b][cv][g][q][n]
+      for (int64_t b = 0; b < nb; ++b)
+        for (int cv = 0; cv < 4; ++cv)
+          for (int q = 0; q < 2; ++q)
+            for (int g = 0; g < G; ++g)
+              cudaMemcpyAsync(reinterpret_cast<uint32_t*>(taps->res) + (((b * 4 + cv) * G + g) * 2 + q) * n,
+                              res + (((b * 4 + cv) * 2 + q) * G + g) * n, sizeof(uint32_t) * n,
+                              cudaMemcpyDeviceToDevice, st);
+    }
+    if (taps->sched)
+      cudaMemcpyAsync(taps->sched, sched, sizeof(int32_t) * nb * 4 * sched_stride(K, L),
+                      cudaMemcpyDeviceToDevice, st);
+    if (taps->W) {  // src Wp [q][b][t][m] (uint2, m^-1 scaled) -> [b][t][q][m] times m
+      uint32_t* tmp = nullptr;
+      cudaMalloc(&tmp, sizeof(uint32_t) * 4 * K * m);
+      cudaMemcpy2DAsync(tmp, sizeof(uint32_t), W, sizeof(uint2), sizeof(uint32_t), 4 * K * m,
+                        cudaMemcpyDeviceToDevice, st);
+      off.clear(); vp.clear();
+      for (int q = 0; q < 2; ++q)
+        for (int bw = 0; bw < 2; ++bw)
+          for (int t = 0; t < K; ++t) {
+            off.push_back(((bw * K + t) * 2 + q) * m);
+            vp.push_back(pl.p[q]);
+          }
+      s = run_perm(tmp, taps->W, true);
+      cudaFree(tmp);
+      if (s) return s;
+    }
+    if (taps->E || taps->kv) {
+      std::vector<int32_t> hs((size_t)nb * stats_stride(K));
+      cudaMemcpyAsync(hs.data(), stats, sizeof(int32_t) * hs.size(), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      std::vector<int32_t> hE((size_t)nb * 2 * K), hk((size_t)nb * 2);
+      for (int64_t b = 0; b < nb; ++b) {
+        const int32_t* r = hs.data() + b * stats_stride(K);
+        hk[b * 2] = r[0];
+        hk[b * 2 + 1] = r[1];
+        for (int i = 0; i < 2 * K; ++i) hE[b * 2 * K + i] = r[2 + i];
+      }
+      if (taps->E) cudaMemcpyAsync(taps->E, hE.data(), sizeof(int32_t) * hE.size(), cudaMemcpyHostToDevice, st);
+      if (taps->kv) cudaMemcpyAsync(taps->kv, hk.data(), sizeof(int32_t) * hk.size(), cudaMemcpyHostToDevice, st);
+      cudaStreamSynchronize(st);
+    }
+    cudaStreamSynchronize(st);
+    if (Xtap) cudaFree(Xtap);
+    if (Ztap) cudaFree(Ztap);
+    s = cuda_check("taps");
+  }
+  return s;
+}
+
+ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, double* out,
+                                         int direction, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  FinishParams FP{};
+  FP.n = pl.n; FP.nb = 1; FP.K = pl.K; FP.L = pl.L; FP.p0 = pl.p[0]; FP.p1 = pl.p[1];
+  FP.p0inv = pl.p0inv_mod_p1; FP.res = res;
+  FP.stats = reinterpret_cast<const int32_t*>(pl.ws + pl.woff.stats);
+  FP.sched = reinterpret_cast<const int32_t*>(pl.ws + pl.woff.sched);
+  FP.chirp = reinterpret_cast<const double2*>(pl.pers + pl.poff.chirp);
+  FP.out = reinterpret_cast<double2*>(out);
+  FP.direction = direction;
+  dim3 grid((unsigned)((pl.n + 255) / 256), 1);
+  k_crt_finish<<<grid, 256, 0, st>>>(FP);
+  return cuda_check("k_crt_finish (shard)");
+}
+
+}  // namespace ozfft

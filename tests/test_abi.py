@@ -1,0 +1,82 @@
+"""The C-ABI library builds, loads and exports every symbol include/ozfft.h declares.
+No compute calls (this runs on the CPU-only container)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "ozfft.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(ozfft_[a-z_]+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2603_29129_b200 import build
+    path = build.build()
+    return ctypes.CDLL(path)
+
+
+def test_exports_match_header(lib):
+    import paper_2603_29129_b200 as oz
+    syms = header_symbols()
+    assert len(syms) >= 13
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(oz.EXPORTS) == syms
+
+
+def test_status_strings_and_version(lib):
+    lib.ozfft_status_string.restype = ctypes.c_char_p
+    lib.ozfft_version.restype = ctypes.c_char_p
+    assert lib.ozfft_status_string(0) == b"OZFFT_OK"
+    assert lib.ozfft_status_string(7) == b"OZFFT_ERR_CUDA"
+    assert lib.ozfft_version().startswith(b"ozfft sm_100a")
+
+
+def test_sass_is_sm100a():
+    """The shared object carries sm_100a SASS (cuobjdump runs without a GPU)."""
+    import subprocess
+    from paper_2603_29129_b200 import build
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", build.build()],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_plan_create_validation(lib):
+    """Host-side argument checks of ozfft_plan_create (no device memory touched)."""
+    import paper_2603_29129_b200 as oz
+    L = oz.load_library()
+
+    def create(**kw):
+        d = oz.PlanDesc(**{"n": 1024, "batch": 1, "K": 3, "L": 3, "p0": 0, "p1": 0,
+                           "device": 0, "reserved": 0, "max_workspace_bytes": 0, **kw})
+        h = ctypes.c_void_p()
+        st = L.ozfft_plan_create(ctypes.byref(d), ctypes.byref(h))
+        if st == 0:
+            info = oz.PlanInfo()
+            assert L.ozfft_plan_get_info(h, ctypes.byref(info)) == 0
+            L.ozfft_plan_destroy(h)
+            return st, info
+        return st, None
+
+    st, info = create()
+    assert st == 0 and info.m == 2048 and info.alpha == 24 and info.rho == 29
+    st, info = create(n=1 << 18, batch=16)
+    assert st == 0 and info.m == 1 << 19 and info.alpha == 20
+    assert info.log2_rows + info.log2_cols == 19
+    st, info = create(n=100003, batch=32)
+    assert st == 0 and info.m == 1 << 18 and info.alpha == 21
+    assert create(n=0)[0] == 1
+    assert create(batch=0)[0] == 1
+    assert create(K=9)[0] == 1
+    assert create(p0=2130706433, p1=2130706433)[0] == 3
+    assert create(p0=2130706431)[0] == 3          # not prime
+    assert create(n=1 << 22)[0] == 2              # m = 2^23 > this build's limit
+    st, info = create(n=1)
+    assert st == 0 and info.m == 1
