@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""bench.py -- fp64-accurate FFT via 32-bit NTTs (arXiv 2603.29129) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Metric (BASELINE.json): pseudo-GFLOP/s = transforms * 5 n log2 n / time, quoted at
+n = 2^18 (config c3: batch 16 complex fp64 DFTs, m = 2^19).  A "step" is one pass
+of the whole hot path (premultiply + split, 12 forward NTTs, NTT-domain
+accumulation, 40 inverse NTTs, CRT, recombination, post-chirp) over the batch.
+
+Multi-GPU (torchrun, one process per GPU): weak scaling -- every rank transforms
+its own batch of B independent transforms (global batch N*B); there is no
+data-path collective; the timed region is bracketed by barriers and the reported
+time is the max over ranks (all_reduce MAX of each rank's CUDA-event time).
+
+--impl reference times the CPU oracle (oracle/, plain C, OpenMP over transforms)
+on this box's host cores: the reference arm of this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "fp64-accurate FFT GFLOP/s (5n·log2 n) at n=2^18; NTT HBM GB/s vs peak"
+UNIT = "GFLOP/s"
+
+# roofline denominators
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK_GBS = 6650.0        # B200_PROFILING.md fallback
+# In-register Shoup DIF butterfly rate measured on this pool's B200
+# (tools/microbench_int.cu, profiles/r01_microbench_int.txt): 3343 G butterflies/s.
+ALU_BFLY_PEAK_GPS = 3343.3
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def workload_desc(cfg):
+    dist = {"uniform": "re/im uniform[-1,1)", "normal": "re/im standard normal",
+            "signexp": "re/im sign*2^e, e in [-30,30]"}[cfg.dist]
+    return (f"{cfg.name}: batch {cfg.batch} complex fp64 DFTs, n={cfg.n} (Bluestein m="
+            f"{1 << math.ceil(math.log2(2 * cfg.n - 1))}), {dist}, seed {cfg.seed}")
+
+
+def flops_per_transform(n):
+    return 5.0 * n * math.log2(n)
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons (NVML) during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- oracle timing
+def time_oracle(cfg, ntrans, nthreads=0, reps=1):
+    import oracle as O
+    x = workloads.draw(cfg.dist, cfg.seed, cfg.batch, cfg.n, rows=slice(0, min(ntrans, cfg.batch)))
+    if x.shape[0] < ntrans:  # sample larger than the batch: repeat rows
+        x = np.ascontiguousarray(np.concatenate([x] * (ntrans // x.shape[0] + 1))[:ntrans])
+    plan = O.Plan(cfg.n)
+    ts, used = [], 1
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        y, used = plan.execute_batch(x, nthreads=nthreads)
+        if cfg.roundtrip:
+            plan.execute_batch(y, inverse=True, nthreads=nthreads)
+        ts.append(time.perf_counter() - t0)
+    dirs = 2 if cfg.roundtrip else 1
+    return ts, used, x.shape[0] * dirs
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return  # other ranks exit 0 without work
+    cores = host_cores()
+    ntrans = min(cfg.batch, cores)
+    for _ in range(args.warmup):
+        time_oracle(cfg, ntrans)
+    ts = []
+    used = 1
+    for _ in range(args.steps):
+        t, used, units = time_oracle(cfg, ntrans)
+        ts.append(t[0])
+    tot = sum(ts)
+    value = units * args.steps * flops_per_transform(cfg.n) / tot / 1e9
+    sample = (f"{ntrans} of the {cfg.batch} transforms of {cfg.name} per step "
+              f"({'fwd+inv' if cfg.roundtrip else 'fwd'}), OpenMP over transforms")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64+u64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "n": cfg.n, "batch": cfg.batch, "K": 3,
+                       "L": 3, "impl": "CPU oracle (oracle/ozfft_oracle.c)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import paper_2603_29129_b200 as oz
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    B, n = cfg.batch, cfg.n
+    # weak scaling: rank r owns transforms [r*B, (r+1)*B) of a global batch of world*B
+    x_np = workloads.draw(cfg.dist, cfg.seed, world * B, n, rows=slice(rank * B, (rank + 1) * B)) \
+        if world > 1 else workloads.config_input(cfg)
+    x = torch.from_numpy(x_np).to(dev)
+    plan = oz.Plan(n, B, device=dev)
+    out = torch.empty_like(x)
+    back = torch.empty_like(x) if cfg.roundtrip else None
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        plan.forward(x, out=out)
+        if cfg.roundtrip:
+            plan.inverse(out, out=back)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    launches0 = oz.kernel_launches()
+    plan.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sampler = ClockSampler(local_rank)
+    torch.cuda.synchronize(dev)
+    with sampler:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = oz.kernel_launches() - launches0
+    prof = plan.profile_read()
+    plan.profile(False)
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if dist:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+        dist.barrier()
+    stats = plan.stats()
+    dirs = 2 if cfg.roundtrip else 1
+    total_transforms = world * B * dirs * args.steps
+    value = total_transforms * flops_per_transform(n) / (t_ms * 1e-3) / 1e9
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the region
+    xh = torch.from_numpy(x_np).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    zh = torch.empty_like(xh).pin_memory() if cfg.roundtrip else None
+
+    def e2e_step():
+        plan.execute_host(xh, -1, out_host=yh)
+        if cfg.roundtrip:
+            plan.execute_host(yh, +1, out_host=zh)
+
+    for _ in range(2):
+        e2e_step()
+    e2e_steps = max(3, min(args.steps, 10))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = world * B * dirs * e2e_steps * flops_per_transform(n) / e2e_s / 1e9
+    io_bytes = B * n * 16 * dirs
+
+    if rank != 0:
+        return
+    # ---- roofline of the dominant stage kernel (live CUDA-event times of the timed region)
+    m = plan.m
+    logR, logC = plan.log2_rows, plan.log2_cols
+    execs = args.steps * dirs
+    fwd_vec = stats["fwd_ntts"]  # forward NTT vectors of the last execute (whole batch)
+    inv_vec = stats["inv_ntts"]  # inverse NTT vectors (2 per Alg.8 group)
+    per_exec = {  # (bytes, butterflies) per execute over the batch -- DESIGN.md "Algorithmic work"
+        "split_max": (3 * 32 * n * B, 0),
+        "split_digits": (32 * n * B + 24 * n * B, 0),
+        "col_fwd": (fwd_vec * 4 * (n + m), fwd_vec * (m // 2) * logR),
+        "row_fused": (fwd_vec * 4 * m + inv_vec * 4 * m, (fwd_vec + inv_vec) * (m // 2) * logC),
+        "col_inv": (inv_vec * 4 * (m + n), inv_vec * (m // 2) * logR),
+        "crt_finish": (inv_vec * 4 * n + 32 * n * B, 0),
+    }
+    hbm, hbm_kind = hbm_peak()
+    stages = {}
+    for s, (ms, cnt) in prof.items():
+        if cnt == 0:
+            continue
+        ms_per_launch = ms / cnt
+        byts, bfly = per_exec[s]
+        launches_per_exec = cnt / execs
+        byts /= launches_per_exec
+        bfly /= launches_per_exec
+        gbs = byts / (ms_per_launch * 1e-3) / 1e9
+        gbf = bfly / (ms_per_launch * 1e-3) / 1e9
+        stages[s] = {"ms_per_launch": ms_per_launch, "share": ms / sum(v[0] for v in prof.values()),
+                     "GB_s": gbs, "frac_hbm": gbs / hbm, "Gbfly_s": gbf,
+                     "frac_alu": gbf / ALU_BFLY_PEAK_GPS, "launches": cnt}
+    dom = max(stages, key=lambda s: stages[s]["share"])
+    d = stages[dom]
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as f:
+                traffic = json.load(f).get(cfg.name, {}).get(dom)
+        except Exception:
+            traffic = None
+    if d["frac_alu"] >= d["frac_hbm"]:
+        roof = {"bound": "alu", "achieved": d["Gbfly_s"], "peak": ALU_BFLY_PEAK_GPS,
+                "unit": "Gbutterfly/s", "frac": d["frac_alu"], "traffic": traffic,
+                "peak_kind": "measured in-register Shoup butterfly rate (tools/microbench_int.cu)",
+                "kernel": dom, "hbm_GB_s": d["GB_s"], "hbm_frac": d["frac_hbm"]}
+    else:
+        roof = {"bound": "hbm", "achieved": d["GB_s"], "peak": hbm, "unit": "GB/s",
+                "frac": d["frac_hbm"], "traffic": traffic, "peak_kind": hbm_kind + " (MEASURED_PEAKS.json)",
+                "kernel": dom, "alu_Gbfly_s": d["Gbfly_s"], "alu_frac": d["frac_alu"]}
+
+    # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1 only
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cores = host_cores()
+        ntr = min(cfg.batch, cores)
+        ts, used, units = time_oracle(cfg, ntr)
+        cpu = {"value": units * flops_per_transform(n) / ts[0] / 1e9, "unit": UNIT, "cores": used,
+               "kind": "oracle",
+               "sample": f"{ntr} transforms of {cfg.name} ({'fwd+inv' if cfg.roundtrip else 'fwd'}), "
+                         f"{ts[0]:.1f} s wall, OpenMP over transforms"}
+    clocks = sampler.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg), "n": n, "m": m, "batch_per_gpu": B,
+                   "global_batch": world * B, "K": plan.K, "L": plan.L, "alpha": plan.alpha,
+                   "ntt_split": f"m = 2^{logR} x 2^{logC}", "parallelism": f"batch-sharded x{world}",
+                   "directions": "fwd+inv" if cfg.roundtrip else "fwd",
+                   "l2": "flushed between timed steps (512 MiB write outside the events)",
+                   "io_dtype": "complex128"},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
+                "d2h_bytes_per_step": io_bytes, "steps": e2e_steps},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "stages": stages,
+        "ntt_counts_per_transform": {"fwd": stats["fwd_ntts"] / B, "inv": stats["inv_ntts"] / B,
+                                     "cached": stats["cached_ntts"]},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    args = ap.parse_args()
+    cfg = workloads.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,25 @@ ozfft_status ozfft_shard_partial(const ozfft_plan* plan, int shard, int nshards,
 ozfft_status ozfft_shard_finish(const ozfft_plan* plan, const void* residues_all, void* out,
                                 int direction, void* stream);
 
+/* ---- profiling (tracing) -----------------------------------------------------------
+ * Per-stage CUDA-event timers.  While enabled, every execute records an event pair
+ * around each stage kernel on the execute stream (no host synchronization).
+ * ozfft_profile_read synchronizes `stream`, returns the summed milliseconds and the
+ * launch count of each stage since enable (or the previous read) and clears them.
+ * Stage ids: */
+#define OZFFT_STAGE_SPLIT_MAX 0    /* k_split_max: premultiply + per-level max (a1, a2) */
+#define OZFFT_STAGE_SPLIT_DIGITS 1 /* k_split_digits: digits + Alg.8 schedule (a2)     */
+#define OZFFT_STAGE_COL_FWD 2      /* k_col_fwd: forward NTT column pass (a3)          */
+#define OZFFT_STAGE_ROW_FUSED 3    /* k_row_fused: fwd rows + accumulate + inv rows (a3-a5) */
+#define OZFFT_STAGE_COL_INV 4      /* k_col_inv: inverse NTT column pass (a5)          */
+#define OZFFT_STAGE_CRT_FINISH 5   /* k_crt_finish: CRT + recombine + post-chirp (a6, a7) */
+#define OZFFT_NSTAGES 6
+ozfft_status ozfft_profile_enable(ozfft_plan* plan, int on);
+ozfft_status ozfft_profile_read(ozfft_plan* plan, double* ms, int64_t* launches, void* stream);
+
+/* Process-wide number of kernels this library has launched (all plans, all calls). */
+uint64_t ozfft_kernel_launches(void);
+
 /* Free the host plan (device buffers stay owned by the caller). */
 ozfft_status ozfft_plan_destroy(ozfft_plan* plan);
 

@@ -67,7 +67,9 @@ EXPORTS = ["ozfft_plan_create", "ozfft_plan_get_info", "ozfft_plan_bind", "ozfft
            "ozfft_execute_host", "ozfft_execute_taps", "ozfft_last_stats",
            "ozfft_shard_residue_bytes", "ozfft_shard_partial", "ozfft_shard_finish",
            "ozfft_plan_destroy", "ozfft_status_string", "ozfft_last_error_string",
-           "ozfft_version"]
+           "ozfft_version", "ozfft_profile_enable", "ozfft_profile_read", "ozfft_kernel_launches"]
+
+STAGES = ["split_max", "split_digits", "col_fwd", "row_fused", "col_inv", "crt_finish"]
 
 _lib = None
 
@@ -94,9 +96,14 @@ def load_library() -> C.CDLL:
     L.ozfft_shard_partial.argtypes = [vp, i32, i32, vp, i32, vp, vp]
     L.ozfft_shard_finish.argtypes = [vp, vp, vp, i32, vp]
     L.ozfft_plan_destroy.argtypes = [vp]
+    L.ozfft_profile_enable.argtypes = [vp, i32]
+    L.ozfft_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), vp]
+    L.ozfft_kernel_launches.argtypes = []
+    L.ozfft_kernel_launches.restype = u64
     for f in ("ozfft_plan_create", "ozfft_plan_get_info", "ozfft_plan_bind", "ozfft_execute",
               "ozfft_execute_host", "ozfft_execute_taps", "ozfft_last_stats",
-              "ozfft_shard_partial", "ozfft_shard_finish", "ozfft_plan_destroy"):
+              "ozfft_shard_partial", "ozfft_shard_finish", "ozfft_plan_destroy",
+              "ozfft_profile_enable", "ozfft_profile_read"):
         getattr(L, f).restype = C.c_int
     L.ozfft_status_string.argtypes = [C.c_int]
     L.ozfft_status_string.restype = C.c_char_p
@@ -115,6 +122,11 @@ def _check(status: int):
 
 def version() -> str:
     return load_library().ozfft_version().decode()
+
+
+def kernel_launches() -> int:
+    """Process-wide number of kernels libozfft.so has launched."""
+    return int(load_library().ozfft_kernel_launches())
 
 
 def _stream_ptr(stream) -> int:
@@ -227,6 +239,18 @@ class Plan:
         return dict(k=list(s.k), fwd_ntts=s.fwd_ntts, inv_ntts=s.inv_ntts,
                     cached_ntts=s.cached_ntts, groups=s.groups, nonfinite=s.nonfinite,
                     flags=s.flags)
+
+    # ------------------------------------------------------------------ profiling
+    def profile(self, on: bool = True):
+        """Enable/disable per-stage CUDA-event timers (OZFFT_STAGE_*)."""
+        _check(self._lib.ozfft_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self, stream=None) -> dict:
+        """{stage: (total_ms, launches)} since enable / last read (synchronizes)."""
+        ms = (C.c_double * len(STAGES))()
+        ln = (C.c_int64 * len(STAGES))()
+        _check(self._lib.ozfft_profile_read(self._h, ms, ln, _stream_ptr(stream)))
+        return {s: (ms[i], ln[i]) for i, s in enumerate(STAGES)}
 
     # ------------------------------------------------------------------ sharding
     def shard_residue_bytes(self) -> int:

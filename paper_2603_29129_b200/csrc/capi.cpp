@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <new>
 #include <string>
@@ -53,6 +54,27 @@ static int compute_alpha(int64_t n, int64_t L, uint32_t p0, uint32_t p1) {
     best = a;
   }
   return best;
+}
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+void prof_mark(const Plan& pl, int stage, bool begin, void* stream) {
+  Prof* pr = pl.prof;
+  if (!pr || !pr->on) return;
+  if (pr->next >= pr->pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    pr->pool.push_back((void*)e);
+  }
+  void* e = pr->pool[pr->next++];
+  cudaEventRecord((cudaEvent_t)e, (cudaStream_t)stream);
+  if (begin) {
+    pr->recs.push_back(Prof::Rec{stage, e, nullptr});
+  } else {
+    for (size_t i = pr->recs.size(); i-- > 0;)
+      if (pr->recs[i].stage == stage && pr->recs[i].e1 == nullptr) { pr->recs[i].e1 = e; break; }
+  }
 }
 
 static uint64_t align256(uint64_t v) { return (v + 255) & ~(uint64_t)255; }
@@ -396,7 +418,41 @@ ozfft_status ozfft_shard_finish(const ozfft_plan* pl, const void* residues_all, 
                                      reinterpret_cast<double*>(out), direction, stream);
 }
 
+ozfft_status ozfft_profile_enable(ozfft_plan* pl, int on) {
+  if (!pl) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null plan");
+  if (!pl->prof) pl->prof = new Prof();
+  pl->prof->on = on != 0;
+  pl->prof->recs.clear();
+  pl->prof->next = 0;
+  return OZFFT_OK;
+}
+
+ozfft_status ozfft_profile_read(ozfft_plan* pl, double* ms, int64_t* launches, void* stream) {
+  if (!pl || !ms || !launches) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null argument");
+  for (int i = 0; i < OZFFT_NSTAGES; ++i) { ms[i] = 0.0; launches[i] = 0; }
+  if (!pl->prof) return OZFFT_OK;
+  ozfft_status s = check_cuda(cudaStreamSynchronize((cudaStream_t)stream), "profile sync");
+  if (s) return s;
+  for (const Prof::Rec& r : pl->prof->recs) {
+    if (!r.e1) continue;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, (cudaEvent_t)r.e0, (cudaEvent_t)r.e1) == cudaSuccess) {
+      ms[r.stage] += t;
+      launches[r.stage] += 1;
+    }
+  }
+  pl->prof->recs.clear();
+  pl->prof->next = 0;
+  return OZFFT_OK;
+}
+
+uint64_t ozfft_kernel_launches(void) { return g_launches.load(); }
+
 ozfft_status ozfft_plan_destroy(ozfft_plan* pl) {
+  if (pl && pl->prof) {
+    for (void* e : pl->prof->pool) cudaEventDestroy((cudaEvent_t)e);
+    delete pl->prof;
+  }
   delete pl;
   return OZFFT_OK;
 }

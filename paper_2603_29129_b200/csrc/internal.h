@@ -54,7 +54,19 @@ struct Plan {
   int kw[2] = {0, 0};
   int32_t Ew[2][kMaxK] = {{0}};
   int64_t last_batch = 0;  // transforms covered by the per-batch stats arrays
+  struct Prof* prof = nullptr;  // profiling state (mutable through the pointer)
 };
+
+// Per-stage CUDA-event timers (ozfft_profile_*).
+struct Prof {
+  bool on = false;
+  std::vector<void*> pool;                     // cudaEvent_t
+  size_t next = 0;
+  struct Rec { int stage; void* e0; void* e1; };
+  std::vector<Rec> recs;
+};
+void prof_mark(const Plan& pl, int stage, bool begin, void* stream);
+void count_launches(int n);
 
 // Schedule row length per (transform, conv): ngroups + K*K groups of (cexp, npairs, L pairs)
 OZ_HD inline int sched_stride(int K, int L) { return 1 + K * K * (2 + 2 * L); }

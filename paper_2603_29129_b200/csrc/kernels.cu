@@ -780,9 +780,13 @@ static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cud
   if (blocks_per < 1) blocks_per = 1;
   if (blocks_per > 65535) blocks_per = 65535;
   dim3 grid((unsigned)blocks_per, (unsigned)nb);
+  prof_mark(pl, OZFFT_STAGE_SPLIT_MAX, true, st);
   for (int level = 0; level < SP.K; ++level) k_split_max<<<grid, threads, 0, st>>>(SP, level);
+  prof_mark(pl, OZFFT_STAGE_SPLIT_MAX, false, st);
+  prof_mark(pl, OZFFT_STAGE_SPLIT_DIGITS, true, st);
   k_split_digits<<<grid, threads, 0, st>>>(SP);
-  (void)pl;
+  prof_mark(pl, OZFFT_STAGE_SPLIT_DIGITS, false, st);
+  count_launches(SP.K + 1);
   return cuda_check("split kernels");
 }
 
@@ -970,7 +974,10 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.tw = tw; CP.digits = SP.digits; CP.in_len = n; CP.Y = Y; CP.stats = stats;
     CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n; CP.unit_mask = A.unit_mask;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4 * K;
+    prof_mark(pl, OZFFT_STAGE_COL_FWD, true, st);
     k_col_fwd<<<(unsigned)nblk, c.col_threads, c.col_smem, st>>>(CP);
+    prof_mark(pl, OZFFT_STAGE_COL_FWD, false, st);
+    count_launches(1);
     s = cuda_check("k_col_fwd");
     if (s) return s;
   }
@@ -981,7 +988,10 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   RP.unit_mask = A.unit_mask; RP.fwd_only = 0; RP.Xout = Xtap; RP.Zout = Ztap;
   {
     dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
+    prof_mark(pl, OZFFT_STAGE_ROW_FUSED, true, st);
     k_row_fused<<<grid, c.row_threads, c.row_smem, st>>>(RP);
+    prof_mark(pl, OZFFT_STAGE_ROW_FUSED, false, st);
+    count_launches(1);
     s = cuda_check("k_row_fused");
     if (s) return s;
   }
@@ -992,7 +1002,10 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.tw = tw; CP.stats = stats; CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n;
     CP.unit_mask = A.unit_mask;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 8 * G;
+    prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
     k_col_inv<<<(unsigned)nblk, c.col_threads, c.col_smem, st>>>(CP);
+    prof_mark(pl, OZFFT_STAGE_COL_INV, false, st);
+    count_launches(1);
     s = cuda_check("k_col_inv");
     if (s) return s;
   }
@@ -1003,7 +1016,10 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     FP.chirp = chirp; FP.out = reinterpret_cast<double2*>(A.out); FP.direction = A.direction;
     FP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)nb);
+    prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
     k_crt_finish<<<grid, 256, 0, st>>>(FP);
+    prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
+    count_launches(1);
     s = cuda_check("k_crt_finish");
     if (s) return s;
   }
@@ -1113,7 +1129,10 @@ ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, do
   FP.out = reinterpret_cast<double2*>(out);
   FP.direction = direction;
   dim3 grid((unsigned)((pl.n + 255) / 256), 1);
+  prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
   k_crt_finish<<<grid, 256, 0, st>>>(FP);
+  prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
+  count_launches(1);
   return cuda_check("k_crt_finish (shard)");
 }
 
