@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -326,95 +327,94 @@ __device__ __forceinline__ void dit_group(uint32_t* x, uint32_t rmod, uint32_t g
   }
 }
 
-template <bool INV, int S>
-__device__ __forceinline__ void groups_compute(uint32_t* x, int gpt, int tv, int Tv, int logstep,
-                                               uint32_t gb_mod, uint32_t gs,
-                                               const uint2* __restrict__ T, uint32_t p) {
-  const uint32_t step = 1u << logstep;
+__device__ __forceinline__ uint32_t pad_idx(uint32_t e) { return e + (e >> 4); }
+
+// Round structure of a length-2^LOGN sub-transform, fixed at compile time.  DIF rounds
+// run from the top (block length 2^lb, lb = LOGN, LOGN-4, ...), 4 radix-2 stages each
+// except a last partial round; DIT runs the same rounds in reverse order.
+template <int LOGN, bool INV, int R>
+struct RoundT {
+  static constexpr int nr = (LOGN + 3) / 4;
+  static constexpr int rd = INV ? (nr - 1 - R) : R;  // index in DIF order
+  static constexpr int lb = LOGN - 4 * rd;           // log2 block length
+  static constexpr int S = lb < 4 ? lb : 4;          // stages in the round
+  static constexpr int logstep = lb - S;
+  static constexpr int cnt = LOGN >= 4 ? 16 : (1 << LOGN);  // elements per thread
+  static constexpr int Tv = LOGN >= 4 ? (1 << (LOGN - 4)) : 1;
+};
+
+// Element index of register i of thread tv in round R.
+template <int LOGN, bool INV, int R>
+__device__ __forceinline__ uint32_t round_elem(int tv, int i) {
+  using RT = RoundT<LOGN, INV, R>;
+  const uint32_t g = (uint32_t)(tv + (i >> RT::S) * RT::Tv);
+  const uint32_t k = (uint32_t)(i & ((1 << RT::S) - 1));
+  return ((g >> RT::logstep) << RT::lb) + (g & ((1u << RT::logstep) - 1)) + (k << RT::logstep);
+}
+
+template <int LOGN, bool INV, int R, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[16], int tv, uint32_t* __restrict__ sm,
+                                              int Cb, uint32_t gb_mod, uint32_t gs,
+                                              const uint2* __restrict__ T, uint32_t p,
+                                              LoadF& load_first, StoreF& store_last) {
+  using RT = RoundT<LOGN, INV, R>;
+  constexpr uint32_t step = 1u << RT::logstep;
 #pragma unroll
-  for (int u = 0; u < 16 / (1 << S); ++u) {
-    if (u < gpt) {
-      const uint32_t g = (uint32_t)(tv + u * Tv);
-      const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
-      if (INV)
-        dit_group<S>(x + u * (1 << S), rmod, step * gs, T, p);
-      else
-        dif_group<S>(x + u * (1 << S), rmod, step * gs, T, p);
-    }
+  for (int i = 0; i < RT::cnt; ++i) {
+    const uint32_t e = round_elem<LOGN, INV, R>(tv, i);
+    if constexpr (R == 0)
+      x[i] = load_first(e);
+    else
+      x[i] = sm[pad_idx(e) * Cb];
+  }
+#pragma unroll
+  for (int u = 0; u < (RT::cnt >> RT::S); ++u) {
+    const uint32_t g = (uint32_t)(tv + u * RT::Tv);
+    const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
+    if constexpr (INV)
+      dit_group<RT::S>(x + u * (1 << RT::S), rmod, step * gs, T, p);
+    else
+      dif_group<RT::S>(x + u * (1 << RT::S), rmod, step * gs, T, p);
+  }
+#pragma unroll
+  for (int i = 0; i < RT::cnt; ++i) {
+    const uint32_t e = round_elem<LOGN, INV, R>(tv, i);
+    if constexpr (R == RT::nr - 1)
+      store_last(e, x[i]);
+    else
+      sm[pad_idx(e) * Cb] = x[i];
+  }
+  if constexpr (R != RT::nr - 1) __syncthreads();
+}
+
+template <int LOGN, bool INV, int R, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[16], int tv, uint32_t* __restrict__ sm,
+                                               int Cb, uint32_t gb_mod, uint32_t gs,
+                                               const uint2* __restrict__ T, uint32_t p,
+                                               LoadF& load_first, StoreF& store_last) {
+  if constexpr (R < RoundT<LOGN, INV, 0>::nr) {
+    sub_ntt_round<LOGN, INV, R>(x, tv, sm, Cb, gb_mod, gs, T, p, load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, R + 1>(x, tv, sm, Cb, gb_mod, gs, T, p, load_first, store_last);
   }
 }
 
-__device__ __forceinline__ uint32_t pad_idx(uint32_t e) { return e + (e >> 4); }
-
-// Length-N (N = 2^logN) sub-transform executed cooperatively by Tv threads (thread
-// index tv), 16 elements per thread per round (N >= 16) in rounds of <= 4 radix-2
-// stages, with shared memory (padded, interleave Cb) between rounds.
-//   INV = false: DIF stages len = N .. 2 (rounds from the top);
-//   INV = true : DIT stages len = 2 .. N.
+// Length-2^LOGN sub-transform executed cooperatively by 2^max(LOGN-4,0) threads (index
+// tv), 16 elements per thread per round (N >= 16) in rounds of <= 4 radix-2 stages, with
+// shared memory (padded, interleave Cb) between rounds.
+//   INV = false: DIF stages len = N .. 2;   INV = true: DIT stages len = 2 .. N.
 // Element e has global position gbase_vec + e*gs; gb_mod = gbase_vec mod (gs*step) for
 // every step used (0 for rows, the column index for columns).  load_first(e) gives the
 // round-0 input; store_last(e, v) consumes the final values.  `sm` must be free for
 // writes (caller-synchronised) on entry.
-template <bool INV, class LoadF, class StoreF>
-__device__ __forceinline__ void sub_ntt(int logN, int tv, int Tv, uint32_t* __restrict__ sm,
-                                        int Cb, uint32_t gb_mod, uint32_t gs,
-                                        const uint2* __restrict__ T, uint32_t p,
+template <int LOGN, bool INV, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, int Cb, uint32_t gb_mod,
+                                        uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                         LoadF&& load_first, StoreF&& store_last) {
-  int rS[8], rLB[8];  // stages and log2(block length) per round
-  int nr = 0;
-  for (int lb = logN; lb > 0;) {
-    const int S = lb < 4 ? lb : 4;
-    rS[nr] = S;
-    rLB[nr] = lb;
-    ++nr;
-    lb -= S;
-  }
-  if (INV) {
-    for (int i = 0; i < nr / 2; ++i) {
-      int t = rS[i]; rS[i] = rS[nr - 1 - i]; rS[nr - 1 - i] = t;
-      t = rLB[i]; rLB[i] = rLB[nr - 1 - i]; rLB[nr - 1 - i] = t;
-    }
-  }
-  uint32_t x[16];
-  if (nr == 0) {  // N == 1: identity
+  if constexpr (LOGN == 0) {  // N == 1: identity
     if (tv == 0) store_last(0u, load_first(0u));
-    return;
-  }
-  for (int r = 0; r < nr; ++r) {
-    const int S = rS[r], lb = rLB[r];
-    const int logstep = lb - S;
-    const int cnt = logN >= 4 ? 16 : (1 << logN);
-    const int gpt = cnt >> S;
-    // gather
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (i < cnt) {
-        const uint32_t g = (uint32_t)(tv + (i >> S) * Tv);
-        const uint32_t k = (uint32_t)(i & ((1 << S) - 1));
-        const uint32_t e = ((g >> logstep) << lb) + (g & ((1u << logstep) - 1)) + (k << logstep);
-        x[i] = (r == 0) ? load_first(e) : sm[pad_idx(e) * Cb];
-      }
-    }
-    switch (S) {
-      case 1: groups_compute<INV, 1>(x, gpt, tv, Tv, logstep, gb_mod, gs, T, p); break;
-      case 2: groups_compute<INV, 2>(x, gpt, tv, Tv, logstep, gb_mod, gs, T, p); break;
-      case 3: groups_compute<INV, 3>(x, gpt, tv, Tv, logstep, gb_mod, gs, T, p); break;
-      default: groups_compute<INV, 4>(x, gpt, tv, Tv, logstep, gb_mod, gs, T, p); break;
-    }
-    // scatter
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (i < cnt) {
-        const uint32_t g = (uint32_t)(tv + (i >> S) * Tv);
-        const uint32_t k = (uint32_t)(i & ((1 << S) - 1));
-        const uint32_t e = ((g >> logstep) << lb) + (g & ((1u << logstep) - 1)) + (k << logstep);
-        if (r == nr - 1)
-          store_last(e, x[i]);
-        else
-          sm[pad_idx(e) * Cb] = x[i];
-      }
-    }
-    if (r != nr - 1) __syncthreads();
+  } else {
+    uint32_t x[16];
+    sub_ntt_rounds<LOGN, INV, 0>(x, tv, sm, Cb, gb_mod, gs, T, p, load_first, store_last);
   }
 }
 
@@ -443,6 +443,7 @@ struct ColParams {
 };
 
 // Forward column pass: global DIF stages len = m .. 2C on columns of the R x C view.
+template <int LOGR>
 __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
   extern __shared__ uint32_t smem[];
   const int64_t ncb = 1ll << (P.logC - P.logCb);
@@ -461,8 +462,6 @@ __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
   const int Cb = 1 << P.logCb;
   const int c = threadIdx.x & (Cb - 1);
   const int tv = threadIdx.x >> P.logCb;
-  const int Tv = P.logR >= 4 ? (1 << (P.logR - 4)) : 1;
-  if (tv >= Tv) return;
   const uint32_t p = P.p[q];
   const uint32_t C = 1u << P.logC;
   const uint32_t col = (uint32_t)(cb << P.logCb) + c;
@@ -470,8 +469,8 @@ __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
   uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (1ll << P.logm);
   const uint2* T = P.tw + (size_t)(q * 2 + 0) * (1ull << P.logm);
   const int64_t in_len = P.in_len;
-  sub_ntt<false>(
-      P.logR, tv, Tv, smem + c, Cb, col, C, T, p,
+  sub_ntt<LOGR, false>(
+      tv, smem + c, Cb, col, C, T, p,
       [&](uint32_t e) -> uint32_t {
         const int64_t i = (int64_t)e * C + col;
         return i < in_len ? lift(__ldg(&D[i]), p) : 0u;
@@ -480,6 +479,7 @@ __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
 }
 
 // Inverse column pass: global DIT stages len = 2C .. m; writes rows i < n only.
+template <int LOGR>
 __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   extern __shared__ uint32_t smem[];
   const int64_t ncb = 1ll << (P.logC - P.logCb);
@@ -495,8 +495,6 @@ __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   const int Cb = 1 << P.logCb;
   const int c = threadIdx.x & (Cb - 1);
   const int tv = threadIdx.x >> P.logCb;
-  const int Tv = P.logR >= 4 ? (1 << (P.logR - 4)) : 1;
-  if (tv >= Tv) return;
   const uint32_t p = P.p[q];
   const uint32_t C = 1u << P.logC;
   const uint32_t col = (uint32_t)(cb << P.logCb) + c;
@@ -505,8 +503,8 @@ __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
   const uint2* T = P.tw + (size_t)(q * 2 + 1) * (1ull << P.logm);
   const int64_t n = P.n;
-  sub_ntt<true>(
-      P.logR, tv, Tv, smem + c, Cb, col, C, T, p,
+  sub_ntt<LOGR, true>(
+      tv, smem + c, Cb, col, C, T, p,
       [&](uint32_t e) -> uint32_t { return __ldg(&in[(int64_t)e * C + col]); },
       [&](uint32_t e, uint32_t val) {
         const int64_t i = (int64_t)e * C + col;
@@ -536,16 +534,16 @@ struct RowParams {
   uint32_t* Zout;         // tap: [nb][2 q][4][K*K][m] (internal order, W m^{-1} scaled)
 };
 
+template <int LOGC>
 __global__ void __launch_bounds__(256) k_row_fused(RowParams P) {
   extern __shared__ uint32_t smem[];
   const int64_t b = blockIdx.x;
   const int a = blockIdx.y & 1;
   const int q = (blockIdx.y >> 1) & 1;
   const uint32_t row = blockIdx.y >> 2;
-  const int logC = P.logC;
-  const uint32_t C = 1u << logC;
-  const uint32_t padC = C + (C >> 4) + 1;
-  const int Tv = logC >= 4 ? (1 << (logC - 4)) : 1;
+  constexpr int logC = LOGC;
+  constexpr uint32_t C = 1u << logC;
+  constexpr uint32_t padC = C + (C >> 4) + 1;
   const int tv = threadIdx.x;
   const int64_t m = 1ll << P.logm;
   const uint32_t p = P.p[q];
@@ -573,8 +571,8 @@ __global__ void __launch_bounds__(256) k_row_fused(RowParams P) {
     uint32_t* outX = P.Xout ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff : nullptr;
     if (P.logR > 0) {
       const uint32_t* y = P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff;
-      sub_ntt<false>(
-          logC, tv, Tv, work + buf * padC, 1, 0u, 1u, Tf, p,
+      sub_ntt<LOGC, false>(
+          tv, work + buf * padC, 1, 0u, 1u, Tf, p,
           [&](uint32_t e) -> uint32_t { return __ldg(&y[e]); },
           [&](uint32_t e, uint32_t v) {
             xs[pad_idx(e)] = v;
@@ -583,8 +581,8 @@ __global__ void __launch_bounds__(256) k_row_fused(RowParams P) {
     } else {
       const int32_t* D = P.digits + ((b * 2 + a) * K + s) * P.in_len;
       const int64_t in_len = P.in_len;
-      sub_ntt<false>(
-          logC, tv, Tv, work + buf * padC, 1, 0u, 1u, Tf, p,
+      sub_ntt<LOGC, false>(
+          tv, work + buf * padC, 1, 0u, 1u, Tf, p,
           [&](uint32_t e) -> uint32_t { return (int64_t)e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
           [&](uint32_t e, uint32_t v) {
             xs[pad_idx(e)] = v;
@@ -605,25 +603,33 @@ __global__ void __launch_bounds__(256) k_row_fused(RowParams P) {
     for (int g = 0; g < ng; ++g) {
       const int32_t* grp = srow + 1 + g * (2 + 2 * L);
       const int np = grp[1];
+      // the group's (s, t) pairs, hoisted: X_s row in shared memory, W_t row in global
+      const uint32_t* xp[kMaxL];
+      const uint2* wp[kMaxL];
+#pragma unroll
+      for (int i = 0; i < kMaxL; ++i) {
+        if (i < np) {
+          xp[i] = Xs + grp[2 + 2 * i] * padC;
+          wp[i] = P.W + ((size_t)(q * 2 + bw) * K + grp[3 + 2 * i]) * m + rowoff;
+        }
+      }
       uint32_t* Zt = P.Zout ? P.Zout + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff : nullptr;
       auto load_z = [&](uint32_t e) -> uint32_t {
         uint32_t z = 0;
-        for (int i = 0; i < np; ++i) {
-          const int s = grp[2 + 2 * i], t = grp[3 + 2 * i];
-          const uint2 w = __ldg(&P.W[((size_t)(q * 2 + bw) * K + t) * m + rowoff + e]);
-          z = add_mod(z, mul_shoup(Xs[s * padC + pad_idx(e)], w, p), p);
-        }
+#pragma unroll
+        for (int i = 0; i < kMaxL; ++i)
+          if (i < np) z = add_mod(z, mul_shoup(xp[i][pad_idx(e)], __ldg(&wp[i][e]), p), p);
         if (Zt) Zt[e] = z;
         return z;
       };
       if (P.logR > 0) {
         uint32_t* gout = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
-        sub_ntt<true>(logC, tv, Tv, work + buf * padC, 1, 0u, 1u, Ti, p, load_z,
-                      [&](uint32_t e, uint32_t v) { gout[e] = v; });
+        sub_ntt<LOGC, true>(tv, work + buf * padC, 1, 0u, 1u, Ti, p, load_z,
+                            [&](uint32_t e, uint32_t v) { gout[e] = v; });
       } else {
         uint32_t* rout = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
         const int64_t n = P.n;
-        sub_ntt<true>(logC, tv, Tv, work + buf * padC, 1, 0u, 1u, Ti, p, load_z,
+        sub_ntt<LOGC, true>(tv, work + buf * padC, 1, 0u, 1u, Ti, p, load_z,
                       [&](uint32_t e, uint32_t v) {
                         if ((int64_t)e < n) rout[e] = v;
                       });
@@ -637,7 +643,8 @@ __global__ void __launch_bounds__(256) k_row_fused(RowParams P) {
 struct FinishParams {
   int64_t n, nb;
   int K, L;
-  uint32_t p0, p1, p0inv;   // p0^{-1} mod p1
+  uint32_t p0, p1, p0inv, p0inv_sh;  // p0^{-1} mod p1 and its Shoup companion
+  unsigned long long P, halfP;       // p0 p1 and (p0 p1 - 1) / 2
   const uint32_t* res;      // [nb][4][2][K*K][n]
   const int32_t* stats;
   const int32_t* sched;
@@ -647,28 +654,33 @@ struct FinishParams {
   int64_t* crt_tap;         // [nb][4][K*K][n] or null
 };
 
-// symmetric residue of z in [0, p): z or z - p, in [-(p-1)/2, (p-1)/2]
-__device__ __forceinline__ int64_t sym_res(uint32_t z, uint32_t p) {
-  return z > (p >> 1) ? (int64_t)z - (int64_t)p : (int64_t)z;
-}
-
-// Garner, two primes (Alg.8 l.974): the unique Z in [-p0p1/2, p0p1/2).
-__device__ __forceinline__ long long garner2(uint32_t z0, uint32_t z1, uint32_t p0, uint32_t p1,
-                                             uint32_t inv) {
-  const int64_t z0s = sym_res(z0, p0);
-  // (z1 - z0s) mod p1 in [0, p1): z0s in (-p0/2, p0/2), p0 < 2 p1
-  int64_t d = (int64_t)z1 - z0s;
-  d %= (int64_t)p1;
-  if (d < 0) d += p1;
-  const uint32_t t = (uint32_t)(((uint64_t)d * inv) % p1);
-  return (long long)(z0s + sym_res(t, p1) * (int64_t)p0);
+// Garner, two primes (Alg.8 l.974): Z' = z0 + p0 ((z1 - z0) p0^{-1} mod p1)
+// in [0, p0 p1), then the symmetric representative in [-p0p1/2, p0p1/2) (
+// it is unique, so this equals the symmetric-Garner form of the oracle).
+__device__ __forceinline__ long long garner2(uint32_t z0, uint32_t z1, const FinishParams& P) {
+  const uint32_t z0r = z0 >= P.p1 ? z0 - P.p1 : z0;  // z0 mod p1 (z0 < p0 < 2 p1)
+  const uint32_t d = sub_mod(z1, z0r, P.p1);
+  const uint32_t t = mul_shoup(d, make_uint2(P.p0inv, P.p0inv_sh), P.p1);
+  const unsigned long long Zp = (unsigned long long)z0 + (unsigned long long)P.p0 * t;
+  return Zp > P.halfP ? (long long)(Zp - P.P) : (long long)Zp;
 }
 
 __global__ void __launch_bounds__(256) k_crt_finish(FinishParams P) {
   const int64_t b = blockIdx.y;
+  const int K = P.K, L = P.L, G = K * K;
+  // per-transform schedule: group counts and exact scales 2^-cexp (l.975), in smem
+  __shared__ int s_ng[4];
+  __shared__ double s_sc[4][kMaxK * kMaxK];
+  if (threadIdx.x < 4) {
+    const int cv = threadIdx.x;
+    const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
+    const int ng = srow[0];
+    s_ng[cv] = ng;
+    for (int g = 0; g < ng; ++g) s_sc[cv][g] = scalbn(1.0, -srow[1 + g * (2 + 2 * L)]);
+  }
+  __syncthreads();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.n) return;
-  const int K = P.K, L = P.L, G = K * K;
   const int32_t* st = P.stats + b * stats_stride(K);
   double2 o;
   if (st[2 + 2 * K] & 1) {
@@ -678,20 +690,19 @@ __global__ void __launch_bounds__(256) k_crt_finish(FinishParams P) {
     return;
   }
   double Sh[4], Sl[4];
+#pragma unroll
   for (int cv = 0; cv < 4; ++cv) {
     double sh = 0.0, sl = 0.0;
-    const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
-    const int ng = srow[0];
+    const int ng = s_ng[cv];
     const uint32_t* r0 = P.res + (((b * 4 + cv) * 2 + 0) * G) * P.n + j;
     const uint32_t* r1 = P.res + (((b * 4 + cv) * 2 + 1) * G) * P.n + j;
     for (int g = 0; g < ng; ++g) {
-      const int cexp = srow[1 + g * (2 + 2 * L)];
-      const long long Z = garner2(__ldg(&r0[g * P.n]), __ldg(&r1[g * P.n]), P.p0, P.p1, P.p0inv);
+      const long long Z = garner2(__ldcs(&r0[g * P.n]), __ldcs(&r1[g * P.n]), P);
       if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + j] = Z;
       const double h = __ll2double_rn(Z);
       const double l = __ll2double_rn(Z - __double2ll_rz(h));
-      const double sc = scalbn(1.0, -cexp);  // z' / c, exact (l.975)
-      dd_add(sh, sl, __dmul_rn(h, sc), __dmul_rn(l, sc), sh, sl);
+      const double sc = s_sc[cv][g];  // z' / c, exact power of two (l.975)
+      dd_add(sh, sl, __dmul_rn(h, sc), __dmul_rn(l, sc), sh, sl);  // flush order (l.976)
     }
     Sh[cv] = sh;
     Sl[cv] = sl;
@@ -715,6 +726,15 @@ __global__ void __launch_bounds__(256) k_crt_finish(FinishParams P) {
   o.x = ore;
   o.y = oim;
   P.out[b * P.n + j] = o;
+}
+
+static void fill_crt_consts(const Plan& pl, FinishParams& FP) {
+  FP.p0 = pl.p[0];
+  FP.p1 = pl.p[1];
+  FP.p0inv = pl.p0inv_mod_p1;
+  FP.p0inv_sh = (uint32_t)(((uint64_t)pl.p0inv_mod_p1 << 32) / pl.p[1]);
+  FP.P = (unsigned long long)pl.p[0] * pl.p[1];
+  FP.halfP = (FP.P - 1) / 2;
 }
 
 // ============================================================== small utility kernels
@@ -809,18 +829,42 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   return c;
 }
 
-static ozfft_status set_smem_attrs(const NttLaunch& c) {
-  static size_t done_col = 0, done_row = 0;
-  if (c.col_smem > 48 * 1024 && c.col_smem > done_col) {
-    cudaFuncSetAttribute(k_col_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.col_smem);
-    cudaFuncSetAttribute(k_col_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.col_smem);
-    done_col = c.col_smem;
+// Compile-time dispatch of the log2 sub-transform length (row: 0..12, column: 1..8).
+template <int LO, int HI, class F>
+static void dispatch_log(int v, F&& f) {
+  if constexpr (LO <= HI) {
+    if (v == LO)
+      f(std::integral_constant<int, LO>{});
+    else
+      dispatch_log<LO + 1, HI>(v, f);
   }
-  if (c.row_smem > 48 * 1024 && c.row_smem > done_row) {
-    cudaFuncSetAttribute(k_row_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.row_smem);
-    done_row = c.row_smem;
-  }
-  return cuda_check("cudaFuncSetAttribute");
+}
+
+template <class K>
+static void set_smem(K kern, size_t bytes) {
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+static void launch_col_fwd(int logR, unsigned nblk, const NttLaunch& c, cudaStream_t st,
+                           const ColParams& CP) {
+  dispatch_log<1, 8>(logR, [&](auto I) {
+    set_smem(k_col_fwd<I.value>, c.col_smem);
+    k_col_fwd<I.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
+  });
+}
+static void launch_col_inv(int logR, unsigned nblk, const NttLaunch& c, cudaStream_t st,
+                           const ColParams& CP) {
+  dispatch_log<1, 8>(logR, [&](auto I) {
+    set_smem(k_col_inv<I.value>, c.col_smem);
+    k_col_inv<I.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
+  });
+}
+static void launch_row(int logC, dim3 grid, const NttLaunch& c, cudaStream_t st, const RowParams& RP) {
+  dispatch_log<0, 12>(logC, [&](auto I) {
+    set_smem(k_row_fused<I.value>, c.row_smem);
+    k_row_fused<I.value><<<grid, c.row_threads, c.row_smem, st>>>(RP);
+  });
 }
 
 // Forward NTT of digit vectors [nb][2][K][in_len] into internal-order spectra Xout
@@ -829,8 +873,6 @@ static ozfft_status launch_forward_only(const Plan& pl, const int32_t* digits, i
                                         const int32_t* stats, uint32_t* Y, uint32_t* Xout,
                                         int64_t nb, cudaStream_t st) {
   const NttLaunch c = ntt_launch_cfg(pl);
-  ozfft_status s = set_smem_attrs(c);
-  if (s) return s;
   const uint2* tw = reinterpret_cast<const uint2*>(pl.pers + pl.poff.tw);
   if (pl.logR > 0) {
     ColParams CP{};
@@ -839,14 +881,14 @@ static ozfft_status launch_forward_only(const Plan& pl, const int32_t* digits, i
     CP.tw = tw; CP.digits = digits; CP.in_len = in_len; CP.Y = Y; CP.stats = stats;
     CP.unit_mask = 0xFF;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4 * pl.K;
-    k_col_fwd<<<(unsigned)nblk, c.col_threads, c.col_smem, st>>>(CP);
+    launch_col_fwd(pl.logR, (unsigned)nblk, c, st, CP);
   }
   RowParams RP{};
   RP.logm = pl.logm; RP.logC = pl.logC; RP.logR = pl.logR; RP.nb = nb; RP.K = pl.K; RP.L = pl.L;
   RP.p[0] = pl.p[0]; RP.p[1] = pl.p[1]; RP.tw = tw; RP.digits = digits; RP.in_len = in_len;
   RP.Y = Y; RP.stats = stats; RP.unit_mask = 0xFF; RP.fwd_only = 1; RP.Xout = Xout;
   dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
-  k_row_fused<<<grid, c.row_threads, c.row_smem, st>>>(RP);
+  launch_row(pl.logC, grid, c, st, RP);
   return cuda_check("forward-only NTT");
 }
 
@@ -957,8 +999,6 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   ozfft_status s = launch_split(pl, SP, nb, st);
   if (s) return s;
   const NttLaunch c = ntt_launch_cfg(pl);
-  s = set_smem_attrs(c);
-  if (s) return s;
   uint32_t* Xtap = nullptr;
   uint32_t* Ztap = nullptr;
   if (taps && (taps->X || taps->Z)) {
@@ -975,7 +1015,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n; CP.unit_mask = A.unit_mask;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4 * K;
     prof_mark(pl, OZFFT_STAGE_COL_FWD, true, st);
-    k_col_fwd<<<(unsigned)nblk, c.col_threads, c.col_smem, st>>>(CP);
+    launch_col_fwd(pl.logR, (unsigned)nblk, c, st, CP);
     prof_mark(pl, OZFFT_STAGE_COL_FWD, false, st);
     count_launches(1);
     s = cuda_check("k_col_fwd");
@@ -989,7 +1029,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   {
     dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
     prof_mark(pl, OZFFT_STAGE_ROW_FUSED, true, st);
-    k_row_fused<<<grid, c.row_threads, c.row_smem, st>>>(RP);
+    launch_row(pl.logC, grid, c, st, RP);
     prof_mark(pl, OZFFT_STAGE_ROW_FUSED, false, st);
     count_launches(1);
     s = cuda_check("k_row_fused");
@@ -1003,7 +1043,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.unit_mask = A.unit_mask;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 8 * G;
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
-    k_col_inv<<<(unsigned)nblk, c.col_threads, c.col_smem, st>>>(CP);
+    launch_col_inv(pl.logR, (unsigned)nblk, c, st, CP);
     prof_mark(pl, OZFFT_STAGE_COL_INV, false, st);
     count_launches(1);
     s = cuda_check("k_col_inv");
@@ -1011,8 +1051,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   }
   if (A.finish) {
     FinishParams FP{};
-    FP.n = n; FP.nb = nb; FP.K = K; FP.L = L; FP.p0 = pl.p[0]; FP.p1 = pl.p[1];
-    FP.p0inv = pl.p0inv_mod_p1; FP.res = res; FP.stats = stats; FP.sched = sched;
+    FP.n = n; FP.nb = nb; FP.K = K; FP.L = L; fill_crt_consts(pl, FP); FP.res = res; FP.stats = stats; FP.sched = sched;
     FP.chirp = chirp; FP.out = reinterpret_cast<double2*>(A.out); FP.direction = A.direction;
     FP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)nb);
@@ -1121,8 +1160,7 @@ ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, do
                                          int direction, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   FinishParams FP{};
-  FP.n = pl.n; FP.nb = 1; FP.K = pl.K; FP.L = pl.L; FP.p0 = pl.p[0]; FP.p1 = pl.p[1];
-  FP.p0inv = pl.p0inv_mod_p1; FP.res = res;
+  FP.n = pl.n; FP.nb = 1; FP.K = pl.K; FP.L = pl.L; fill_crt_consts(pl, FP); FP.res = res;
   FP.stats = reinterpret_cast<const int32_t*>(pl.ws + pl.woff.stats);
   FP.sched = reinterpret_cast<const int32_t*>(pl.ws + pl.woff.sched);
   FP.chirp = reinterpret_cast<const double2*>(pl.pers + pl.poff.chirp);
