@@ -442,16 +442,28 @@ struct ColParams {
   uint32_t unit_mask;
 };
 
+// Column tile geometry: R x Cb columns with R*Cb/16 = 256 threads (Cb >= 8 so that each
+// row segment is at least one 32-byte sector).
+__host__ __device__ constexpr int col_log_cb(int logR, int logC) {
+  return (logR >= 4 ? (12 - logR < 3 ? 3 : 12 - logR) : 8) > logC
+             ? logC
+             : (logR >= 4 ? (12 - logR < 3 ? 3 : 12 - logR) : 8);
+}
+
 // Forward column pass: global DIF stages len = m .. 2C on columns of the R x C view.
-template <int LOGR>
+template <int LOGR, int LOGC>
 __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
   extern __shared__ uint32_t smem[];
-  const int64_t ncb = 1ll << (P.logC - P.logCb);
-  const int64_t cb = blockIdx.x % ncb;
-  int64_t v = blockIdx.x / ncb;  // ((b * 2 + q) * 2 + a) * K + s
+  constexpr int LOGCB = col_log_cb(LOGR, LOGC);
+  constexpr int Cb = 1 << LOGCB;
+  constexpr uint32_t C = 1u << LOGC;
+  constexpr uint32_t m = 1u << (LOGR + LOGC);
+  constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
+  const uint32_t cb = blockIdx.x % ncb;
+  uint32_t v = blockIdx.x / ncb;  // ((b * 2 + q) * 2 + a) * K + s
   const int s = (int)(v % P.K); v /= P.K;
-  const int a = (int)(v % 2); v /= 2;
-  const int q = (int)(v % 2); v /= 2;
+  const int a = (int)(v & 1); v >>= 1;
+  const int q = (int)(v & 1); v >>= 1;
   const int64_t b = v;
   const int32_t* st = P.stats + b * stats_stride(P.K);
   if (s >= st[a]) return;  // slice does not exist (k_a <= s) or transform non-finite
@@ -459,56 +471,51 @@ __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
   const uint32_t need = a == 0 ? ((1u << (0 * 2 + q)) | (1u << (3 * 2 + q)))
                                : ((1u << (1 * 2 + q)) | (1u << (2 * 2 + q)));
   if (!(P.unit_mask & need)) return;
-  const int Cb = 1 << P.logCb;
   const int c = threadIdx.x & (Cb - 1);
-  const int tv = threadIdx.x >> P.logCb;
-  const uint32_t p = P.p[q];
-  const uint32_t C = 1u << P.logC;
-  const uint32_t col = (uint32_t)(cb << P.logCb) + c;
-  const int32_t* D = P.digits + ((b * 2 + a) * P.K + s) * P.in_len;
-  uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (1ll << P.logm);
-  const uint2* T = P.tw + (size_t)(q * 2 + 0) * (1ull << P.logm);
-  const int64_t in_len = P.in_len;
+  const int tv = threadIdx.x >> LOGCB;
+  const uint32_t p = q ? P.p[1] : P.p[0];  // no dynamic param-array index (local memory)
+  const uint32_t col = (cb << LOGCB) + c;
+  const int32_t* D = P.digits + ((b * 2 + a) * P.K + s) * P.in_len + col;
+  uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (int64_t)m + col;
+  const uint2* T = P.tw + (size_t)(q * 2 + 0) * m;
+  const uint32_t lim = P.in_len > col ? (uint32_t)(P.in_len - col) : 0u;  // e*C < lim <=> i < in_len
   sub_ntt<LOGR, false>(
       tv, smem + c, Cb, col, C, T, p,
-      [&](uint32_t e) -> uint32_t {
-        const int64_t i = (int64_t)e * C + col;
-        return i < in_len ? lift(__ldg(&D[i]), p) : 0u;
-      },
-      [&](uint32_t e, uint32_t val) { out[(int64_t)e * C + col] = val; });
+      [&](uint32_t e) -> uint32_t { return e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u; },
+      [&](uint32_t e, uint32_t val) { out[e * C] = val; });
 }
 
 // Inverse column pass: global DIT stages len = 2C .. m; writes rows i < n only.
-template <int LOGR>
+template <int LOGR, int LOGC>
 __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   extern __shared__ uint32_t smem[];
-  const int64_t ncb = 1ll << (P.logC - P.logCb);
+  constexpr int LOGCB = col_log_cb(LOGR, LOGC);
+  constexpr int Cb = 1 << LOGCB;
+  constexpr uint32_t C = 1u << LOGC;
+  constexpr uint32_t m = 1u << (LOGR + LOGC);
+  constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
   const int G = P.K * P.K;
-  const int64_t cb = blockIdx.x % ncb;
-  int64_t v = blockIdx.x / ncb;  // ((b * 2 + q) * 4 + cv) * G + g
+  const uint32_t cb = blockIdx.x % ncb;
+  uint32_t v = blockIdx.x / ncb;  // ((b * 2 + q) * 4 + cv) * G + g
   const int g = (int)(v % G); v /= G;
-  const int cv = (int)(v % 4); v /= 4;
-  const int q = (int)(v % 2); v /= 2;
+  const int cv = (int)(v & 3); v >>= 2;
+  const int q = (int)(v & 1); v >>= 1;
   const int64_t b = v;
   if (!(P.unit_mask & (1u << (cv * 2 + q)))) return;
   if (g >= P.sched[(b * 4 + cv) * sched_stride(P.K, P.L)]) return;
-  const int Cb = 1 << P.logCb;
   const int c = threadIdx.x & (Cb - 1);
-  const int tv = threadIdx.x >> P.logCb;
-  const uint32_t p = P.p[q];
-  const uint32_t C = 1u << P.logC;
-  const uint32_t col = (uint32_t)(cb << P.logCb) + c;
-  const int64_t m = 1ll << P.logm;
-  const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m;
-  uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
-  const uint2* T = P.tw + (size_t)(q * 2 + 1) * (1ull << P.logm);
-  const int64_t n = P.n;
+  const int tv = threadIdx.x >> LOGCB;
+  const uint32_t p = q ? P.p[1] : P.p[0];  // no dynamic param-array index (local memory)
+  const uint32_t col = (cb << LOGCB) + c;
+  const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * (int64_t)m + col;
+  uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
+  const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
+  const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
   sub_ntt<LOGR, true>(
       tv, smem + c, Cb, col, C, T, p,
-      [&](uint32_t e) -> uint32_t { return __ldg(&in[(int64_t)e * C + col]); },
+      [&](uint32_t e) -> uint32_t { return __ldg(&in[e * C]); },
       [&](uint32_t e, uint32_t val) {
-        const int64_t i = (int64_t)e * C + col;
-        if (i < n) out[i] = val;
+        if (e * C < lim) out[e * C] = val;
       });
 }
 
@@ -535,8 +542,16 @@ struct RowParams {
 };
 
 template <int LOGC>
-__global__ void __launch_bounds__(256) k_row_fused(RowParams P) {
+struct RowCfg {
+  static constexpr int threads = LOGC >= 4 ? (1 << (LOGC - 4)) : 1;
+  static constexpr int min_blocks = LOGC == 11 ? 6 : 1;
+};
+
+template <int LOGC>
+__global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_blocks)
+    k_row_fused(RowParams P) {
   extern __shared__ uint32_t smem[];
+  __shared__ int s_ng[2];
   const int64_t b = blockIdx.x;
   const int a = blockIdx.y & 1;
   const int q = (blockIdx.y >> 1) & 1;
@@ -546,33 +561,50 @@ __global__ void __launch_bounds__(256) k_row_fused(RowParams P) {
   constexpr uint32_t padC = C + (C >> 4) + 1;
   const int tv = threadIdx.x;
   const int64_t m = 1ll << P.logm;
-  const uint32_t p = P.p[q];
+  const uint32_t p = q ? P.p[1] : P.p[0];
   const int K = P.K, L = P.L, G = K * K;
   const int32_t* st = P.stats + b * stats_stride(K);
   const int ka = st[a];
   // convolutions using part a: a = 0 -> rr (0), ri (3); a = 1 -> ii (1), ir (2)
-  const int cvs[2] = {a == 0 ? 0 : 1, a == 0 ? 3 : 2};
-  bool want[2];
-  for (int i = 0; i < 2; ++i) want[i] = (P.unit_mask >> (cvs[i] * 2 + q)) & 1u;
-  if (!P.fwd_only && !want[0] && !want[1]) return;
-  if (ka == 0 && !P.fwd_only) {
-    // nothing to convolve; the schedule has no groups for these convolutions
-    return;
+  const int cv0 = a == 0 ? 0 : 1, cv1 = a == 0 ? 3 : 2;
+  const bool want0 = (P.unit_mask >> (cv0 * 2 + q)) & 1u;
+  const bool want1 = (P.unit_mask >> (cv1 * 2 + q)) & 1u;
+  if (!P.fwd_only && !want0 && !want1) return;
+  if (ka == 0 && !P.fwd_only) return;  // no slices: the schedule has no groups here
+  uint32_t* Xs = smem;              // [K][padC]: forward spectra rows of the K slices
+  uint32_t* work = smem + K * padC;  // [padC]: inter-round exchange buffer
+  // group table for 2 convs x K*K groups: npairs, then (X row offset, W row index) x L
+  uint32_t* tab = work + padC;
+  const int tstride = 1 + 2 * L;
+  if (!P.fwd_only && tv < 2) {
+    const int ci = tv;
+    const int cv = ci ? cv1 : cv0;
+    const bool want = ci ? want1 : want0;
+    const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
+    const int ng = want ? srow[0] : 0;
+    s_ng[ci] = ng;
+    for (int g = 0; g < ng; ++g) {
+      const int32_t* grp = srow + 1 + g * (2 + 2 * L);
+      uint32_t* tg = tab + (ci * G + g) * tstride;
+      tg[0] = (uint32_t)grp[1];
+      for (int i = 0; i < grp[1]; ++i) {
+        tg[1 + 2 * i] = (uint32_t)grp[2 + 2 * i] * padC;
+        tg[2 + 2 * i] = (uint32_t)grp[3 + 2 * i] * (uint32_t)m;
+      }
+    }
   }
-  uint32_t* Xs = smem;                 // [K][padC]
-  uint32_t* work = smem + K * padC;    // 2 x [padC]
   const uint2* Tf = P.tw + (size_t)(q * 2 + 0) * m;
   const uint2* Ti = P.tw + (size_t)(q * 2 + 1) * m;
   const uint32_t rowoff = row << logC;
-  int buf = 0;
   // ---- forward: last log2(C) DIF stages of each slice's NTT (Alg.6 l.787)
   for (int s = 0; s < ka; ++s) {
     uint32_t* xs = Xs + s * padC;
     uint32_t* outX = P.Xout ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff : nullptr;
+    __syncthreads();  // `work` is free (previous sub-transform's last reads are done)
     if (P.logR > 0) {
       const uint32_t* y = P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff;
       sub_ntt<LOGC, false>(
-          tv, work + buf * padC, 1, 0u, 1u, Tf, p,
+          tv, work, 1, 0u, 1u, Tf, p,
           [&](uint32_t e) -> uint32_t { return __ldg(&y[e]); },
           [&](uint32_t e, uint32_t v) {
             xs[pad_idx(e)] = v;
@@ -580,61 +612,49 @@ __global__ void __launch_bounds__(256) k_row_fused(RowParams P) {
           });
     } else {
       const int32_t* D = P.digits + ((b * 2 + a) * K + s) * P.in_len;
-      const int64_t in_len = P.in_len;
+      const uint32_t in_len = (uint32_t)P.in_len;
       sub_ntt<LOGC, false>(
-          tv, work + buf * padC, 1, 0u, 1u, Tf, p,
-          [&](uint32_t e) -> uint32_t { return (int64_t)e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
+          tv, work, 1, 0u, 1u, Tf, p,
+          [&](uint32_t e) -> uint32_t { return e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
           [&](uint32_t e, uint32_t v) {
             xs[pad_idx(e)] = v;
             if (outX) outX[e] = v;
           });
     }
-    buf ^= 1;
   }
   if (P.fwd_only) return;
-  __syncthreads();
   // ---- per group: Z = sum X_s (.) W_t (Alg.8 l.981-982), then first DIT stages
   for (int ci = 0; ci < 2; ++ci) {
-    if (!want[ci]) continue;
-    const int cv = cvs[ci];
+    const int cv = ci ? cv1 : cv0;
     const int bw = conv_b(cv);
-    const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
-    const int ng = srow[0];
+    __syncthreads();  // group table visible; `work` free
+    const int ng = s_ng[ci];
+    const uint2* Wb = P.W + (size_t)(q * 2 + bw) * K * m + rowoff;
     for (int g = 0; g < ng; ++g) {
-      const int32_t* grp = srow + 1 + g * (2 + 2 * L);
-      const int np = grp[1];
-      // the group's (s, t) pairs, hoisted: X_s row in shared memory, W_t row in global
-      const uint32_t* xp[kMaxL];
-      const uint2* wp[kMaxL];
-#pragma unroll
-      for (int i = 0; i < kMaxL; ++i) {
-        if (i < np) {
-          xp[i] = Xs + grp[2 + 2 * i] * padC;
-          wp[i] = P.W + ((size_t)(q * 2 + bw) * K + grp[3 + 2 * i]) * m + rowoff;
-        }
-      }
+      if (g > 0) __syncthreads();
+      const uint32_t* tg = tab + (ci * G + g) * tstride;
+      const int np = (int)tg[0];
       uint32_t* Zt = P.Zout ? P.Zout + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff : nullptr;
       auto load_z = [&](uint32_t e) -> uint32_t {
         uint32_t z = 0;
-#pragma unroll
-        for (int i = 0; i < kMaxL; ++i)
-          if (i < np) z = add_mod(z, mul_shoup(xp[i][pad_idx(e)], __ldg(&wp[i][e]), p), p);
+        const uint32_t pe = pad_idx(e);
+        for (int i = 0; i < np; ++i)
+          z = add_mod(z, mul_shoup(Xs[tg[1 + 2 * i] + pe], __ldg(&Wb[tg[2 + 2 * i] + e]), p), p);
         if (Zt) Zt[e] = z;
         return z;
       };
       if (P.logR > 0) {
         uint32_t* gout = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
-        sub_ntt<LOGC, true>(tv, work + buf * padC, 1, 0u, 1u, Ti, p, load_z,
+        sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
                             [&](uint32_t e, uint32_t v) { gout[e] = v; });
       } else {
         uint32_t* rout = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
-        const int64_t n = P.n;
-        sub_ntt<LOGC, true>(tv, work + buf * padC, 1, 0u, 1u, Ti, p, load_z,
-                      [&](uint32_t e, uint32_t v) {
-                        if ((int64_t)e < n) rout[e] = v;
-                      });
+        const uint32_t n = (uint32_t)P.n;
+        sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
+                            [&](uint32_t e, uint32_t v) {
+                              if (e < n) rout[e] = v;
+                            });
       }
-      buf ^= 1;
     }
   }
 }
@@ -778,13 +798,7 @@ static ozfft_status cuda_check(const char* what) {
   return OZFFT_OK;
 }
 
-static int col_logCb(int logR, int logC) {
-  // tile = R x Cb columns with R*Cb/16 = 256 threads (>= 8 columns for 32-byte sectors)
-  int lcb = (logR >= 4) ? 12 - logR : 8;
-  if (lcb < 3) lcb = 3;
-  if (lcb > logC) lcb = logC;
-  return lcb;
-}
+static int col_logCb(int logR, int logC) { return col_log_cb(logR, logC); }
 static size_t col_smem(int logR, int logCb) {
   const size_t R = 1ull << logR;
   return (R + (R >> 4) + 1) * (1ull << logCb) * sizeof(uint32_t);
@@ -824,7 +838,7 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   c.col_threads = col_threads(pl.logR, c.logCb);
   const size_t C = 1ull << pl.logC;
   const size_t padC = C + (C >> 4) + 1;
-  c.row_smem = (size_t)(pl.K + 2) * padC * sizeof(uint32_t);
+  c.row_smem = ((size_t)(pl.K + 1) * padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
   c.row_threads = pl.logC >= 4 ? (1 << (pl.logC - 4)) : 1;  // exactly Tv: every thread active
   return c;
 }
@@ -846,19 +860,29 @@ static void set_smem(K kern, size_t bytes) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-static void launch_col_fwd(int logR, unsigned nblk, const NttLaunch& c, cudaStream_t st,
-                           const ColParams& CP) {
-  dispatch_log<1, 8>(logR, [&](auto I) {
-    set_smem(k_col_fwd<I.value>, c.col_smem);
-    k_col_fwd<I.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
+template <int LOGR>
+static void launch_col_fwd_r(int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
+                             const ColParams& CP) {
+  dispatch_log<11, 12>(logC, [&](auto J) {
+    set_smem(k_col_fwd<LOGR, J.value>, c.col_smem);
+    k_col_fwd<LOGR, J.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
   });
 }
-static void launch_col_inv(int logR, unsigned nblk, const NttLaunch& c, cudaStream_t st,
-                           const ColParams& CP) {
-  dispatch_log<1, 8>(logR, [&](auto I) {
-    set_smem(k_col_inv<I.value>, c.col_smem);
-    k_col_inv<I.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
+template <int LOGR>
+static void launch_col_inv_r(int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
+                             const ColParams& CP) {
+  dispatch_log<11, 12>(logC, [&](auto J) {
+    set_smem(k_col_inv<LOGR, J.value>, c.col_smem);
+    k_col_inv<LOGR, J.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
   });
+}
+static void launch_col_fwd(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
+                           const ColParams& CP) {
+  dispatch_log<1, 8>(logR, [&](auto I) { launch_col_fwd_r<I.value>(logC, nblk, c, st, CP); });
+}
+static void launch_col_inv(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
+                           const ColParams& CP) {
+  dispatch_log<1, 8>(logR, [&](auto I) { launch_col_inv_r<I.value>(logC, nblk, c, st, CP); });
 }
 static void launch_row(int logC, dim3 grid, const NttLaunch& c, cudaStream_t st, const RowParams& RP) {
   dispatch_log<0, 12>(logC, [&](auto I) {
@@ -881,7 +905,7 @@ static ozfft_status launch_forward_only(const Plan& pl, const int32_t* digits, i
     CP.tw = tw; CP.digits = digits; CP.in_len = in_len; CP.Y = Y; CP.stats = stats;
     CP.unit_mask = 0xFF;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4 * pl.K;
-    launch_col_fwd(pl.logR, (unsigned)nblk, c, st, CP);
+    launch_col_fwd(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
   }
   RowParams RP{};
   RP.logm = pl.logm; RP.logC = pl.logC; RP.logR = pl.logR; RP.nb = nb; RP.K = pl.K; RP.L = pl.L;
@@ -1015,7 +1039,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n; CP.unit_mask = A.unit_mask;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4 * K;
     prof_mark(pl, OZFFT_STAGE_COL_FWD, true, st);
-    launch_col_fwd(pl.logR, (unsigned)nblk, c, st, CP);
+    launch_col_fwd(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
     prof_mark(pl, OZFFT_STAGE_COL_FWD, false, st);
     count_launches(1);
     s = cuda_check("k_col_fwd");
@@ -1043,7 +1067,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.unit_mask = A.unit_mask;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 8 * G;
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
-    launch_col_inv(pl.logR, (unsigned)nblk, c, st, CP);
+    launch_col_inv(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
     prof_mark(pl, OZFFT_STAGE_COL_INV, false, st);
     count_launches(1);
     s = cuda_check("k_col_inv");
