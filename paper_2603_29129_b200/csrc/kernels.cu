@@ -576,8 +576,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
   // group table for 2 convs x K*K groups: npairs, then (X row offset, W row index) x L
   uint32_t* tab = work + padC;
   const int tstride = 1 + 2 * L;
-  if (!P.fwd_only && tv < 2) {
-    const int ci = tv;
+  for (int ci = tv; ci < 2 && !P.fwd_only; ci += blockDim.x) {  // blockDim may be 1 (C < 32)
     const int cv = ci ? cv1 : cv0;
     const bool want = ci ? want1 : want0;
     const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
