@@ -634,25 +634,48 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
       const uint32_t* tg = tab + (ci * G + g) * tstride;
       const int np = (int)tg[0];
       uint32_t* Zt = P.Zout ? P.Zout + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff : nullptr;
-      auto load_z = [&](uint32_t e) -> uint32_t {
-        uint32_t z = 0;
-        const uint32_t pe = pad_idx(e);
-        for (int i = 0; i < np; ++i)
-          z = add_mod(z, mul_shoup(Xs[tg[1 + 2 * i] + pe], __ldg(&Wb[tg[2 + 2 * i] + e]), p), p);
-        if (Zt) Zt[e] = z;
-        return z;
+      // Z(e) = sum_i X_{s_i}(e) * W_{t_i}(e) mod p; the pair count is made a compile-time
+      // constant for the common sizes so that all W loads of a round issue back to back.
+      auto run_group = [&](auto NPc) {
+        constexpr int NP = decltype(NPc)::value;
+        uint32_t xo[NP > 0 ? NP : 1], wo[NP > 0 ? NP : 1];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          xo[i] = tg[1 + 2 * i];
+          wo[i] = tg[2 + 2 * i];
+        }
+        auto load_z = [&](uint32_t e) -> uint32_t {
+          uint32_t z = 0;
+          const uint32_t pe = pad_idx(e);
+          if constexpr (NP > 0) {
+#pragma unroll
+            for (int i = 0; i < NP; ++i)
+              z = add_mod(z, mul_shoup(Xs[xo[i] + pe], __ldg(&Wb[wo[i] + e]), p), p);
+          } else {
+            for (int i = 0; i < np; ++i)
+              z = add_mod(z, mul_shoup(Xs[tg[1 + 2 * i] + pe], __ldg(&Wb[tg[2 + 2 * i] + e]), p), p);
+          }
+          if (Zt) Zt[e] = z;
+          return z;
+        };
+        if (P.logR > 0) {
+          uint32_t* gout = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
+          sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
+                              [&](uint32_t e, uint32_t v) { gout[e] = v; });
+        } else {
+          uint32_t* rout = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
+          const uint32_t n = (uint32_t)P.n;
+          sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
+                              [&](uint32_t e, uint32_t v) {
+                                if (e < n) rout[e] = v;
+                              });
+        }
       };
-      if (P.logR > 0) {
-        uint32_t* gout = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
-        sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
-                            [&](uint32_t e, uint32_t v) { gout[e] = v; });
-      } else {
-        uint32_t* rout = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
-        const uint32_t n = (uint32_t)P.n;
-        sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
-                            [&](uint32_t e, uint32_t v) {
-                              if (e < n) rout[e] = v;
-                            });
+      switch (np) {
+        case 1: run_group(std::integral_constant<int, 1>{}); break;
+        case 2: run_group(std::integral_constant<int, 2>{}); break;
+        case 3: run_group(std::integral_constant<int, 3>{}); break;
+        default: run_group(std::integral_constant<int, 0>{}); break;
       }
     }
   }
