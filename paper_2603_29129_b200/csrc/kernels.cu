@@ -363,7 +363,7 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[16], int tv, uint32_
   for (int i = 0; i < RT::cnt; ++i) {
     const uint32_t e = round_elem<LOGN, INV, R>(tv, i);
     if constexpr (R == 0)
-      x[i] = load_first(e);
+      x[i] = load_first(i, e);
     else
       x[i] = sm[pad_idx(e) * Cb];
   }
@@ -380,7 +380,7 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[16], int tv, uint32_
   for (int i = 0; i < RT::cnt; ++i) {
     const uint32_t e = round_elem<LOGN, INV, R>(tv, i);
     if constexpr (R == RT::nr - 1)
-      store_last(e, x[i]);
+      store_last(i, e, x[i]);
     else
       sm[pad_idx(e) * Cb] = x[i];
   }
@@ -403,15 +403,15 @@ __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[16], int tv, uint32
 // shared memory (padded, interleave Cb) between rounds.
 //   INV = false: DIF stages len = N .. 2;   INV = true: DIT stages len = 2 .. N.
 // Element e has global position gbase_vec + e*gs; gb_mod = gbase_vec mod (gs*step) for
-// every step used (0 for rows, the column index for columns).  load_first(e) gives the
-// round-0 input; store_last(e, v) consumes the final values.  `sm` must be free for
+// every step used (0 for rows, the column index for columns).  load_first(i, e) gives the
+// round-0 input of register i / element e; store_last(i, e, v) consumes the final values.  `sm` must be free for
 // writes (caller-synchronised) on entry.
 template <int LOGN, bool INV, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, int Cb, uint32_t gb_mod,
                                         uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                         LoadF&& load_first, StoreF&& store_last) {
   if constexpr (LOGN == 0) {  // N == 1: identity
-    if (tv == 0) store_last(0u, load_first(0u));
+    if (tv == 0) store_last(0, 0u, load_first(0, 0u));
   } else {
     uint32_t x[16];
     sub_ntt_rounds<LOGN, INV, 0>(x, tv, sm, Cb, gb_mod, gs, T, p, load_first, store_last);
@@ -481,8 +481,8 @@ __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
   const uint32_t lim = P.in_len > col ? (uint32_t)(P.in_len - col) : 0u;  // e*C < lim <=> i < in_len
   sub_ntt<LOGR, false>(
       tv, smem + c, Cb, col, C, T, p,
-      [&](uint32_t e) -> uint32_t { return e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u; },
-      [&](uint32_t e, uint32_t val) { out[e * C] = val; });
+      [&](int, uint32_t e) -> uint32_t { return e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u; },
+      [&](int, uint32_t e, uint32_t val) { out[e * C] = val; });
 }
 
 // Inverse column pass: global DIT stages len = 2C .. m; writes rows i < n only.
@@ -513,8 +513,8 @@ __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
   sub_ntt<LOGR, true>(
       tv, smem + c, Cb, col, C, T, p,
-      [&](uint32_t e) -> uint32_t { return __ldg(&in[e * C]); },
-      [&](uint32_t e, uint32_t val) {
+      [&](int, uint32_t e) -> uint32_t { return __ldg(&in[e * C]); },
+      [&](int, uint32_t e, uint32_t val) {
         if (e * C < lim) out[e * C] = val;
       });
 }
@@ -545,9 +545,19 @@ template <int LOGC>
 struct RowCfg {
   static constexpr int threads = LOGC >= 4 ? (1 << (LOGC - 4)) : 1;
   static constexpr int min_blocks = LOGC == 11 ? 6 : 1;
+  // stages of the first DIT round (= last DIF round): its groups are contiguous blocks
+  static constexpr int S0 = LOGC == 0 ? 0 : LOGC - 4 * ((LOGC + 3) / 4 - 1);
 };
 
-template <int LOGC>
+// Row-local storage order used for the X rows in shared memory and for the cached W
+// spectra: element e of a row (internal bit-reversed order) lives at
+// (e mod 2^S0) * (C / 2^S0) + e / 2^S0, so that in the first DIT round (groups of 2^S0
+// contiguous elements, one group per thread) a warp touches consecutive words.
+__host__ __device__ __forceinline__ uint32_t row_perm(uint32_t e, int logC, int S0) {
+  return ((e & ((1u << S0) - 1)) << (logC - S0)) + (e >> S0);
+}
+
+template <int LOGC, bool TWO_PASS>
 __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_blocks)
     k_row_fused(RowParams P) {
   extern __shared__ uint32_t smem[];
@@ -557,6 +567,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
   const int q = (blockIdx.y >> 1) & 1;
   const uint32_t row = blockIdx.y >> 2;
   constexpr int logC = LOGC;
+  constexpr int S0 = RowCfg<LOGC>::S0;
   constexpr uint32_t C = 1u << logC;
   constexpr uint32_t padC = C + (C >> 4) + 1;
   const int tv = threadIdx.x;
@@ -571,9 +582,9 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
   const bool want1 = (P.unit_mask >> (cv1 * 2 + q)) & 1u;
   if (!P.fwd_only && !want0 && !want1) return;
   if (ka == 0 && !P.fwd_only) return;  // no slices: the schedule has no groups here
-  uint32_t* Xs = smem;              // [K][padC]: forward spectra rows of the K slices
-  uint32_t* work = smem + K * padC;  // [padC]: inter-round exchange buffer
-  // group table for 2 convs x K*K groups: npairs, then (X row offset, W row index) x L
+  uint32_t* Xs = smem;               // [K][C] forward spectra rows (row_perm order)
+  uint32_t* work = smem + K * C;     // [padC]: inter-round exchange buffer
+  // group table for 2 convs x K*K groups: npairs, then (X row offset, W row offset) x L
   uint32_t* tab = work + padC;
   const int tstride = 1 + 2 * L;
   for (int ci = tv; ci < 2 && !P.fwd_only; ci += blockDim.x) {  // blockDim may be 1 (C < 32)
@@ -587,7 +598,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
       uint32_t* tg = tab + (ci * G + g) * tstride;
       tg[0] = (uint32_t)grp[1];
       for (int i = 0; i < grp[1]; ++i) {
-        tg[1 + 2 * i] = (uint32_t)grp[2 + 2 * i] * padC;
+        tg[1 + 2 * i] = (uint32_t)grp[2 + 2 * i] * C;
         tg[2 + 2 * i] = (uint32_t)grp[3 + 2 * i] * (uint32_t)m;
       }
     }
@@ -597,32 +608,30 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
   const uint32_t rowoff = row << logC;
   // ---- forward: last log2(C) DIF stages of each slice's NTT (Alg.6 l.787)
   for (int s = 0; s < ka; ++s) {
-    uint32_t* xs = Xs + s * padC;
+    uint32_t* xs = Xs + s * C;
     uint32_t* outX = P.Xout ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff : nullptr;
     __syncthreads();  // `work` is free (previous sub-transform's last reads are done)
-    if (P.logR > 0) {
+    auto store_x = [&](int, uint32_t e, uint32_t v) {
+      xs[row_perm(e, logC, S0)] = v;
+      if (outX) outX[e] = v;
+    };
+    if constexpr (TWO_PASS) {
       const uint32_t* y = P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff;
-      sub_ntt<LOGC, false>(
-          tv, work, 1, 0u, 1u, Tf, p,
-          [&](uint32_t e) -> uint32_t { return __ldg(&y[e]); },
-          [&](uint32_t e, uint32_t v) {
-            xs[pad_idx(e)] = v;
-            if (outX) outX[e] = v;
-          });
+      sub_ntt<LOGC, false>(tv, work, 1, 0u, 1u, Tf, p,
+                           [&](int, uint32_t e) -> uint32_t { return __ldg(&y[e]); }, store_x);
     } else {
       const int32_t* D = P.digits + ((b * 2 + a) * K + s) * P.in_len;
       const uint32_t in_len = (uint32_t)P.in_len;
       sub_ntt<LOGC, false>(
           tv, work, 1, 0u, 1u, Tf, p,
-          [&](uint32_t e) -> uint32_t { return e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
-          [&](uint32_t e, uint32_t v) {
-            xs[pad_idx(e)] = v;
-            if (outX) outX[e] = v;
-          });
+          [&](int, uint32_t e) -> uint32_t { return e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
+          store_x);
     }
   }
   if (P.fwd_only) return;
-  // ---- per group: Z = sum X_s (.) W_t (Alg.8 l.981-982), then first DIT stages
+  // ---- per group: Z = sum X_s (.) W_t (Alg.8 l.981-982), then the first log2(C) DIT
+  // stages of its inverse NTT (l.973)
+  constexpr int CNT = RoundT<LOGC, true, 0>::cnt;
   for (int ci = 0; ci < 2; ++ci) {
     const int cv = ci ? cv1 : cv0;
     const int bw = conv_b(cv);
@@ -633,49 +642,35 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
       if (g > 0) __syncthreads();
       const uint32_t* tg = tab + (ci * G + g) * tstride;
       const int np = (int)tg[0];
+      // pointwise products for this thread's round-0 elements, all loads of a pair batched
+      uint32_t z[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) z[i] = 0;
+      for (int ip = 0; ip < np; ++ip) {
+        const uint32_t* xr = Xs + tg[1 + 2 * ip];
+        const uint2* wr = Wb + tg[2 + 2 * ip];
+#pragma unroll
+        for (int i = 0; i < CNT; ++i) {
+          const uint32_t pe = row_perm(round_elem<LOGC, true, 0>(tv, i), logC, S0);
+          z[i] = add_mod(z[i], mul_shoup(xr[pe], __ldg(&wr[pe]), p), p);
+        }
+      }
       uint32_t* Zt = P.Zout ? P.Zout + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff : nullptr;
-      // Z(e) = sum_i X_{s_i}(e) * W_{t_i}(e) mod p; the pair count is made a compile-time
-      // constant for the common sizes so that all W loads of a round issue back to back.
-      auto run_group = [&](auto NPc) {
-        constexpr int NP = decltype(NPc)::value;
-        uint32_t xo[NP > 0 ? NP : 1], wo[NP > 0 ? NP : 1];
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          xo[i] = tg[1 + 2 * i];
-          wo[i] = tg[2 + 2 * i];
-        }
-        auto load_z = [&](uint32_t e) -> uint32_t {
-          uint32_t z = 0;
-          const uint32_t pe = pad_idx(e);
-          if constexpr (NP > 0) {
-#pragma unroll
-            for (int i = 0; i < NP; ++i)
-              z = add_mod(z, mul_shoup(Xs[xo[i] + pe], __ldg(&Wb[wo[i] + e]), p), p);
-          } else {
-            for (int i = 0; i < np; ++i)
-              z = add_mod(z, mul_shoup(Xs[tg[1 + 2 * i] + pe], __ldg(&Wb[tg[2 + 2 * i] + e]), p), p);
-          }
-          if (Zt) Zt[e] = z;
-          return z;
-        };
-        if (P.logR > 0) {
-          uint32_t* gout = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
-          sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
-                              [&](uint32_t e, uint32_t v) { gout[e] = v; });
-        } else {
-          uint32_t* rout = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
-          const uint32_t n = (uint32_t)P.n;
-          sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
-                              [&](uint32_t e, uint32_t v) {
-                                if (e < n) rout[e] = v;
-                              });
-        }
+      auto load_z = [&](int i, uint32_t e) -> uint32_t {
+        if (Zt) Zt[e] = z[i];
+        return z[i];
       };
-      switch (np) {
-        case 1: run_group(std::integral_constant<int, 1>{}); break;
-        case 2: run_group(std::integral_constant<int, 2>{}); break;
-        case 3: run_group(std::integral_constant<int, 3>{}); break;
-        default: run_group(std::integral_constant<int, 0>{}); break;
+      if constexpr (TWO_PASS) {
+        uint32_t* gout = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
+        sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
+                            [&](int, uint32_t e, uint32_t v) { gout[e] = v; });
+      } else {
+        uint32_t* rout = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
+        const uint32_t n = (uint32_t)P.n;
+        sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
+                            [&](int, uint32_t e, uint32_t v) {
+                              if (e < n) rout[e] = v;
+                            });
       }
     }
   }
@@ -780,30 +775,39 @@ static void fill_crt_consts(const Plan& pl, FinishParams& FP) {
 }
 
 // ============================================================== small utility kernels
-// W finalize: Wp[q][b][t][i] = (W m^{-1} mod p, Shoup companion) from the forward spectra.
+// W finalize: Wp[q][b][t][row*C + row_perm(e)] = (W m^{-1} mod p, Shoup companion) from the
+// forward spectra X[q][b][t][row*C + e] (internal order).
 __global__ void k_w_finalize(const uint32_t* __restrict__ X, uint2* __restrict__ Wp, int K,
-                             int64_t m, uint32_t p0, uint32_t p1, uint32_t minv0, uint32_t minv1) {
+                             int64_t m, int logC, int S0, uint32_t p0, uint32_t p1, uint32_t minv0,
+                             uint32_t minv1) {
   const int64_t total = (int64_t)4 * K * m;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int q = (int)(i / (2 * K * m));
     const uint32_t p = q ? p1 : p0, mi = q ? minv1 : minv0;
     const uint32_t w = (uint32_t)(((uint64_t)X[i] * mi) % p);
-    Wp[i] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));
+    const int64_t e = i & ((1ll << logC) - 1);
+    const int64_t dst = (i - e) + row_perm((uint32_t)e, logC, S0);
+    Wp[dst] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));
   }
 }
 
-// Tap conversion: internal bit-reversed order (optionally times a constant) -> natural.
-//   dst[o(v)][k] = src[v][bitrev(k)] * mult mod p, for vectors v of length m.
+// Tap conversion: internal bit-reversed order (optionally row-permuted, optionally times
+// m mod p) -> natural order:  dst[o(v)][k] = src[v][pos(bitrev(k))] (* m mod p).
 __global__ void k_tap_permute(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                               int64_t nvec, int logm, const int64_t* __restrict__ dst_off,
-                              const uint32_t* __restrict__ vec_p, uint32_t mult_is_m) {
+                              const uint32_t* __restrict__ vec_p, uint32_t mult_is_m, int logC,
+                              int S0) {
   const int64_t m = 1ll << logm;
   const int64_t total = nvec * m;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = i >> logm, k = i & (m - 1);
-    const int64_t br = logm ? (int64_t)(__brevll((unsigned long long)k) >> (64 - logm)) : 0;
+    int64_t br = logm ? (int64_t)(__brevll((unsigned long long)k) >> (64 - logm)) : 0;
+    if (logC >= 0) {  // source stored in row_perm order
+      const int64_t e = br & ((1ll << logC) - 1);
+      br = (br - e) + row_perm((uint32_t)e, logC, S0);
+    }
     uint32_t val = src[v * m + br];
     if (mult_is_m) val = (uint32_t)(((uint64_t)val * (uint64_t)(m % vec_p[v])) % vec_p[v]);
     dst[dst_off[v] + k] = val;
@@ -860,7 +864,7 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   c.col_threads = col_threads(pl.logR, c.logCb);
   const size_t C = 1ull << pl.logC;
   const size_t padC = C + (C >> 4) + 1;
-  c.row_smem = ((size_t)(pl.K + 1) * padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
+  c.row_smem = ((size_t)pl.K * C + padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
   c.row_threads = pl.logC >= 4 ? (1 << (pl.logC - 4)) : 1;  // exactly Tv: every thread active
   return c;
 }
@@ -906,12 +910,21 @@ static void launch_col_inv(int logR, int logC, unsigned nblk, const NttLaunch& c
                            const ColParams& CP) {
   dispatch_log<1, 8>(logR, [&](auto I) { launch_col_inv_r<I.value>(logC, nblk, c, st, CP); });
 }
-static void launch_row(int logC, dim3 grid, const NttLaunch& c, cudaStream_t st, const RowParams& RP) {
-  dispatch_log<0, 12>(logC, [&](auto I) {
-    set_smem(k_row_fused<I.value>, c.row_smem);
-    k_row_fused<I.value><<<grid, c.row_threads, c.row_smem, st>>>(RP);
-  });
+static void launch_row(int logC, int logR, dim3 grid, const NttLaunch& c, cudaStream_t st,
+                       const RowParams& RP) {
+  if (logR > 0) {
+    dispatch_log<11, 12>(logC, [&](auto I) {
+      set_smem(k_row_fused<I.value, true>, c.row_smem);
+      k_row_fused<I.value, true><<<grid, c.row_threads, c.row_smem, st>>>(RP);
+    });
+  } else {
+    dispatch_log<0, 12>(logC, [&](auto I) {
+      set_smem(k_row_fused<I.value, false>, c.row_smem);
+      k_row_fused<I.value, false><<<grid, c.row_threads, c.row_smem, st>>>(RP);
+    });
+  }
 }
+static int row_s0(int logC) { return logC == 0 ? 0 : logC - 4 * ((logC + 3) / 4 - 1); }
 
 // Forward NTT of digit vectors [nb][2][K][in_len] into internal-order spectra Xout
 // [nb][2 q][2 a][K][m] (used at plan time for omega~*; the hot path fuses the row part).
@@ -934,7 +947,7 @@ static ozfft_status launch_forward_only(const Plan& pl, const int32_t* digits, i
   RP.p[0] = pl.p[0]; RP.p[1] = pl.p[1]; RP.tw = tw; RP.digits = digits; RP.in_len = in_len;
   RP.Y = Y; RP.stats = stats; RP.unit_mask = 0xFF; RP.fwd_only = 1; RP.Xout = Xout;
   dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
-  launch_row(pl.logC, grid, c, st, RP);
+  launch_row(pl.logC, pl.logR, grid, c, st, RP);
   return cuda_check("forward-only NTT");
 }
 
@@ -995,7 +1008,8 @@ ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
     cudaMemcpyAsync(pl.pers + pl.poff.wsplit, wsplit, sizeof(int32_t) * (2 + 2 * K),
                     cudaMemcpyHostToDevice, st);
     k_w_finalize<<<592, 256, 0, st>>>(X, reinterpret_cast<uint2*>(pl.pers + pl.poff.W), K, m,
-                                      pl.p[0], pl.p[1], pl.minv[0], pl.minv[1]);
+                                      pl.logC, row_s0(pl.logC), pl.p[0], pl.p[1], pl.minv[0],
+                                      pl.minv[1]);
     s = cuda_check("W finalize");
     if (!s && cudaStreamSynchronize(st) != cudaSuccess) s = cuda_check("plan precompute sync");
   }
@@ -1075,7 +1089,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   {
     dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
     prof_mark(pl, OZFFT_STAGE_ROW_FUSED, true, st);
-    launch_row(pl.logC, grid, c, st, RP);
+    launch_row(pl.logC, pl.logR, grid, c, st, RP);
     prof_mark(pl, OZFFT_STAGE_ROW_FUSED, false, st);
     count_launches(1);
     s = cuda_check("k_row_fused");
@@ -1112,7 +1126,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   if (taps) {
     std::vector<int64_t> off;
     std::vector<uint32_t> vp;
-    auto run_perm = [&](const uint32_t* src, void* dst, bool mult) -> ozfft_status {
+    auto run_perm = [&](const uint32_t* src, void* dst, bool mult, bool rowperm) -> ozfft_status {
       int64_t* doff = nullptr;
       uint32_t* dvp = nullptr;
       const int64_t nvec = (int64_t)off.size();
@@ -1121,7 +1135,8 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
       cudaMemcpyAsync(doff, off.data(), sizeof(int64_t) * nvec, cudaMemcpyHostToDevice, st);
       cudaMemcpyAsync(dvp, vp.data(), sizeof(uint32_t) * nvec, cudaMemcpyHostToDevice, st);
       k_tap_permute<<<1184, 256, 0, st>>>(src, reinterpret_cast<uint32_t*>(dst), nvec, pl.logm,
-                                          doff, dvp, mult ? 1u : 0u);
+                                          doff, dvp, mult ? 1u : 0u, rowperm ? pl.logC : -1,
+                                          row_s0(pl.logC));
       cudaStreamSynchronize(st);
       cudaFree(doff);
       cudaFree(dvp);
@@ -1136,7 +1151,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
               off.push_back((((b * 2 + a) * K + s2) * 2 + q) * m);
               vp.push_back(pl.p[q]);
             }
-      s = run_perm(Xtap, taps->X, false);
+      s = run_perm(Xtap, taps->X, false, false);
       if (s) return s;
     }
     if (taps->Z) {  // src [b][q][cv][g][m] (W m^-1 scaled) -> dst [b][cv][g][q][m] (times m)
@@ -1148,7 +1163,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
               off.push_back((((b * 4 + cv) * G + g) * 2 + q) * m);
               vp.push_back(pl.p[q]);
             }
-      s = run_perm(Ztap, taps->Z, true);
+      s = run_perm(Ztap, taps->Z, true, false);
       if (s) return s;
     }
     if (taps->res) {  // [b][cv][q][g][n] -> [b][cv][g][q][n]
@@ -1175,7 +1190,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
             off.push_back(((bw * K + t) * 2 + q) * m);
             vp.push_back(pl.p[q]);
           }
-      s = run_perm(tmp, taps->W, true);
+      s = run_perm(tmp, taps->W, true, true);
       cudaFree(tmp);
       if (s) return s;
     }
