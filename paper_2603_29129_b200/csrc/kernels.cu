@@ -352,20 +352,33 @@ __device__ __forceinline__ uint32_t round_elem(int tv, int i) {
   return ((g >> RT::logstep) << RT::lb) + (g & ((1u << RT::logstep) - 1)) + (k << RT::logstep);
 }
 
-template <int LOGN, bool INV, int R, class LoadF, class StoreF>
+// Shared-memory slot of register i in round R: pad_idx(base_g) + koff(k), where base_g is
+// the group's first element and koff(k) = k*step + (k*step >> 4) is a compile-time
+// constant (valid because every block has length >= 16 when a round touches smem), so
+// the per-element address is a base register plus an immediate offset.
+template <int LOGN, bool INV, int R, int CB>
+__device__ __forceinline__ uint32_t* round_slot(uint32_t* sm, int tv, int i) {
+  using RT = RoundT<LOGN, INV, R>;
+  const uint32_t g = (uint32_t)(tv + (i >> RT::S) * RT::Tv);
+  const uint32_t k = (uint32_t)(i & ((1 << RT::S) - 1));
+  const uint32_t base = ((g >> RT::logstep) << RT::lb) + (g & ((1u << RT::logstep) - 1));
+  const uint32_t ks = k << RT::logstep;
+  return sm + (pad_idx(base) + ks + (ks >> 4)) * CB;
+}
+
+template <int LOGN, bool INV, int R, int CB, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[16], int tv, uint32_t* __restrict__ sm,
-                                              int Cb, uint32_t gb_mod, uint32_t gs,
+                                              uint32_t gb_mod, uint32_t gs,
                                               const uint2* __restrict__ T, uint32_t p,
                                               LoadF& load_first, StoreF& store_last) {
   using RT = RoundT<LOGN, INV, R>;
   constexpr uint32_t step = 1u << RT::logstep;
 #pragma unroll
   for (int i = 0; i < RT::cnt; ++i) {
-    const uint32_t e = round_elem<LOGN, INV, R>(tv, i);
     if constexpr (R == 0)
-      x[i] = load_first(i, e);
+      x[i] = load_first(i, round_elem<LOGN, INV, R>(tv, i));
     else
-      x[i] = sm[pad_idx(e) * Cb];
+      x[i] = *round_slot<LOGN, INV, R, CB>(sm, tv, i);
   }
 #pragma unroll
   for (int u = 0; u < (RT::cnt >> RT::S); ++u) {
@@ -378,23 +391,22 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[16], int tv, uint32_
   }
 #pragma unroll
   for (int i = 0; i < RT::cnt; ++i) {
-    const uint32_t e = round_elem<LOGN, INV, R>(tv, i);
     if constexpr (R == RT::nr - 1)
-      store_last(i, e, x[i]);
+      store_last(i, round_elem<LOGN, INV, R>(tv, i), x[i]);
     else
-      sm[pad_idx(e) * Cb] = x[i];
+      *round_slot<LOGN, INV, R, CB>(sm, tv, i) = x[i];
   }
   if constexpr (R != RT::nr - 1) __syncthreads();
 }
 
-template <int LOGN, bool INV, int R, class LoadF, class StoreF>
+template <int LOGN, bool INV, int R, int CB, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[16], int tv, uint32_t* __restrict__ sm,
-                                               int Cb, uint32_t gb_mod, uint32_t gs,
+                                               uint32_t gb_mod, uint32_t gs,
                                                const uint2* __restrict__ T, uint32_t p,
                                                LoadF& load_first, StoreF& store_last) {
   if constexpr (R < RoundT<LOGN, INV, 0>::nr) {
-    sub_ntt_round<LOGN, INV, R>(x, tv, sm, Cb, gb_mod, gs, T, p, load_first, store_last);
-    sub_ntt_rounds<LOGN, INV, R + 1>(x, tv, sm, Cb, gb_mod, gs, T, p, load_first, store_last);
+    sub_ntt_round<LOGN, INV, R, CB>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, R + 1, CB>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
   }
 }
 
@@ -406,15 +418,15 @@ __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[16], int tv, uint32
 // every step used (0 for rows, the column index for columns).  load_first(i, e) gives the
 // round-0 input of register i / element e; store_last(i, e, v) consumes the final values.  `sm` must be free for
 // writes (caller-synchronised) on entry.
-template <int LOGN, bool INV, class LoadF, class StoreF>
-__device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, int Cb, uint32_t gb_mod,
+template <int LOGN, bool INV, int CB, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, uint32_t gb_mod,
                                         uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                         LoadF&& load_first, StoreF&& store_last) {
   if constexpr (LOGN == 0) {  // N == 1: identity
     if (tv == 0) store_last(0, 0u, load_first(0, 0u));
   } else {
     uint32_t x[16];
-    sub_ntt_rounds<LOGN, INV, 0>(x, tv, sm, Cb, gb_mod, gs, T, p, load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, 0, CB>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
   }
 }
 
@@ -479,8 +491,8 @@ __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
   uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (int64_t)m + col;
   const uint2* T = P.tw + (size_t)(q * 2 + 0) * m;
   const uint32_t lim = P.in_len > col ? (uint32_t)(P.in_len - col) : 0u;  // e*C < lim <=> i < in_len
-  sub_ntt<LOGR, false>(
-      tv, smem + c, Cb, col, C, T, p,
+  sub_ntt<LOGR, false, Cb>(
+      tv, smem + c, col, C, T, p,
       [&](int, uint32_t e) -> uint32_t { return e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u; },
       [&](int, uint32_t e, uint32_t val) { out[e * C] = val; });
 }
@@ -511,8 +523,8 @@ __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
   const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
   const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
-  sub_ntt<LOGR, true>(
-      tv, smem + c, Cb, col, C, T, p,
+  sub_ntt<LOGR, true, Cb>(
+      tv, smem + c, col, C, T, p,
       [&](int, uint32_t e) -> uint32_t { return __ldg(&in[e * C]); },
       [&](int, uint32_t e, uint32_t val) {
         if (e * C < lim) out[e * C] = val;
@@ -555,6 +567,15 @@ struct RowCfg {
 // contiguous elements, one group per thread) a warp touches consecutive words.
 __host__ __device__ __forceinline__ uint32_t row_perm(uint32_t e, int logC, int S0) {
   return ((e & ((1u << S0) - 1)) << (logC - S0)) + (e >> S0);
+}
+
+// row_perm of the element held in register i by thread tv in the first DIT round (element
+// g*2^S0 + k, g = tv + u*Tv, i = u*2^S0 + k): tv + compile-time offset.
+template <int LOGC>
+__device__ __forceinline__ uint32_t row_slot(int tv, int i) {
+  constexpr int S0 = RowCfg<LOGC>::S0;
+  constexpr int Tv = RowCfg<LOGC>::threads;
+  return (uint32_t)tv + ((uint32_t)(i & ((1 << S0) - 1)) << (LOGC - S0)) + (uint32_t)(i >> S0) * Tv;
 }
 
 template <int LOGC, bool TWO_PASS>
@@ -611,19 +632,19 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
     uint32_t* xs = Xs + s * C;
     uint32_t* outX = P.Xout ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff : nullptr;
     __syncthreads();  // `work` is free (previous sub-transform's last reads are done)
-    auto store_x = [&](int, uint32_t e, uint32_t v) {
-      xs[row_perm(e, logC, S0)] = v;
+    auto store_x = [&](int i, uint32_t e, uint32_t v) {
+      xs[row_slot<LOGC>(tv, i)] = v;  // == row_perm(e)
       if (outX) outX[e] = v;
     };
     if constexpr (TWO_PASS) {
       const uint32_t* y = P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff;
-      sub_ntt<LOGC, false>(tv, work, 1, 0u, 1u, Tf, p,
+      sub_ntt<LOGC, false, 1>(tv, work, 0u, 1u, Tf, p,
                            [&](int, uint32_t e) -> uint32_t { return __ldg(&y[e]); }, store_x);
     } else {
       const int32_t* D = P.digits + ((b * 2 + a) * K + s) * P.in_len;
       const uint32_t in_len = (uint32_t)P.in_len;
-      sub_ntt<LOGC, false>(
-          tv, work, 1, 0u, 1u, Tf, p,
+      sub_ntt<LOGC, false, 1>(
+          tv, work, 0u, 1u, Tf, p,
           [&](int, uint32_t e) -> uint32_t { return e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
           store_x);
     }
@@ -651,7 +672,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
         const uint2* wr = Wb + tg[2 + 2 * ip];
 #pragma unroll
         for (int i = 0; i < CNT; ++i) {
-          const uint32_t pe = row_perm(round_elem<LOGC, true, 0>(tv, i), logC, S0);
+          const uint32_t pe = row_slot<LOGC>(tv, i);  // == row_perm(round-0 element)
           z[i] = add_mod(z[i], mul_shoup(xr[pe], __ldg(&wr[pe]), p), p);
         }
       }
@@ -662,12 +683,12 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
       };
       if constexpr (TWO_PASS) {
         uint32_t* gout = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
-        sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
+        sub_ntt<LOGC, true, 1>(tv, work, 0u, 1u, Ti, p, load_z,
                             [&](int, uint32_t e, uint32_t v) { gout[e] = v; });
       } else {
         uint32_t* rout = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
         const uint32_t n = (uint32_t)P.n;
-        sub_ntt<LOGC, true>(tv, work, 1, 0u, 1u, Ti, p, load_z,
+        sub_ntt<LOGC, true, 1>(tv, work, 0u, 1u, Ti, p, load_z,
                             [&](int, uint32_t e, uint32_t v) {
                               if (e < n) rout[e] = v;
                             });
