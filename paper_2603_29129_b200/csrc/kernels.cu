@@ -723,7 +723,7 @@ __device__ __forceinline__ long long garner2(uint32_t z0, uint32_t z1, const Fin
   return Zp > P.halfP ? (long long)(Zp - P.P) : (long long)Zp;
 }
 
-__global__ void __launch_bounds__(256) k_crt_finish(FinishParams P) {
+__global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
   const int64_t b = blockIdx.y;
   const int K = P.K, L = P.L, G = K * K;
   // per-transform schedule: group counts and exact scales 2^-cexp (l.975), in smem
@@ -748,22 +748,39 @@ __global__ void __launch_bounds__(256) k_crt_finish(FinishParams P) {
     return;
   }
   double Sh[4], Sl[4];
-#pragma unroll
+#pragma unroll 1
   for (int cv = 0; cv < 4; ++cv) {
     double sh = 0.0, sl = 0.0;
     const int ng = s_ng[cv];
     const uint32_t* r0 = P.res + (((b * 4 + cv) * 2 + 0) * G) * P.n + j;
     const uint32_t* r1 = P.res + (((b * 4 + cv) * 2 + 1) * G) * P.n + j;
-    for (int g = 0; g < ng; ++g) {
-      const long long Z = garner2(__ldcs(&r0[g * P.n]), __ldcs(&r1[g * P.n]), P);
-      if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + j] = Z;
-      const double h = __ll2double_rn(Z);
-      const double l = __ll2double_rn(Z - __double2ll_rz(h));
-      const double sc = s_sc[cv][g];  // z' / c, exact power of two (l.975)
-      dd_add(sh, sl, __dmul_rn(h, sc), __dmul_rn(l, sc), sh, sl);  // flush order (l.976)
+    for (int g0 = 0; g0 < ng; g0 += 9) {
+      // issue every residue load of up to 9 groups before the dependent DD chain
+      uint32_t z0[9], z1[9];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        if (g0 + i < ng) {
+          z0[i] = __ldcs(&r0[(int64_t)(g0 + i) * P.n]);
+          z1[i] = __ldcs(&r1[(int64_t)(g0 + i) * P.n]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        if (g0 + i < ng) {
+          const int g = g0 + i;
+          const long long Z = garner2(z0[i], z1[i], P);
+          if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + j] = Z;
+          const double h = __ll2double_rn(Z);
+          const double l = __ll2double_rn(Z - __double2ll_rz(h));
+          const double sc = s_sc[cv][g];  // z' / c, exact power of two (l.975)
+          dd_add(sh, sl, __dmul_rn(h, sc), __dmul_rn(l, sc), sh, sl);  // flush order (l.976)
+        }
+      }
     }
-    Sh[cv] = sh;
-    Sl[cv] = sl;
+    if (cv == 0) { Sh[0] = sh; Sl[0] = sl; }
+    else if (cv == 1) { Sh[1] = sh; Sl[1] = sl; }
+    else if (cv == 2) { Sh[2] = sh; Sl[2] = sl; }
+    else { Sh[3] = sh; Sl[3] = sl; }
   }
   double yrh, yrl, yih, yil;
   dd_add(Sh[0], Sl[0], -Sh[1], -Sl[1], yrh, yrl);  // rr - ii
