@@ -463,6 +463,8 @@ __host__ __device__ constexpr int col_log_cb(int logR, int logC) {
 }
 
 // Forward column pass: global DIF stages len = m .. 2C on columns of the R x C view.
+// One CTA per (transform, prime, part, column block) loops over the part's slices; the
+// next slice's column tile is loaded while the current one is transformed.
 template <int LOGR, int LOGC>
 __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
   extern __shared__ uint32_t smem[];
@@ -471,33 +473,50 @@ __global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
   constexpr uint32_t C = 1u << LOGC;
   constexpr uint32_t m = 1u << (LOGR + LOGC);
   constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
+  constexpr int CNT = RoundT<LOGR, false, 0>::cnt;
   const uint32_t cb = blockIdx.x % ncb;
-  uint32_t v = blockIdx.x / ncb;  // ((b * 2 + q) * 2 + a) * K + s
-  const int s = (int)(v % P.K); v /= P.K;
+  uint32_t v = blockIdx.x / ncb;  // (b * 2 + q) * 2 + a
   const int a = (int)(v & 1); v >>= 1;
   const int q = (int)(v & 1); v >>= 1;
   const int64_t b = v;
   const int32_t* st = P.stats + b * stats_stride(P.K);
-  if (s >= st[a]) return;  // slice does not exist (k_a <= s) or transform non-finite
+  const int ka = st[a];  // 0 if the transform is non-finite
   // unit (cv, q) needs part a if conv_a(cv) == a
   const uint32_t need = a == 0 ? ((1u << (0 * 2 + q)) | (1u << (3 * 2 + q)))
                                : ((1u << (1 * 2 + q)) | (1u << (2 * 2 + q)));
-  if (!(P.unit_mask & need)) return;
+  if (ka == 0 || !(P.unit_mask & need)) return;
   const int c = threadIdx.x & (Cb - 1);
   const int tv = threadIdx.x >> LOGCB;
-  const uint32_t p = q ? P.p[1] : P.p[0];  // no dynamic param-array index (local memory)
+  const uint32_t p = q ? P.p[1] : P.p[0];
   const uint32_t col = (cb << LOGCB) + c;
-  const int32_t* D = P.digits + ((b * 2 + a) * P.K + s) * P.in_len + col;
-  uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (int64_t)m + col;
   const uint2* T = P.tw + (size_t)(q * 2 + 0) * m;
   const uint32_t lim = P.in_len > col ? (uint32_t)(P.in_len - col) : 0u;  // e*C < lim <=> i < in_len
-  sub_ntt<LOGR, false, Cb>(
-      tv, smem + c, col, C, T, p,
-      [&](int, uint32_t e) -> uint32_t { return e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u; },
-      [&](int, uint32_t e, uint32_t val) { out[e * C] = val; });
+  uint32_t nxt[16];
+  auto fetch = [&](int s) {
+    const int32_t* D = P.digits + ((b * 2 + a) * P.K + s) * P.in_len + col;
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) {
+      const uint32_t e = round_elem<LOGR, false, 0>(tv, i);
+      nxt[i] = e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u;
+    }
+  };
+  fetch(0);
+  for (int s = 0; s < ka; ++s) {
+    uint32_t cur[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+    if (s + 1 < ka) fetch(s + 1);
+    if (s > 0) __syncthreads();  // smem tile free
+    uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (int64_t)m + col;
+    sub_ntt<LOGR, false, Cb>(
+        tv, smem + c, col, C, T, p, [&](int i, uint32_t) -> uint32_t { return cur[i]; },
+        [&](int, uint32_t e, uint32_t val) { out[e * C] = val; });
+  }
 }
 
 // Inverse column pass: global DIT stages len = 2C .. m; writes rows i < n only.
+// One CTA per (transform, prime, conv, column block) loops over the conv's Alg.8 groups
+// with the next group's tile prefetched.
 template <int LOGR, int LOGC>
 __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   extern __shared__ uint32_t smem[];
@@ -506,29 +525,42 @@ __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   constexpr uint32_t C = 1u << LOGC;
   constexpr uint32_t m = 1u << (LOGR + LOGC);
   constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
+  constexpr int CNT = RoundT<LOGR, true, 0>::cnt;
   const int G = P.K * P.K;
   const uint32_t cb = blockIdx.x % ncb;
-  uint32_t v = blockIdx.x / ncb;  // ((b * 2 + q) * 4 + cv) * G + g
-  const int g = (int)(v % G); v /= G;
+  uint32_t v = blockIdx.x / ncb;  // (b * 2 + q) * 4 + cv
   const int cv = (int)(v & 3); v >>= 2;
   const int q = (int)(v & 1); v >>= 1;
   const int64_t b = v;
   if (!(P.unit_mask & (1u << (cv * 2 + q)))) return;
-  if (g >= P.sched[(b * 4 + cv) * sched_stride(P.K, P.L)]) return;
+  const int ng = P.sched[(b * 4 + cv) * sched_stride(P.K, P.L)];
+  if (ng == 0) return;
   const int c = threadIdx.x & (Cb - 1);
   const int tv = threadIdx.x >> LOGCB;
-  const uint32_t p = q ? P.p[1] : P.p[0];  // no dynamic param-array index (local memory)
+  const uint32_t p = q ? P.p[1] : P.p[0];
   const uint32_t col = (cb << LOGCB) + c;
-  const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * (int64_t)m + col;
-  uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
   const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
   const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
-  sub_ntt<LOGR, true, Cb>(
-      tv, smem + c, col, C, T, p,
-      [&](int, uint32_t e) -> uint32_t { return __ldg(&in[e * C]); },
-      [&](int, uint32_t e, uint32_t val) {
-        if (e * C < lim) out[e * C] = val;
-      });
+  uint32_t nxt[16];
+  auto fetch = [&](int g) {
+    const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * (int64_t)m + col;
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0>(tv, i) * C]);
+  };
+  fetch(0);
+  for (int g = 0; g < ng; ++g) {
+    uint32_t cur[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+    if (g + 1 < ng) fetch(g + 1);
+    if (g > 0) __syncthreads();  // smem tile free
+    uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
+    sub_ntt<LOGR, true, Cb>(
+        tv, smem + c, col, C, T, p, [&](int i, uint32_t) -> uint32_t { return cur[i]; },
+        [&](int, uint32_t e, uint32_t val) {
+          if (e * C < lim) out[e * C] = val;
+        });
+  }
 }
 
 // ============================================================== fused row kernel
@@ -977,7 +1009,7 @@ static ozfft_status launch_forward_only(const Plan& pl, const int32_t* digits, i
     CP.nb = nb; CP.K = pl.K; CP.L = pl.L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
     CP.tw = tw; CP.digits = digits; CP.in_len = in_len; CP.Y = Y; CP.stats = stats;
     CP.unit_mask = 0xFF;
-    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4 * pl.K;
+    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
     launch_col_fwd(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
   }
   RowParams RP{};
@@ -1111,7 +1143,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.nb = nb; CP.K = K; CP.L = L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
     CP.tw = tw; CP.digits = SP.digits; CP.in_len = n; CP.Y = Y; CP.stats = stats;
     CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n; CP.unit_mask = A.unit_mask;
-    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4 * K;
+    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
     prof_mark(pl, OZFFT_STAGE_COL_FWD, true, st);
     launch_col_fwd(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
     prof_mark(pl, OZFFT_STAGE_COL_FWD, false, st);
@@ -1139,7 +1171,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.nb = nb; CP.K = K; CP.L = L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
     CP.tw = tw; CP.stats = stats; CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n;
     CP.unit_mask = A.unit_mask;
-    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 8 * G;
+    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 8;
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
     launch_col_inv(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
     prof_mark(pl, OZFFT_STAGE_COL_INV, false, st);
