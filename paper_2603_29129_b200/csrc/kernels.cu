@@ -466,7 +466,7 @@ __host__ __device__ constexpr int col_log_cb(int logR, int logC) {
 // One CTA per (transform, prime, part, column block) loops over the part's slices; the
 // next slice's column tile is loaded while the current one is transformed.
 template <int LOGR, int LOGC>
-__global__ void __launch_bounds__(256) k_col_fwd(ColParams P) {
+__global__ void __launch_bounds__(256, 5) k_col_fwd(ColParams P) {
   extern __shared__ uint32_t smem[];
   constexpr int LOGCB = col_log_cb(LOGR, LOGC);
   constexpr int Cb = 1 << LOGCB;
