@@ -319,10 +319,17 @@ __device__ __forceinline__ void dit_group(uint32_t* x, uint32_t rmod, uint32_t g
     for (int k = 0; k < (1 << S); ++k) {
       if (k & d) continue;
       const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);
-      const uint32_t u = x[k];
-      const uint32_t v = mul_shoup(x[k + d], w, p);
-      x[k] = add_mod(u, v, p);
-      x[k + d] = sub_mod(u, v, p);
+      const uint32_t u = x[k];  // always canonical: it was a "u" of this stage
+      const uint32_t v = mul_shoup(x[k + d], w, p);  // x[k+d] may be lazy, < 2p < 2^32
+      if (st + 1 < S && (k & (2 * d))) {
+        // both outputs are the "v" operand of the next stage, whose Shoup product accepts
+        // any 32-bit input: keep them in [0, 2p) and skip the conditional subtractions
+        x[k] = u + v;
+        x[k + d] = u + (p - v);
+      } else {
+        x[k] = add_mod(u, v, p);
+        x[k + d] = sub_mod(u, v, p);
+      }
     }
   }
 }
