@@ -270,6 +270,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         "col_inv": (inv_vec * 4 * (m + n), inv_vec * (m // 2) * logR),
         "crt_finish": (inv_vec * 4 * n + 32 * n * B, 0),
     }
+    if logR > 0:  # fused inverse column pass + CRT + DD accumulation; finish reads the DD sums
+        per_exec["col_inv"] = (inv_vec * 4 * m + 64 * n * B, inv_vec * (m // 2) * logR)
+        per_exec["crt_finish"] = (80 * n * B + 16 * n, 0)  # S (4 DD) + out per transform, chirp once
     hbm, hbm_kind = hbm_peak()
     stages = {}
     for s, (ms, cnt) in prof.items():

@@ -93,7 +93,7 @@ static void layout(Plan& pl) {
   const bool two = pl.logR > 0;
   const uint64_t per = (uint64_t)2 * K * 8 + (uint64_t)8 * K * n +
                        (two ? (uint64_t)16 * K * m + (uint64_t)32 * G * m : 0) +
-                       (uint64_t)32 * G * n + (uint64_t)32 * n;
+                       (uint64_t)32 * G * n + (uint64_t)32 * n + (two ? (uint64_t)64 * n : 0);
   int64_t chunk = (int64_t)std::max<uint64_t>(1, pl.max_ws / std::max<uint64_t>(per, 1));
   chunk = std::min<int64_t>(chunk, pl.batch);
   pl.chunk = chunk;
@@ -105,6 +105,7 @@ static void layout(Plan& pl) {
   pl.woff.Y = o;      o = align256(o + (two ? (uint64_t)chunk * 4 * K * m * 4 : 0));
   pl.woff.G = o;      o = align256(o + (two ? (uint64_t)chunk * 8 * G * m * 4 : 0));
   pl.woff.res = o;    o = align256(o + (uint64_t)chunk * 8 * G * n * 4);
+  pl.woff.S = o;      o = align256(o + (two ? (uint64_t)chunk * 4 * n * 16 : 0));
   pl.woff.io_in = o;  o = align256(o + (uint64_t)chunk * n * 16);
   pl.woff.io_out = o; o = align256(o + (uint64_t)chunk * n * 16);
   pl.woff.end = o;

@@ -45,7 +45,7 @@ struct Plan {
     uint64_t chirp, tw, W, wsplit, end;
   } poff{};
   struct {
-    uint64_t stats, sched, mu, digits, Y, G, res, io_in, io_out, end;
+    uint64_t stats, sched, mu, digits, Y, G, res, S, io_in, io_out, end;
   } woff{};
   // bound state
   bool bound = false;

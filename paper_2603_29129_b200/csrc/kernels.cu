@@ -842,6 +842,156 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
   P.out[b * P.n + j] = o;
 }
 
+// ============================================================== fused inverse column pass + CRT
+// For R > 1 the last log2(R) DIT stages, Garner's CRT and the scaled DD accumulation
+// of one real convolution run in one kernel: CTA = (transform, conv, column block),
+// looping over the conv's Alg.8 groups and both primes (next tile prefetched).  Only
+// the output rows i1 < R/2 are needed (n <= m/2), so the upper half of the last
+// stage is pruned.  Output: the conv's DD sum S_cv(j) = sum_g Z_g(j) 2^-cexp_g in
+// flush order (Alg.8 l.975-976), [nb][4][n] double2 (hi, lo).
+struct ColCrtParams {
+  int logm, K, L;
+  int64_t n, nb;
+  FinishParams F;          // CRT constants (p0, p1, p0inv, ...)
+  const uint2* tw;         // [2 prime][2 dir][m]
+  const uint32_t* G;       // [nb][2 q][4 cv][K*K][m]
+  const int32_t* sched;    // [nb][4][sched_stride]
+  double2* S;              // [nb][4][n]
+  uint32_t* res_tap;       // null, or [nb][4][2][K*K][n] (workspace res layout)
+  int64_t* crt_tap;        // null, or [nb][4][K*K][n]
+};
+
+template <int LOGR, int LOGC>
+__global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
+  extern __shared__ uint32_t smem[];
+  constexpr int LOGCB = col_log_cb(LOGR, LOGC);
+  constexpr int Cb = 1 << LOGCB;
+  constexpr uint32_t C = 1u << LOGC;
+  constexpr uint32_t m = 1u << (LOGR + LOGC);
+  constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
+  constexpr int CNT = RoundT<LOGR, true, 0>::cnt;
+  constexpr int NR = RoundT<LOGR, true, 0>::nr;
+  constexpr int NH = RoundT<LOGR, true, NR - 1>::cnt / 2;  // needed (lower-half) registers
+  constexpr int THREADS = RoundT<LOGR, true, 0>::Tv << LOGCB;
+  const int G = P.K * P.K;
+  const uint32_t cb = blockIdx.x % ncb;
+  uint32_t v = blockIdx.x / ncb;  // b * 4 + cv
+  const int cv = (int)(v & 3);
+  const int64_t b = v >> 2;
+  const int tid = threadIdx.x;
+  const int c = tid & (Cb - 1);
+  const int tv = tid >> LOGCB;
+  const uint32_t col = (cb << LOGCB) + c;
+  __shared__ double s_sc[kMaxK * kMaxK];
+  const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(P.K, P.L);
+  const int ng = srow[0];
+  for (int g = tid; g < ng; g += blockDim.x) s_sc[g] = scalbn(1.0, -srow[1 + g * (2 + 2 * P.L)]);
+  constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / 16 + 1) * Cb;
+  double2* Sacc = reinterpret_cast<double2*>(smem + TILE + (TILE & 1));  // [NH][THREADS]
+#pragma unroll
+  for (int i = 0; i < NH; ++i) Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
+  const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
+  uint32_t nxt[16];
+  auto fetch = [&](int t) {  // tile t = 2 g + q
+    const int g = t >> 1, q = t & 1;
+    const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * (int64_t)m + col;
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0>(tv, i) * C]);
+  };
+  if (ng > 0) fetch(0);
+  __syncthreads();  // s_sc ready
+  uint32_t r0[NH];
+  for (int t = 0; t < 2 * ng; ++t) {
+    const int g = t >> 1, q = t & 1;
+    uint32_t cur[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+    if (t + 1 < 2 * ng) fetch(t + 1);
+    if (t > 0) __syncthreads();  // smem tile free
+    const uint32_t p = q ? P.F.p1 : P.F.p0;
+    const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
+    uint32_t rr[NH];
+    sub_ntt<LOGR, true, Cb>(tv, smem + c, col, C, T, p,
+                            [&](int i, uint32_t) -> uint32_t { return cur[i]; },
+                            [&](int i, uint32_t, uint32_t val) {
+                              if (i < NH) rr[i] = val;  // rows >= R/2 are never needed
+                            });
+    if (P.res_tap) {
+      uint32_t* rt = P.res_tap + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
+#pragma unroll
+      for (int i = 0; i < NH; ++i) {
+        const uint32_t e = round_elem<LOGR, true, NR - 1>(tv, i);
+        if (e * C < lim) rt[e * C] = rr[i];
+      }
+    }
+    if (q == 0) {
+#pragma unroll
+      for (int i = 0; i < NH; ++i) r0[i] = rr[i];
+    } else {
+      const double sc = s_sc[g];
+#pragma unroll
+      for (int i = 0; i < NH; ++i) {
+        const uint32_t e = round_elem<LOGR, true, NR - 1>(tv, i);
+        if (e * C < lim) {
+          const long long Z = garner2(r0[i], rr[i], P.F);  // l.974
+          if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + col + e * C] = Z;
+          const double h = __ll2double_rn(Z);
+          const double l = __ll2double_rn(Z - __double2ll_rz(h));
+          double2 a = Sacc[i * THREADS + tid];
+          dd_add(a.x, a.y, __dmul_rn(h, sc), __dmul_rn(l, sc), a.x, a.y);  // l.975-976
+          Sacc[i * THREADS + tid] = a;
+        }
+      }
+    }
+  }
+  double2* So = P.S + (b * 4 + cv) * P.n + col;
+#pragma unroll
+  for (int i = 0; i < NH; ++i) {
+    const uint32_t e = round_elem<LOGR, true, NR - 1>(tv, i);
+    if (e * C < lim) So[e * C] = Sacc[i * THREADS + tid];
+  }
+}
+
+// y' = (S_rr - S_ii) + i (S_ir + S_ri), post-chirp y = y' (.) omega
+// (Alg.4 l.480-484), fp64 output; inverse direction: conj and RN division by n (O10).
+__global__ void __launch_bounds__(256) k_finish_dd(const double2* __restrict__ S,
+                                                   const int32_t* __restrict__ stats, int K,
+                                                   const double2* __restrict__ chirp,
+                                                   double2* __restrict__ out, int64_t n,
+                                                   int direction) {
+  const int64_t b = blockIdx.y;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double2 o;
+  if (stats[b * stats_stride(K) + 2 + 2 * K] & 1) {
+    o.x = __longlong_as_double(0x7FF8000000000000ll);
+    o.y = o.x;
+    out[b * n + j] = o;
+    return;
+  }
+  const double2 rr = __ldcs(&S[(b * 4 + 0) * n + j]), ii = __ldcs(&S[(b * 4 + 1) * n + j]);
+  const double2 ir = __ldcs(&S[(b * 4 + 2) * n + j]), ri = __ldcs(&S[(b * 4 + 3) * n + j]);
+  double yrh, yrl, yih, yil;
+  dd_add(rr.x, rr.y, -ii.x, -ii.y, yrh, yrl);
+  dd_add(ir.x, ir.y, ri.x, ri.y, yih, yil);
+  const double2 w = chirp[j];
+  double a1h, a1l, a2h, a2l, ore, oim, tmp;
+  dd_mul_d(yrh, yrl, w.x, a1h, a1l);
+  dd_mul_d(yih, yil, w.y, a2h, a2l);
+  dd_add(a1h, a1l, -a2h, -a2l, ore, tmp);
+  dd_mul_d(yrh, yrl, w.y, a1h, a1l);
+  dd_mul_d(yih, yil, w.x, a2h, a2l);
+  dd_add(a1h, a1l, a2h, a2l, oim, tmp);
+  if (direction > 0) {
+    const double dn = (double)n;
+    ore = __ddiv_rn(ore, dn);
+    oim = __ddiv_rn(-oim, dn);
+  }
+  o.x = ore;
+  o.y = oim;
+  out[b * n + j] = o;
+}
+
 static void fill_crt_consts(const Plan& pl, FinishParams& FP) {
   FP.p0 = pl.p[0];
   FP.p1 = pl.p[1];
@@ -1172,7 +1322,41 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     s = cuda_check("k_row_fused");
     if (s) return s;
   }
-  if (pl.logR > 0) {
+  // fused inverse column pass + CRT + DD accumulation (full transforms with R > 1)
+  const bool fused = pl.logR > 0 && A.unit_mask == 0xFFu && A.finish;
+  if (fused) {
+    ColCrtParams XP{};
+    XP.logm = pl.logm; XP.K = K; XP.L = L; XP.n = n; XP.nb = nb;
+    fill_crt_consts(pl, XP.F);
+    XP.tw = tw; XP.G = Gb; XP.sched = sched;
+    XP.S = reinterpret_cast<double2*>(ws + pl.woff.S);
+    XP.res_tap = taps && taps->res ? res : nullptr;
+    XP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
+    const size_t tile = ((1ull << pl.logR) + (1ull << pl.logR) / 16 + 1) * (1ull << c.logCb);
+    const int nh = (pl.logR >= 4 ? 16 : (1 << pl.logR)) / 2;
+    const size_t smem = (tile + (tile & 1)) * 4 + (size_t)nh * c.col_threads * 16;
+    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
+    prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
+    dispatch_log<1, 8>(pl.logR, [&](auto I) {
+      dispatch_log<11, 12>(pl.logC, [&](auto J) {
+        set_smem(k_col_inv_crt<I.value, J.value>, smem);
+        k_col_inv_crt<I.value, J.value><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+      });
+    });
+    prof_mark(pl, OZFFT_STAGE_COL_INV, false, st);
+    count_launches(1);
+    s = cuda_check("k_col_inv_crt");
+    if (s) return s;
+    dim3 grid((unsigned)((n + 255) / 256), (unsigned)nb);
+    prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
+    k_finish_dd<<<grid, 256, 0, st>>>(XP.S, stats, K, chirp, reinterpret_cast<double2*>(A.out), n,
+                                      A.direction);
+    prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
+    count_launches(1);
+    s = cuda_check("k_finish_dd");
+    if (s) return s;
+  }
+  if (pl.logR > 0 && !fused) {
     ColParams CP{};
     CP.logm = pl.logm; CP.logC = pl.logC; CP.logR = pl.logR; CP.logCb = c.logCb;
     CP.nb = nb; CP.K = K; CP.L = L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
@@ -1186,7 +1370,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     s = cuda_check("k_col_inv");
     if (s) return s;
   }
-  if (A.finish) {
+  if (A.finish && !fused) {
     FinishParams FP{};
     FP.n = n; FP.nb = nb; FP.K = K; FP.L = L; fill_crt_consts(pl, FP); FP.res = res; FP.stats = stats; FP.sched = sched;
     FP.chirp = chirp; FP.out = reinterpret_cast<double2*>(A.out); FP.direction = A.direction;
