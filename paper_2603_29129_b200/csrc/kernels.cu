@@ -343,8 +343,10 @@ template <int LOGN, bool INV, int R>
 struct RoundT {
   static constexpr int nr = (LOGN + 3) / 4;
   static constexpr int rd = INV ? (nr - 1 - R) : R;  // index in DIF order
-  static constexpr int lb = LOGN - 4 * rd;           // log2 block length
-  static constexpr int S = lb < 4 ? lb : 4;          // stages in the round
+  // the partial round (LOGN mod 4 stages) comes first in DIF order / last in DIT order,
+  // so that the step-1 round always has 16-element groups (conflict-free padded smem)
+  static constexpr int S = rd == 0 ? LOGN - 4 * (nr - 1) : 4;  // stages in the round
+  static constexpr int lb = rd == 0 ? LOGN : 4 * (nr - rd);      // log2 block length
   static constexpr int logstep = lb - S;
   static constexpr int cnt = LOGN >= 4 ? 16 : (1 << LOGN);  // elements per thread
   static constexpr int Tv = LOGN >= 4 ? (1 << (LOGN - 4)) : 1;
@@ -597,7 +599,7 @@ struct RowCfg {
   static constexpr int threads = LOGC >= 4 ? (1 << (LOGC - 4)) : 1;
   static constexpr int min_blocks = LOGC == 11 ? 6 : 1;
   // stages of the first DIT round (= last DIF round): its groups are contiguous blocks
-  static constexpr int S0 = LOGC == 0 ? 0 : LOGC - 4 * ((LOGC + 3) / 4 - 1);
+  static constexpr int S0 = LOGC >= 4 ? 4 : LOGC;
 };
 
 // Row-local storage order used for the X rows in shared memory and for the cached W
@@ -871,7 +873,12 @@ __global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
   constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
   constexpr int CNT = RoundT<LOGR, true, 0>::cnt;
   constexpr int NR = RoundT<LOGR, true, 0>::nr;
-  constexpr int NH = RoundT<LOGR, true, NR - 1>::cnt / 2;  // needed (lower-half) registers
+  // last DIT round: registers i with (i mod 2^S) < 2^(S-1) hold rows < R/2 (the only rows
+  // needed, n <= m/2); they are packed into NH slots by hslot(i)
+  constexpr int SL = RoundT<LOGR, true, NR - 1>::S;
+  constexpr int NH = RoundT<LOGR, true, NR - 1>::cnt / 2;
+  auto needed = [](int i) { return (i & ((1 << SL) - 1)) < (1 << (SL - 1)); };
+  auto hslot = [](int i) { return ((i >> SL) << (SL - 1)) + (i & ((1 << (SL - 1)) - 1)); };
   constexpr int THREADS = RoundT<LOGR, true, 0>::Tv << LOGCB;
   const int G = P.K * P.K;
   const uint32_t cb = blockIdx.x % ncb;
@@ -914,14 +921,15 @@ __global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
     sub_ntt<LOGR, true, Cb>(tv, smem + c, col, C, T, p,
                             [&](int i, uint32_t) -> uint32_t { return cur[i]; },
                             [&](int i, uint32_t, uint32_t val) {
-                              if (i < NH) rr[i] = val;  // rows >= R/2 are never needed
+                              if (needed(i)) rr[hslot(i)] = val;  // rows >= R/2 never needed
                             });
     if (P.res_tap) {
       uint32_t* rt = P.res_tap + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
 #pragma unroll
-      for (int i = 0; i < NH; ++i) {
+      for (int i = 0; i < 2 * NH; ++i) {
+        if (!needed(i)) continue;
         const uint32_t e = round_elem<LOGR, true, NR - 1>(tv, i);
-        if (e * C < lim) rt[e * C] = rr[i];
+        if (e * C < lim) rt[e * C] = rr[hslot(i)];
       }
     }
     if (q == 0) {
@@ -930,25 +938,28 @@ __global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
     } else {
       const double sc = s_sc[g];
 #pragma unroll
-      for (int i = 0; i < NH; ++i) {
+      for (int i = 0; i < 2 * NH; ++i) {
+        if (!needed(i)) continue;
         const uint32_t e = round_elem<LOGR, true, NR - 1>(tv, i);
+        const int h = hslot(i);
         if (e * C < lim) {
-          const long long Z = garner2(r0[i], rr[i], P.F);  // l.974
+          const long long Z = garner2(r0[h], rr[h], P.F);  // l.974
           if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + col + e * C] = Z;
-          const double h = __ll2double_rn(Z);
-          const double l = __ll2double_rn(Z - __double2ll_rz(h));
-          double2 a = Sacc[i * THREADS + tid];
-          dd_add(a.x, a.y, __dmul_rn(h, sc), __dmul_rn(l, sc), a.x, a.y);  // l.975-976
-          Sacc[i * THREADS + tid] = a;
+          const double hi = __ll2double_rn(Z);
+          const double lo = __ll2double_rn(Z - __double2ll_rz(hi));
+          double2 a = Sacc[h * THREADS + tid];
+          dd_add(a.x, a.y, __dmul_rn(hi, sc), __dmul_rn(lo, sc), a.x, a.y);  // l.975-976
+          Sacc[h * THREADS + tid] = a;
         }
       }
     }
   }
   double2* So = P.S + (b * 4 + cv) * P.n + col;
 #pragma unroll
-  for (int i = 0; i < NH; ++i) {
+  for (int i = 0; i < 2 * NH; ++i) {
+    if (!needed(i)) continue;
     const uint32_t e = round_elem<LOGR, true, NR - 1>(tv, i);
-    if (e * C < lim) So[e * C] = Sacc[i * THREADS + tid];
+    if (e * C < lim) So[e * C] = Sacc[hslot(i) * THREADS + tid];
   }
 }
 
@@ -1151,7 +1162,7 @@ static void launch_row(int logC, int logR, dim3 grid, const NttLaunch& c, cudaSt
     });
   }
 }
-static int row_s0(int logC) { return logC == 0 ? 0 : logC - 4 * ((logC + 3) / 4 - 1); }
+static int row_s0(int logC) { return logC >= 4 ? 4 : logC; }
 
 // Forward NTT of digit vectors [nb][2][K][in_len] into internal-order spectra Xout
 // [nb][2 q][2 a][K][m] (used at plan time for omega~*; the hot path fuses the row part).
