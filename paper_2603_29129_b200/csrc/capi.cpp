@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -186,6 +187,10 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
   }
   // NTT decomposition: one pass up to m = 2^12, else rows of C = 2^11 (2^12 at m = 2^20)
   pl->logC = logm <= 12 ? logm : std::max(11, logm - 8);
+  if (const char* t = std::getenv("OZFFT_TUNE_LOGC")) {  // tuning knob (tools/, not the hot path)
+    const int v = std::atoi(t);
+    if (v >= 11 && v <= 12 && logm > v && logm - v <= 8) pl->logC = v;
+  }
   pl->logR = logm - pl->logC;
   pl->alpha = compute_alpha(desc.n, desc.L, p0, p1);
   if (pl->alpha < 1) {
@@ -296,15 +301,47 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
                                 void* stream) {
   ozfft_status s = check_exec(pl, in, out, direction);
   if (s) return s;
+  ozfft_plan* mp = const_cast<ozfft_plan*>(pl);
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = pl->n;
-  double* din = reinterpret_cast<double*>(pl->ws + pl->woff.io_in);
-  double* dout = reinterpret_cast<double*>(pl->ws + pl->woff.io_out);
-  for (int64_t b0 = 0; b0 < pl->batch; b0 += pl->chunk) {
-    const int64_t nb = std::min<int64_t>(pl->chunk, pl->batch - b0);
-    const size_t bytes = (size_t)nb * n * 16;
-    s = check_cuda(cudaMemcpyAsync(din, in + 2 * b0 * n, bytes, cudaMemcpyHostToDevice, st), "H2D");
+  // sub-batches of sb transforms; nslots staging slots (ring) in the io_in / io_out areas
+  const int64_t sb = std::max<int64_t>(1, std::min<int64_t>(pl->chunk, (pl->batch + 3) / 4));
+  const int64_t nsub = (pl->batch + sb - 1) / sb;
+  const int64_t nslots = std::max<int64_t>(1, std::min<int64_t>(4, pl->chunk / sb));
+  if (!mp->pipe) {
+    mp->pipe = new HostPipe();
+    cudaStream_t a, b;
+    if (cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking) != cudaSuccess)
+      return check_cuda(cudaGetLastError(), "copy stream create");
+    mp->pipe->h2d = (void*)a;
+    mp->pipe->d2h = (void*)b;
+  }
+  HostPipe& hp = *mp->pipe;
+  while ((int64_t)hp.ev.size() < 3 * nsub + 1) {
+    cudaEvent_t e;
+    s = check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
     if (s) return s;
+    hp.ev.push_back((void*)e);
+  }
+  cudaStream_t h2d = (cudaStream_t)hp.h2d, d2h = (cudaStream_t)hp.d2h;
+  auto ev = [&](int64_t k) { return (cudaEvent_t)hp.ev[k]; };
+  // copies start after everything already queued on the caller's stream
+  cudaEventRecord(ev(3 * nsub), st);
+  cudaStreamWaitEvent(h2d, ev(3 * nsub), 0);
+  double* din0 = reinterpret_cast<double*>(pl->ws + pl->woff.io_in);
+  double* dout0 = reinterpret_cast<double*>(pl->ws + pl->woff.io_out);
+  for (int64_t j = 0; j < nsub; ++j) {
+    const int64_t b0 = j * sb, nb = std::min<int64_t>(sb, pl->batch - b0);
+    const size_t bytes = (size_t)nb * n * 16;
+    double* din = din0 + 2 * (j % nslots) * sb * n;
+    double* dout = dout0 + 2 * (j % nslots) * sb * n;
+    if (j >= nslots) cudaStreamWaitEvent(h2d, ev(3 * (j - nslots) + 1), 0);  // in-slot consumed
+    s = check_cuda(cudaMemcpyAsync(din, in + 2 * b0 * n, bytes, cudaMemcpyHostToDevice, h2d), "H2D");
+    if (s) return s;
+    cudaEventRecord(ev(3 * j + 0), h2d);
+    cudaStreamWaitEvent(st, ev(3 * j + 0), 0);
+    if (j >= nslots) cudaStreamWaitEvent(st, ev(3 * (j - nslots) + 2), 0);  // out-slot drained
     ExecArgs a{};
     a.nb = nb;
     a.in = din;
@@ -315,10 +352,14 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
     a.finish = true;
     s = launch_execute(*pl, a, stream);
     if (s) return s;
-    s = check_cuda(cudaMemcpyAsync(out + 2 * b0 * n, dout, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    cudaEventRecord(ev(3 * j + 1), st);
+    cudaStreamWaitEvent(d2h, ev(3 * j + 1), 0);
+    s = check_cuda(cudaMemcpyAsync(out + 2 * b0 * n, dout, bytes, cudaMemcpyDeviceToHost, d2h), "D2H");
     if (s) return s;
+    cudaEventRecord(ev(3 * j + 2), d2h);
   }
-  const_cast<ozfft_plan*>(pl)->last_batch = pl->batch;
+  cudaStreamWaitEvent(st, ev(3 * (nsub - 1) + 2), 0);
+  mp->last_batch = pl->batch;
   return check_cuda(cudaStreamSynchronize(st), "execute_host sync");
 }
 
@@ -450,6 +491,12 @@ ozfft_status ozfft_profile_read(ozfft_plan* pl, double* ms, int64_t* launches, v
 uint64_t ozfft_kernel_launches(void) { return g_launches.load(); }
 
 ozfft_status ozfft_plan_destroy(ozfft_plan* pl) {
+  if (pl && pl->pipe) {
+    for (void* e : pl->pipe->ev) cudaEventDestroy((cudaEvent_t)e);
+    if (pl->pipe->h2d) cudaStreamDestroy((cudaStream_t)pl->pipe->h2d);
+    if (pl->pipe->d2h) cudaStreamDestroy((cudaStream_t)pl->pipe->d2h);
+    delete pl->pipe;
+  }
   if (pl && pl->prof) {
     for (void* e : pl->prof->pool) cudaEventDestroy((cudaEvent_t)e);
     delete pl->prof;

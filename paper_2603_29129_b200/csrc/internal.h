@@ -55,6 +55,15 @@ struct Plan {
   int32_t Ew[2][kMaxK] = {{0}};
   int64_t last_batch = 0;  // transforms covered by the per-batch stats arrays
   struct Prof* prof = nullptr;  // profiling state (mutable through the pointer)
+  struct HostPipe* pipe = nullptr;  // copy streams/events of ozfft_execute_host (lazy)
+};
+
+// Copy/compute pipelining of ozfft_execute_host: H2D and D2H run on their own streams,
+// overlapping the device pipeline of neighbouring sub-batches.
+struct HostPipe {
+  void* h2d = nullptr;
+  void* d2h = nullptr;
+  std::vector<void*> ev;  // cudaEvent_t, 3 per sub-batch
 };
 
 // Per-stage CUDA-event timers (ozfft_profile_*).

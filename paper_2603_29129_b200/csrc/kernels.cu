@@ -629,7 +629,6 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
   const int q = (blockIdx.y >> 1) & 1;
   const uint32_t row = blockIdx.y >> 2;
   constexpr int logC = LOGC;
-  constexpr int S0 = RowCfg<LOGC>::S0;
   constexpr uint32_t C = 1u << logC;
   constexpr uint32_t padC = C + (C >> 4) + 1;
   const int tv = threadIdx.x;
