@@ -38,6 +38,7 @@ struct Plan {
   std::vector<double> wstar;       // [m][2] omega~* = ZeroPad_pm(conj(omega), m)
   std::vector<uint32_t> tw[2][2];  // [prime][dir] -> [m][2] = (w, shoup) at T[h + j] = w_{2h}^{+-j}
   uint32_t minv[2] = {0, 0};       // m^{-1} mod p
+  uint32_t pinv[2] = {0, 0};       // -p^{-1} mod 2^32 (Montgomery REDC)
   uint32_t p0inv_mod_p1 = 0;       // Garner constant
   // sizes and layout
   uint64_t persistent_bytes = 0, workspace_bytes = 0;

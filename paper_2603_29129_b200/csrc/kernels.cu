@@ -47,6 +47,17 @@ __device__ __forceinline__ uint32_t mul_shoup(uint32_t a, uint2 w, uint32_t p) {
   return min(r, r - p);
 }
 
+// T * 2^-32 mod p for T < 3 p^2 (a sum of at most three products of residues), p < 2^31:
+// fold the high word below p (T < 2p 2^32), then Montgomery REDC with pinv = -p^{-1} mod 2^32.
+__device__ __forceinline__ uint32_t redc_lazy3(unsigned long long T, uint32_t p, uint32_t pinv) {
+  uint32_t th = (uint32_t)(T >> 32);
+  const uint32_t tl = (uint32_t)T;
+  th = min(th, th - p);
+  const uint32_t mq = tl * pinv;
+  const uint32_t r = th + __umulhi(mq, p) + (tl != 0u ? 1u : 0u);  // (T + mq p) / 2^32 < 2p
+  return min(r, r - p);
+}
+
 // ============================================================== double-double (DD)
 // Fixed IEEE RN operation sequences (no contraction): must match the oracle bit for bit.
 __device__ __forceinline__ void two_prod(double a, double b, double& p, double& e) {
@@ -582,7 +593,8 @@ struct RowParams {
   const int32_t* digits;  // R == 1: [nb][2][K][in_len]
   int64_t in_len;
   const uint32_t* Y;      // R > 1: [nb][2][2][K][m]
-  const uint2* W;         // [2 q][2 b][K][m] (W m^{-1}, Shoup)
+  const uint32_t* W;      // [2 q][2 b][K][m] Montgomery form W m^{-1} 2^32 mod p (row_perm)
+  uint32_t pinv[2];       // -p^{-1} mod 2^32 (Montgomery)
   uint32_t* G;            // R > 1: [nb][2 q][4][K*K][m]
   uint32_t* res;          // R == 1: [nb][4][2][K*K][n]
   int64_t n;
@@ -698,22 +710,35 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
     const int bw = conv_b(cv);
     __syncthreads();  // group table visible; `work` free
     const int ng = s_ng[ci];
-    const uint2* Wb = P.W + (size_t)(q * 2 + bw) * K * m + rowoff;
+    const uint32_t* Wb = P.W + (size_t)(q * 2 + bw) * K * m + rowoff;
+    const uint32_t pinv = q ? P.pinv[1] : P.pinv[0];
     for (int g = 0; g < ng; ++g) {
       if (g > 0) __syncthreads();
       const uint32_t* tg = tab + (ci * G + g) * tstride;
       const int np = (int)tg[0];
-      // pointwise products for this thread's round-0 elements, all loads of a pair batched
+      // pointwise products for this thread's round-0 elements: 64-bit lazy sums of up to 3
+      // products X * W~ (W~ = W m^{-1} 2^32, < 3 p^2 < 2^64), one Montgomery reduction each
       uint32_t z[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) z[i] = 0;
-      for (int ip = 0; ip < np; ++ip) {
-        const uint32_t* xr = Xs + tg[1 + 2 * ip];
-        const uint2* wr = Wb + tg[2 + 2 * ip];
+      for (int ip0 = 0; ip0 < np; ip0 += 3) {
+        unsigned long long T[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) T[i] = 0ull;
+        const int ipe = min(np, ip0 + 3);
+        for (int ip = ip0; ip < ipe; ++ip) {
+          const uint32_t* xr = Xs + tg[1 + 2 * ip];
+          const uint32_t* wr = Wb + tg[2 + 2 * ip];
+#pragma unroll
+          for (int i = 0; i < CNT; ++i) {
+            const uint32_t pe = row_slot<LOGC>(tv, i);  // == row_perm(round-0 element)
+            T[i] += (unsigned long long)xr[pe] * __ldg(&wr[pe]);
+          }
+        }
 #pragma unroll
         for (int i = 0; i < CNT; ++i) {
-          const uint32_t pe = row_slot<LOGC>(tv, i);  // == row_perm(round-0 element)
-          z[i] = add_mod(z[i], mul_shoup(xr[pe], __ldg(&wr[pe]), p), p);
+          const uint32_t r = redc_lazy3(T[i], p, pinv);
+          z[i] = ip0 == 0 ? r : add_mod(z[i], r, p);
         }
       }
       uint32_t* Zt = P.Zout ? P.Zout + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff : nullptr;
@@ -1012,9 +1037,9 @@ static void fill_crt_consts(const Plan& pl, FinishParams& FP) {
 }
 
 // ============================================================== small utility kernels
-// W finalize: Wp[q][b][t][row*C + row_perm(e)] = (W m^{-1} mod p, Shoup companion) from the
-// forward spectra X[q][b][t][row*C + e] (internal order).
-__global__ void k_w_finalize(const uint32_t* __restrict__ X, uint2* __restrict__ Wp, int K,
+// W finalize: W~[q][b][t][row*C + row_perm(e)] = W m^{-1} 2^32 mod p (Montgomery form for the
+// pointwise REDC) from the forward spectra X[q][b][t][row*C + e] (internal order).
+__global__ void k_w_finalize(const uint32_t* __restrict__ X, uint32_t* __restrict__ Wm, int K,
                              int64_t m, int logC, int S0, uint32_t p0, uint32_t p1, uint32_t minv0,
                              uint32_t minv1) {
   const int64_t total = (int64_t)4 * K * m;
@@ -1025,16 +1050,16 @@ __global__ void k_w_finalize(const uint32_t* __restrict__ X, uint2* __restrict__
     const uint32_t w = (uint32_t)(((uint64_t)X[i] * mi) % p);
     const int64_t e = i & ((1ll << logC) - 1);
     const int64_t dst = (i - e) + row_perm((uint32_t)e, logC, S0);
-    Wp[dst] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));
+    Wm[dst] = (uint32_t)(((uint64_t)w << 32) % p);
   }
 }
 
-// Tap conversion: internal bit-reversed order (optionally row-permuted, optionally times
-// m mod p) -> natural order:  dst[o(v)][k] = src[v][pos(bitrev(k))] (* m mod p).
+// Tap conversion: internal bit-reversed order (optionally row-permuted, optionally times a
+// per-vector constant mod p) -> natural order:  dst[o(v)][k] = src[v][pos(bitrev(k))] * mult[v].
 __global__ void k_tap_permute(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                               int64_t nvec, int logm, const int64_t* __restrict__ dst_off,
-                              const uint32_t* __restrict__ vec_p, uint32_t mult_is_m, int logC,
-                              int S0) {
+                              const uint32_t* __restrict__ vec_p,
+                              const uint32_t* __restrict__ vec_mult, int logC, int S0) {
   const int64_t m = 1ll << logm;
   const int64_t total = nvec * m;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -1046,7 +1071,7 @@ __global__ void k_tap_permute(const uint32_t* __restrict__ src, uint32_t* __rest
       br = (br - e) + row_perm((uint32_t)e, logC, S0);
     }
     uint32_t val = src[v * m + br];
-    if (mult_is_m) val = (uint32_t)(((uint64_t)val * (uint64_t)(m % vec_p[v])) % vec_p[v]);
+    if (vec_mult) val = (uint32_t)(((uint64_t)val * vec_mult[v]) % vec_p[v]);
     dst[dst_off[v] + k] = val;
   }
 }
@@ -1244,7 +1269,7 @@ ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
       }
     cudaMemcpyAsync(pl.pers + pl.poff.wsplit, wsplit, sizeof(int32_t) * (2 + 2 * K),
                     cudaMemcpyHostToDevice, st);
-    k_w_finalize<<<592, 256, 0, st>>>(X, reinterpret_cast<uint2*>(pl.pers + pl.poff.W), K, m,
+    k_w_finalize<<<592, 256, 0, st>>>(X, reinterpret_cast<uint32_t*>(pl.pers + pl.poff.W), K, m,
                                       pl.logC, row_s0(pl.logC), pl.p[0], pl.p[1], pl.minv[0],
                                       pl.minv[1]);
     s = cuda_check("W finalize");
@@ -1272,7 +1297,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   uint32_t* Gb = reinterpret_cast<uint32_t*>(ws + pl.woff.G);
   uint32_t* res = reinterpret_cast<uint32_t*>(ws + pl.woff.res);
   const uint2* tw = reinterpret_cast<const uint2*>(pl.pers + pl.poff.tw);
-  const uint2* W = reinterpret_cast<const uint2*>(pl.pers + pl.poff.W);
+  const uint32_t* W = reinterpret_cast<const uint32_t*>(pl.pers + pl.poff.W);
   const double2* chirp = reinterpret_cast<const double2*>(pl.pers + pl.poff.chirp);
   const int32_t* wsplit = reinterpret_cast<const int32_t*>(pl.pers + pl.poff.wsplit);
   const ozfft_taps* taps = A.taps;
@@ -1321,7 +1346,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   RowParams RP{};
   RP.logm = pl.logm; RP.logC = pl.logC; RP.logR = pl.logR; RP.nb = nb; RP.K = K; RP.L = L;
   RP.p[0] = pl.p[0]; RP.p[1] = pl.p[1]; RP.tw = tw; RP.digits = SP.digits; RP.in_len = n;
-  RP.Y = Y; RP.W = W; RP.G = Gb; RP.res = res; RP.n = n; RP.stats = stats; RP.sched = sched;
+  RP.Y = Y; RP.W = W; RP.pinv[0] = pl.pinv[0]; RP.pinv[1] = pl.pinv[1]; RP.G = Gb; RP.res = res; RP.n = n; RP.stats = stats; RP.sched = sched;
   RP.unit_mask = A.unit_mask; RP.fwd_only = 0; RP.Xout = Xtap; RP.Zout = Ztap;
   {
     dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
@@ -1396,21 +1421,35 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   // ---- taps (test only): convert internal orders to the oracle's natural layouts
   if (taps) {
     std::vector<int64_t> off;
-    std::vector<uint32_t> vp;
+    std::vector<uint32_t> vp, vm;
+    // per-vector constants: m (undo m^-1 folded into W) and m 2^-32 (Montgomery W~)
+    uint32_t mconst[2], mmont[2];
+    for (int q = 0; q < 2; ++q) {
+      const uint64_t pq = pl.p[q];
+      mconst[q] = (uint32_t)((uint64_t)m % pq);
+      uint64_t inv2_32 = 1;  // 2^-32 mod p = (2^-1)^32
+      const uint64_t half = (pq + 1) / 2;
+      for (int i = 0; i < 32; ++i) inv2_32 = inv2_32 * half % pq;
+      mmont[q] = (uint32_t)((uint64_t)mconst[q] * inv2_32 % pq);
+    }
     auto run_perm = [&](const uint32_t* src, void* dst, bool mult, bool rowperm) -> ozfft_status {
       int64_t* doff = nullptr;
-      uint32_t* dvp = nullptr;
+      uint32_t *dvp = nullptr, *dvm = nullptr;
       const int64_t nvec = (int64_t)off.size();
       cudaMalloc(&doff, sizeof(int64_t) * nvec);
       cudaMalloc(&dvp, sizeof(uint32_t) * nvec);
+      cudaMalloc(&dvm, sizeof(uint32_t) * nvec);
       cudaMemcpyAsync(doff, off.data(), sizeof(int64_t) * nvec, cudaMemcpyHostToDevice, st);
       cudaMemcpyAsync(dvp, vp.data(), sizeof(uint32_t) * nvec, cudaMemcpyHostToDevice, st);
+      if (mult) cudaMemcpyAsync(dvm, vm.data(), sizeof(uint32_t) * nvec, cudaMemcpyHostToDevice, st);
       k_tap_permute<<<1184, 256, 0, st>>>(src, reinterpret_cast<uint32_t*>(dst), nvec, pl.logm,
-                                          doff, dvp, mult ? 1u : 0u, rowperm ? pl.logC : -1,
+                                          doff, dvp, mult ? dvm : nullptr, rowperm ? pl.logC : -1,
                                           row_s0(pl.logC));
       cudaStreamSynchronize(st);
       cudaFree(doff);
       cudaFree(dvp);
+      cudaFree(dvm);
+      vm.clear();
       return cuda_check("tap permute");
     };
     if (taps->X) {  // src [b][q][a][s][m] -> dst [b][a][s][q][m]
@@ -1433,6 +1472,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
             for (int g = 0; g < G; ++g) {
               off.push_back((((b * 4 + cv) * G + g) * 2 + q) * m);
               vp.push_back(pl.p[q]);
+              vm.push_back(mconst[q]);
             }
       s = run_perm(Ztap, taps->Z, true, false);
       if (s) return s;
@@ -1449,20 +1489,16 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     if (taps->sched)
       cudaMemcpyAsync(taps->sched, sched, sizeof(int32_t) * nb * 4 * sched_stride(K, L),
                       cudaMemcpyDeviceToDevice, st);
-    if (taps->W) {  // src Wp [q][b][t][m] (uint2, m^-1 scaled) -> [b][t][q][m] times m
-      uint32_t* tmp = nullptr;
-      cudaMalloc(&tmp, sizeof(uint32_t) * 4 * K * m);
-      cudaMemcpy2DAsync(tmp, sizeof(uint32_t), W, sizeof(uint2), sizeof(uint32_t), 4 * K * m,
-                        cudaMemcpyDeviceToDevice, st);
+    if (taps->W) {  // src W~ [q][b][t][m] (W m^-1 2^32) -> [b][t][q][m] times m 2^-32
       off.clear(); vp.clear();
       for (int q = 0; q < 2; ++q)
         for (int bw = 0; bw < 2; ++bw)
           for (int t = 0; t < K; ++t) {
             off.push_back(((bw * K + t) * 2 + q) * m);
             vp.push_back(pl.p[q]);
+            vm.push_back(mmont[q]);
           }
-      s = run_perm(tmp, taps->W, true, true);
-      cudaFree(tmp);
+      s = run_perm(W, taps->W, true, true);
       if (s) return s;
     }
     if (taps->E || taps->kv) {

@@ -88,6 +88,9 @@ ozfft_status build_plan_tables(Plan& pl) {
     const uint32_t wm = pow_mod(generator(p), (uint64_t)(p - 1) / (uint64_t)m, p);
     const uint32_t wmi = pow_mod(wm, p - 2, p);
     pl.minv[q] = pow_mod((uint64_t)m % p, p - 2, p);
+    uint32_t inv = p;  // p^{-1} mod 2^32 by Newton iteration (p odd)
+    for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
+    pl.pinv[q] = 0u - inv;
     for (int dir = 0; dir < 2; ++dir) {
       std::vector<uint32_t>& T = pl.tw[q][dir];
       T.assign((size_t)2 * std::max<int64_t>(m, 2), 0);
