@@ -48,7 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s] + hdrs + [__file__]):
-            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
+            extra = os.environ.get("OZFFT_NVCC_EXTRA", "").split()
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", *extra,
                    "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
                    "-c", s, "-o", o]
             subprocess.check_call(cmd)

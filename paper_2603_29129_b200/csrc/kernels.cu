@@ -609,7 +609,10 @@ struct RowParams {
 template <int LOGC>
 struct RowCfg {
   static constexpr int threads = LOGC >= 4 ? (1 << (LOGC - 4)) : 1;
-  static constexpr int min_blocks = LOGC == 11 ? 6 : 1;
+#ifndef OZ_ROW_MINB
+#define OZ_ROW_MINB 5
+#endif
+  static constexpr int min_blocks = LOGC == 11 ? OZ_ROW_MINB : 1;
   // stages of the first DIT round (= last DIF round): its groups are contiguous blocks
   static constexpr int S0 = LOGC >= 4 ? 4 : LOGC;
 };
