@@ -301,9 +301,9 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
 // A group of 2^S registers x[k] holding global positions gbase + k*gstep, with
 // rmod = gbase mod gstep.  DIF stages h = gstep*2^(S-1) .. gstep (block length 2h):
 //   (u, v) -> (u + v, (u - v) * T[h + (pos mod h)]),  T[h + j] = w_{2h}^j.
-template <int S>
-__device__ __forceinline__ void dif_group(uint32_t* x, uint32_t rmod, uint32_t gstep,
-                                          const uint2* __restrict__ T, uint32_t p) {
+template <int S, int NV>
+__device__ __forceinline__ void dif_group(uint32_t (&x)[NV][16], int off, uint32_t rmod,
+                                          uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
 #pragma unroll
   for (int st = S - 1; st >= 0; --st) {
     const int d = 1 << st;
@@ -311,17 +311,20 @@ __device__ __forceinline__ void dif_group(uint32_t* x, uint32_t rmod, uint32_t g
 #pragma unroll
     for (int k = 0; k < (1 << S); ++k) {
       if (k & d) continue;
-      const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);
-      const uint32_t u = x[k], v = x[k + d];
-      x[k] = add_mod(u, v, p);
-      x[k + d] = mul_shoup(u + (p - v), w, p);
+      const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);  // shared by NV
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const uint32_t a = x[v][off + k], b = x[v][off + k + d];
+        x[v][off + k] = add_mod(a, b, p);
+        x[v][off + k + d] = mul_shoup(a + (p - b), w, p);
+      }
     }
   }
 }
 // DIT stages h = gstep .. gstep*2^(S-1): v' = v * Tinv[h + (pos mod h)]; (u + v', u - v')
-template <int S>
-__device__ __forceinline__ void dit_group(uint32_t* x, uint32_t rmod, uint32_t gstep,
-                                          const uint2* __restrict__ T, uint32_t p) {
+template <int S, int NV>
+__device__ __forceinline__ void dit_group(uint32_t (&x)[NV][16], int off, uint32_t rmod,
+                                          uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
 #pragma unroll
   for (int st = 0; st < S; ++st) {
     const int d = 1 << st;
@@ -329,17 +332,20 @@ __device__ __forceinline__ void dit_group(uint32_t* x, uint32_t rmod, uint32_t g
 #pragma unroll
     for (int k = 0; k < (1 << S); ++k) {
       if (k & d) continue;
-      const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);
-      const uint32_t u = x[k];  // always canonical: it was a "u" of this stage
-      const uint32_t v = mul_shoup(x[k + d], w, p);  // x[k+d] may be lazy, < 2p < 2^32
-      if (st + 1 < S && (k & (2 * d))) {
-        // both outputs are the "v" operand of the next stage, whose Shoup product accepts
-        // any 32-bit input: keep them in [0, 2p) and skip the conditional subtractions
-        x[k] = u + v;
-        x[k + d] = u + (p - v);
-      } else {
-        x[k] = add_mod(u, v, p);
-        x[k + d] = sub_mod(u, v, p);
+      const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);  // shared by NV
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const uint32_t a = x[v][off + k];  // always canonical: it was a "u" of this stage
+        const uint32_t b = mul_shoup(x[v][off + k + d], w, p);  // input may be lazy (< 2p)
+        if (st + 1 < S && (k & (2 * d))) {
+          // both outputs are the "v" operand of the next stage, whose Shoup product
+          // accepts any 32-bit input: keep them in [0, 2p), skip the subtractions
+          x[v][off + k] = a + b;
+          x[v][off + k + d] = a + (p - b);
+        } else {
+          x[v][off + k] = add_mod(a, b, p);
+          x[v][off + k + d] = sub_mod(a, b, p);
+        }
       }
     }
   }
@@ -386,68 +392,86 @@ __device__ __forceinline__ uint32_t* round_slot(uint32_t* sm, int tv, int i) {
   return sm + (pad_idx(base) + ks + (ks >> 4)) * CB;
 }
 
-template <int LOGN, bool INV, int R, int CB, class LoadF, class StoreF>
-__device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[16], int tv, uint32_t* __restrict__ sm,
-                                              uint32_t gb_mod, uint32_t gs,
-                                              const uint2* __restrict__ T, uint32_t p,
+template <int LOGN, bool INV, int R, int CB, int NV, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][16], int tv,
+                                              uint32_t* const (&sm)[NV], uint32_t gb_mod,
+                                              uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                               LoadF& load_first, StoreF& store_last) {
   using RT = RoundT<LOGN, INV, R>;
   constexpr uint32_t step = 1u << RT::logstep;
 #pragma unroll
-  for (int i = 0; i < RT::cnt; ++i) {
-    if constexpr (R == 0)
-      x[i] = load_first(i, round_elem<LOGN, INV, R>(tv, i));
-    else
-      x[i] = *round_slot<LOGN, INV, R, CB>(sm, tv, i);
-  }
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int i = 0; i < RT::cnt; ++i) {
+      if constexpr (R == 0)
+        x[v][i] = load_first(v, i, round_elem<LOGN, INV, R>(tv, i));
+      else
+        x[v][i] = *round_slot<LOGN, INV, R, CB>(sm[v], tv, i);
+    }
 #pragma unroll
   for (int u = 0; u < (RT::cnt >> RT::S); ++u) {
     const uint32_t g = (uint32_t)(tv + u * RT::Tv);
     const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
     if constexpr (INV)
-      dit_group<RT::S>(x + u * (1 << RT::S), rmod, step * gs, T, p);
+      dit_group<RT::S, NV>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     else
-      dif_group<RT::S>(x + u * (1 << RT::S), rmod, step * gs, T, p);
+      dif_group<RT::S, NV>(x, u * (1 << RT::S), rmod, step * gs, T, p);
   }
 #pragma unroll
-  for (int i = 0; i < RT::cnt; ++i) {
-    if constexpr (R == RT::nr - 1)
-      store_last(i, round_elem<LOGN, INV, R>(tv, i), x[i]);
-    else
-      *round_slot<LOGN, INV, R, CB>(sm, tv, i) = x[i];
-  }
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int i = 0; i < RT::cnt; ++i) {
+      if constexpr (R == RT::nr - 1)
+        store_last(v, i, round_elem<LOGN, INV, R>(tv, i), x[v][i]);
+      else
+        *round_slot<LOGN, INV, R, CB>(sm[v], tv, i) = x[v][i];
+    }
   if constexpr (R != RT::nr - 1) __syncthreads();
 }
 
-template <int LOGN, bool INV, int R, int CB, class LoadF, class StoreF>
-__device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[16], int tv, uint32_t* __restrict__ sm,
-                                               uint32_t gb_mod, uint32_t gs,
-                                               const uint2* __restrict__ T, uint32_t p,
+template <int LOGN, bool INV, int R, int CB, int NV, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][16], int tv,
+                                               uint32_t* const (&sm)[NV], uint32_t gb_mod,
+                                               uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                                LoadF& load_first, StoreF& store_last) {
   if constexpr (R < RoundT<LOGN, INV, 0>::nr) {
-    sub_ntt_round<LOGN, INV, R, CB>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
-    sub_ntt_rounds<LOGN, INV, R + 1, CB>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
+    sub_ntt_round<LOGN, INV, R, CB, NV>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
   }
 }
 
-// Length-2^LOGN sub-transform executed cooperatively by 2^max(LOGN-4,0) threads (index
-// tv), 16 elements per thread per round (N >= 16) in rounds of <= 4 radix-2 stages, with
-// shared memory (padded, interleave Cb) between rounds.
+// Length-2^LOGN sub-transforms of NV vectors at the same positions, executed cooperatively
+// by 2^max(LOGN-4,0) threads (index tv), 16 elements per thread and vector per round (N >=
+// 16) in rounds of <= 4 radix-2 stages; twiddles are loaded once for the NV vectors, and
+// shared memory (padded, interleave CB) is used between rounds (one buffer per vector).
 //   INV = false: DIF stages len = N .. 2;   INV = true: DIT stages len = 2 .. N.
 // Element e has global position gbase_vec + e*gs; gb_mod = gbase_vec mod (gs*step) for
-// every step used (0 for rows, the column index for columns).  load_first(i, e) gives the
-// round-0 input of register i / element e; store_last(i, e, v) consumes the final values.  `sm` must be free for
-// writes (caller-synchronised) on entry.
+// every step used (0 for rows, the column index for columns).  load_first(v, i, e) gives
+// the round-0 input of register i / element e of vector v; store_last(v, i, e, val)
+// consumes the final values.  The buffers must be free for writes on entry.
+template <int LOGN, bool INV, int CB, int NV, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV], uint32_t gb_mod,
+                                              uint32_t gs, const uint2* __restrict__ T, uint32_t p,
+                                              LoadF&& load_first, StoreF&& store_last) {
+  if constexpr (LOGN == 0) {  // N == 1: identity
+    if (tv == 0)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) store_last(v, 0, 0u, load_first(v, 0, 0u));
+  } else {
+    uint32_t x[NV][16];
+    sub_ntt_rounds<LOGN, INV, 0, CB, NV>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
+  }
+}
+
+// Single-vector form: load_first(i, e), store_last(i, e, val).
 template <int LOGN, bool INV, int CB, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, uint32_t gb_mod,
                                         uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                         LoadF&& load_first, StoreF&& store_last) {
-  if constexpr (LOGN == 0) {  // N == 1: identity
-    if (tv == 0) store_last(0, 0u, load_first(0, 0u));
-  } else {
-    uint32_t x[16];
-    sub_ntt_rounds<LOGN, INV, 0, CB>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
-  }
+  uint32_t* const sms[1] = {sm};
+  sub_ntt_multi<LOGN, INV, CB, 1>(
+      tv, sms, gb_mod, gs, T, p, [&](int, int i, uint32_t e) { return load_first(i, e); },
+      [&](int, int i, uint32_t e, uint32_t v) { store_last(i, e, v); });
 }
 
 __device__ __forceinline__ uint32_t lift(int32_t D, uint32_t p) {
@@ -706,62 +730,75 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
   }
   if (P.fwd_only) return;
   // ---- per group: Z = sum X_s (.) W_t (Alg.8 l.981-982), then the first log2(C) DIT
-  // stages of its inverse NTT (l.973)
+  // stages of its inverse NTT (l.973).  The (conv, group) items of both convolutions are
+  // processed two at a time: their twiddles are shared and one barrier serves both.
   constexpr int CNT = RoundT<LOGC, true, 0>::cnt;
-  for (int ci = 0; ci < 2; ++ci) {
+  const uint32_t pinv = q ? P.pinv[1] : P.pinv[0];
+  __syncthreads();  // group table visible
+  const int ng0 = s_ng[0], nitems = s_ng[0] + s_ng[1];
+  auto item = [&](int it, int& ci, int& g) {
+    ci = it < ng0 ? 0 : 1;
+    g = it < ng0 ? it : it - ng0;
+  };
+  // pointwise products for this thread's round-0 elements: 64-bit lazy sums of up to 3
+  // products X * W~ (W~ = W m^{-1} 2^32, sums < 3 p^2 < 2^64), one Montgomery reduction each
+  auto pointwise = [&](int ci, int g, uint32_t (&z)[16]) {
     const int cv = ci ? cv1 : cv0;
-    const int bw = conv_b(cv);
-    __syncthreads();  // group table visible; `work` free
-    const int ng = s_ng[ci];
-    const uint32_t* Wb = P.W + (size_t)(q * 2 + bw) * K * m + rowoff;
-    const uint32_t pinv = q ? P.pinv[1] : P.pinv[0];
-    for (int g = 0; g < ng; ++g) {
-      if (g > 0) __syncthreads();
-      const uint32_t* tg = tab + (ci * G + g) * tstride;
-      const int np = (int)tg[0];
-      // pointwise products for this thread's round-0 elements: 64-bit lazy sums of up to 3
-      // products X * W~ (W~ = W m^{-1} 2^32, < 3 p^2 < 2^64), one Montgomery reduction each
-      uint32_t z[16];
+    const uint32_t* Wb = P.W + (size_t)(q * 2 + conv_b(cv)) * K * m + rowoff;
+    const uint32_t* tg = tab + (ci * G + g) * tstride;
+    const int np = (int)tg[0];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) z[i] = 0;
-      for (int ip0 = 0; ip0 < np; ip0 += 3) {
-        unsigned long long T[16];
+    for (int i = 0; i < 16; ++i) z[i] = 0;
+    for (int ip0 = 0; ip0 < np; ip0 += 3) {
+      unsigned long long T[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) T[i] = 0ull;
-        const int ipe = min(np, ip0 + 3);
-        for (int ip = ip0; ip < ipe; ++ip) {
-          const uint32_t* xr = Xs + tg[1 + 2 * ip];
-          const uint32_t* wr = Wb + tg[2 + 2 * ip];
-#pragma unroll
-          for (int i = 0; i < CNT; ++i) {
-            const uint32_t pe = row_slot<LOGC>(tv, i);  // == row_perm(round-0 element)
-            T[i] += (unsigned long long)xr[pe] * __ldg(&wr[pe]);
-          }
-        }
+      for (int i = 0; i < 16; ++i) T[i] = 0ull;
+      const int ipe = min(np, ip0 + 3);
+      for (int ip = ip0; ip < ipe; ++ip) {
+        const uint32_t* xr = Xs + tg[1 + 2 * ip];
+        const uint32_t* wr = Wb + tg[2 + 2 * ip];
 #pragma unroll
         for (int i = 0; i < CNT; ++i) {
-          const uint32_t r = redc_lazy3(T[i], p, pinv);
-          z[i] = ip0 == 0 ? r : add_mod(z[i], r, p);
+          const uint32_t pe = row_slot<LOGC>(tv, i);  // == row_perm(round-0 element)
+          T[i] += (unsigned long long)xr[pe] * __ldg(&wr[pe]);
         }
       }
-      uint32_t* Zt = P.Zout ? P.Zout + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff : nullptr;
-      auto load_z = [&](int i, uint32_t e) -> uint32_t {
-        if (Zt) Zt[e] = z[i];
-        return z[i];
-      };
-      if constexpr (TWO_PASS) {
-        uint32_t* gout = P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
-        sub_ntt<LOGC, true, 1>(tv, work, 0u, 1u, Ti, p, load_z,
-                            [&](int, uint32_t e, uint32_t v) { gout[e] = v; });
-      } else {
-        uint32_t* rout = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
-        const uint32_t n = (uint32_t)P.n;
-        sub_ntt<LOGC, true, 1>(tv, work, 0u, 1u, Ti, p, load_z,
-                            [&](int, uint32_t e, uint32_t v) {
-                              if (e < n) rout[e] = v;
-                            });
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) {
+        const uint32_t r = redc_lazy3(T[i], p, pinv);
+        z[i] = ip0 == 0 ? r : add_mod(z[i], r, p);
       }
     }
+  };
+  auto out_ptr = [&](int ci, int g) -> uint32_t* {
+    const int cv = ci ? cv1 : cv0;
+    if constexpr (TWO_PASS) return P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
+    return P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
+  };
+  auto ztap_ptr = [&](int ci, int g) -> uint32_t* {
+    const int cv = ci ? cv1 : cv0;
+    return P.Zout ? P.Zout + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff : nullptr;
+  };
+  const uint32_t nlim = TWO_PASS ? C : (uint32_t)P.n;
+  // (processing two items at once with sub_ntt_multi<..., 2> shares twiddles and barriers
+  // but measured slower on B200 -- fewer resident CTAs -- so items run one at a time)
+  for (int it = 0; it < nitems; ++it) {
+    if (it > 0) __syncthreads();  // exchange buffer free
+    int ci0, g0;
+    item(it, ci0, g0);
+    uint32_t z[16];
+    pointwise(ci0, g0, z);
+    uint32_t* const zt = ztap_ptr(ci0, g0);
+    uint32_t* const op = out_ptr(ci0, g0);
+    sub_ntt<LOGC, true, 1>(
+        tv, work, 0u, 1u, Ti, p,
+        [&](int i, uint32_t e) -> uint32_t {
+          if (zt) zt[e] = z[i];
+          return z[i];
+        },
+        [&](int, uint32_t e, uint32_t val) {
+          if (e < nlim) op[e] = val;
+        });
   }
 }
 
