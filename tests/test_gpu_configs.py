@@ -81,3 +81,20 @@ def test_config_c5_roundtrip(oz):
         assert np.array_equal(xr[b], xs[i])
     err = np.max(np.abs(xr - x)) / np.max(np.abs(x))
     assert err <= 1e-15, err
+
+
+@pytest.mark.parametrize("n,B", [(20000, 3), (300000, 1)])
+def test_decomposition_sizes(oz, n, B):
+    """NTT decompositions not covered by c1-c5: m = 2^16 (R = 32) and the largest supported
+    m = 2^20 (C = 2^12, R = 2^8)."""
+    x = workloads.draw("normal", n, B, n)
+    plan = oz.Plan(n, B)
+    y, gt = plan.execute_taps(torch.from_numpy(x).cuda())
+    op = O.Plan(n)
+    for b in range(B):
+        yo, ot = op.execute(x[b], taps=True)
+        assert np.array_equal(y[b].cpu().numpy(), yo)
+        assert np.array_equal(gt["digits"][b].cpu().numpy(), ot["digits"])
+        for cv in range(4):
+            ng = int(ot["sched"][cv, 0])
+            assert np.array_equal(gt["crt"][b, cv, :ng].cpu().numpy(), ot["crt"][cv, :ng])
