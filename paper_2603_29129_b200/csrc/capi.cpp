@@ -304,9 +304,23 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
   ozfft_plan* mp = const_cast<ozfft_plan*>(pl);
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = pl->n;
-  // sub-batches of sb transforms; nslots staging slots (ring) in the io_in / io_out areas
+  // sub-batch schedule: small first/last sub-batches shorten the pipeline fill (first H2D)
+  // and drain (last D2H); the middle ones are large enough to keep the GPU busy.  Staging
+  // slots (a ring of nslots x sb transforms) live in the io_in / io_out areas.
   const int64_t sb = std::max<int64_t>(1, std::min<int64_t>(pl->chunk, (pl->batch + 3) / 4));
-  const int64_t nsub = (pl->batch + sb - 1) / sb;
+  std::vector<int64_t> sizes;
+  {
+    const bool ramp = pl->batch >= 2 * sb + 4 && sb > 2;
+    int64_t rem = pl->batch - (ramp ? 4 : 0);
+    if (ramp) { sizes.push_back(1); sizes.push_back(2); }
+    while (rem > 0) {
+      const int64_t take = std::min(sb, rem);
+      sizes.push_back(take);
+      rem -= take;
+    }
+    if (ramp) sizes.push_back(1);
+  }
+  const int64_t nsub = (int64_t)sizes.size();
   const int64_t nslots = std::max<int64_t>(1, std::min<int64_t>(4, pl->chunk / sb));
   if (!mp->pipe) {
     mp->pipe = new HostPipe();
@@ -331,8 +345,9 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
   cudaStreamWaitEvent(h2d, ev(3 * nsub), 0);
   double* din0 = reinterpret_cast<double*>(pl->ws + pl->woff.io_in);
   double* dout0 = reinterpret_cast<double*>(pl->ws + pl->woff.io_out);
-  for (int64_t j = 0; j < nsub; ++j) {
-    const int64_t b0 = j * sb, nb = std::min<int64_t>(sb, pl->batch - b0);
+  int64_t b0 = 0;
+  for (int64_t j = 0; j < nsub; b0 += sizes[j], ++j) {
+    const int64_t nb = sizes[j];
     const size_t bytes = (size_t)nb * n * 16;
     double* din = din0 + 2 * (j % nslots) * sb * n;
     double* dout = dout0 + 2 * (j % nslots) * sb * n;
