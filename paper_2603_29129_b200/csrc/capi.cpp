@@ -185,11 +185,13 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     delete pl;
     return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "this build supports m <= 2^20 (n <= 2^19)");
   }
-  // NTT decomposition: one pass up to m = 2^12, else rows of C = 2^11 (2^12 at m = 2^20)
+  // NTT decomposition: one pass up to m = 2^12, else rows of C = 2^11 (2^12 at m = 2^20) and
+  // columns of R = m / C <= 2^8.  (One-warp rows of C = 2^10 with 32 elements per thread,
+  // OZFFT_TUNE_LOGC=10, measured slower on B200: 122 vs 147 GFLOP/s at c3.)
   pl->logC = logm <= 12 ? logm : std::max(11, logm - 8);
   if (const char* t = std::getenv("OZFFT_TUNE_LOGC")) {  // tuning knob (tools/, not the hot path)
     const int v = std::atoi(t);
-    if (v >= 11 && v <= 12 && logm > v && logm - v <= 8) pl->logC = v;
+    if ((v == 10 || v == 11) && logm > 12 && logm - v <= 10) pl->logC = v;
   }
   pl->logR = logm - pl->logC;
   pl->alpha = compute_alpha(desc.n, desc.L, p0, p1);

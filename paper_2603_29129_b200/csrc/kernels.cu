@@ -301,8 +301,9 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
 // A group of 2^S registers x[k] holding global positions gbase + k*gstep, with
 // rmod = gbase mod gstep.  DIF stages h = gstep*2^(S-1) .. gstep (block length 2h):
 //   (u, v) -> (u + v, (u - v) * T[h + (pos mod h)]),  T[h + j] = w_{2h}^j.
-template <int S, int NV>
-__device__ __forceinline__ void dif_group(uint32_t (&x)[NV][16], int off, uint32_t rmod,
+// x is [NV][E] (E = elements per thread); the group occupies x[v][off .. off + 2^S).
+template <int S, int NV, int E>
+__device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_t rmod,
                                           uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
 #pragma unroll
   for (int st = S - 1; st >= 0; --st) {
@@ -322,8 +323,8 @@ __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][16], int off, uint32
   }
 }
 // DIT stages h = gstep .. gstep*2^(S-1): v' = v * Tinv[h + (pos mod h)]; (u + v', u - v')
-template <int S, int NV>
-__device__ __forceinline__ void dit_group(uint32_t (&x)[NV][16], int off, uint32_t rmod,
+template <int S, int NV, int E>
+__device__ __forceinline__ void dit_group(uint32_t (&x)[NV][E], int off, uint32_t rmod,
                                           uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
 #pragma unroll
   for (int st = 0; st < S; ++st) {
@@ -351,105 +352,114 @@ __device__ __forceinline__ void dit_group(uint32_t (&x)[NV][16], int off, uint32
   }
 }
 
-__device__ __forceinline__ uint32_t pad_idx(uint32_t e) { return e + (e >> 4); }
+// Padded shared-memory index: one word of padding per 2^LOGE words.
+template <int LOGE>
+__device__ __forceinline__ uint32_t pad_idx(uint32_t e) { return e + (e >> LOGE); }
 
-// Round structure of a length-2^LOGN sub-transform, fixed at compile time.  DIF rounds
-// run from the top (block length 2^lb, lb = LOGN, LOGN-4, ...), 4 radix-2 stages each
-// except a last partial round; DIT runs the same rounds in reverse order.
-template <int LOGN, bool INV, int R>
+// Round structure of a length-2^LOGN sub-transform with 2^LOGE elements per thread, fixed at
+// compile time.  Rounds have LOGE radix-2 stages except a partial round that comes first
+// in DIF order (block length 2^LOGN) / last in DIT order, so that the step-1 round always
+// has 2^LOGE-element groups (conflict-free padded smem).
+template <int LOGN, bool INV, int R, int LOGE = 4>
 struct RoundT {
-  static constexpr int nr = (LOGN + 3) / 4;
+  static constexpr int E = 1 << LOGE;
+  static constexpr int nr = (LOGN + LOGE - 1) / LOGE;
   static constexpr int rd = INV ? (nr - 1 - R) : R;  // index in DIF order
-  // the partial round (LOGN mod 4 stages) comes first in DIF order / last in DIT order,
-  // so that the step-1 round always has 16-element groups (conflict-free padded smem)
-  static constexpr int S = rd == 0 ? LOGN - 4 * (nr - 1) : 4;  // stages in the round
-  static constexpr int lb = rd == 0 ? LOGN : 4 * (nr - rd);      // log2 block length
+  static constexpr int S = rd == 0 ? LOGN - LOGE * (nr - 1) : LOGE;  // stages in the round
+  static constexpr int lb = rd == 0 ? LOGN : LOGE * (nr - rd);       // log2 block length
   static constexpr int logstep = lb - S;
-  static constexpr int cnt = LOGN >= 4 ? 16 : (1 << LOGN);  // elements per thread
-  static constexpr int Tv = LOGN >= 4 ? (1 << (LOGN - 4)) : 1;
+  static constexpr int cnt = LOGN >= LOGE ? E : (1 << LOGN);  // elements per thread
+  static constexpr int Tv = LOGN >= LOGE ? (1 << (LOGN - LOGE)) : 1;
 };
 
 // Element index of register i of thread tv in round R.
-template <int LOGN, bool INV, int R>
+template <int LOGN, bool INV, int R, int LOGE = 4>
 __device__ __forceinline__ uint32_t round_elem(int tv, int i) {
-  using RT = RoundT<LOGN, INV, R>;
+  using RT = RoundT<LOGN, INV, R, LOGE>;
   const uint32_t g = (uint32_t)(tv + (i >> RT::S) * RT::Tv);
   const uint32_t k = (uint32_t)(i & ((1 << RT::S) - 1));
   return ((g >> RT::logstep) << RT::lb) + (g & ((1u << RT::logstep) - 1)) + (k << RT::logstep);
 }
 
-// Shared-memory slot of register i in round R: pad_idx(base_g) + koff(k), where base_g is
-// the group's first element and koff(k) = k*step + (k*step >> 4) is a compile-time
-// constant (valid because every block has length >= 16 when a round touches smem), so
-// the per-element address is a base register plus an immediate offset.
-template <int LOGN, bool INV, int R, int CB>
+// Shared-memory slot of register i in round R: pad(base_g) + koff(k), where base_g is the
+// group's first element and koff(k) = k*step + (k*step >> LOGE) is a compile-time constant
+// (valid because every block has length >= 2^LOGE when a round touches smem), so the
+// per-element address is a base register plus an immediate offset.
+template <int LOGN, bool INV, int R, int CB, int LOGE = 4>
 __device__ __forceinline__ uint32_t* round_slot(uint32_t* sm, int tv, int i) {
-  using RT = RoundT<LOGN, INV, R>;
+  using RT = RoundT<LOGN, INV, R, LOGE>;
   const uint32_t g = (uint32_t)(tv + (i >> RT::S) * RT::Tv);
   const uint32_t k = (uint32_t)(i & ((1 << RT::S) - 1));
   const uint32_t base = ((g >> RT::logstep) << RT::lb) + (g & ((1u << RT::logstep) - 1));
   const uint32_t ks = k << RT::logstep;
-  return sm + (pad_idx(base) + ks + (ks >> 4)) * CB;
+  return sm + (pad_idx<LOGE>(base) + ks + (ks >> LOGE)) * CB;
 }
 
-template <int LOGN, bool INV, int R, int CB, int NV, class LoadF, class StoreF>
-__device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][16], int tv,
+template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int tv,
                                               uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                               LoadF& load_first, StoreF& store_last) {
-  using RT = RoundT<LOGN, INV, R>;
+  using RT = RoundT<LOGN, INV, R, LOGE>;
+  constexpr int E = 1 << LOGE;
   constexpr uint32_t step = 1u << RT::logstep;
 #pragma unroll
   for (int v = 0; v < NV; ++v)
 #pragma unroll
     for (int i = 0; i < RT::cnt; ++i) {
       if constexpr (R == 0)
-        x[v][i] = load_first(v, i, round_elem<LOGN, INV, R>(tv, i));
+        x[v][i] = load_first(v, i, round_elem<LOGN, INV, R, LOGE>(tv, i));
       else
-        x[v][i] = *round_slot<LOGN, INV, R, CB>(sm[v], tv, i);
+        x[v][i] = *round_slot<LOGN, INV, R, CB, LOGE>(sm[v], tv, i);
     }
 #pragma unroll
   for (int u = 0; u < (RT::cnt >> RT::S); ++u) {
     const uint32_t g = (uint32_t)(tv + u * RT::Tv);
     const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
     if constexpr (INV)
-      dit_group<RT::S, NV>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+      dit_group<RT::S, NV, E>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     else
-      dif_group<RT::S, NV>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+      dif_group<RT::S, NV, E>(x, u * (1 << RT::S), rmod, step * gs, T, p);
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v)
 #pragma unroll
     for (int i = 0; i < RT::cnt; ++i) {
       if constexpr (R == RT::nr - 1)
-        store_last(v, i, round_elem<LOGN, INV, R>(tv, i), x[v][i]);
+        store_last(v, i, round_elem<LOGN, INV, R, LOGE>(tv, i), x[v][i]);
       else
-        *round_slot<LOGN, INV, R, CB>(sm[v], tv, i) = x[v][i];
+        *round_slot<LOGN, INV, R, CB, LOGE>(sm[v], tv, i) = x[v][i];
     }
-  if constexpr (R != RT::nr - 1) __syncthreads();
+  if constexpr (R != RT::nr - 1) {
+    if constexpr (RT::Tv * CB <= 32)
+      __syncwarp();  // the whole sub-transform lives in one warp
+    else
+      __syncthreads();
+  }
 }
 
-template <int LOGN, bool INV, int R, int CB, int NV, class LoadF, class StoreF>
-__device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][16], int tv,
+template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int tv,
                                                uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                                uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                                LoadF& load_first, StoreF& store_last) {
-  if constexpr (R < RoundT<LOGN, INV, 0>::nr) {
-    sub_ntt_round<LOGN, INV, R, CB, NV>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
-    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
+  if constexpr (R < RoundT<LOGN, INV, 0, LOGE>::nr) {
+    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE>(x, tv, sm, gb_mod, gs, T, p, load_first,
+                                                   store_last);
   }
 }
 
 // Length-2^LOGN sub-transforms of NV vectors at the same positions, executed cooperatively
-// by 2^max(LOGN-4,0) threads (index tv), 16 elements per thread and vector per round (N >=
-// 16) in rounds of <= 4 radix-2 stages; twiddles are loaded once for the NV vectors, and
+// by 2^max(LOGN-LOGE,0) threads (index tv), 2^LOGE elements per thread and vector per round
+// in rounds of <= LOGE radix-2 stages; twiddles are loaded once for the NV vectors, and
 // shared memory (padded, interleave CB) is used between rounds (one buffer per vector).
 //   INV = false: DIF stages len = N .. 2;   INV = true: DIT stages len = 2 .. N.
 // Element e has global position gbase_vec + e*gs; gb_mod = gbase_vec mod (gs*step) for
 // every step used (0 for rows, the column index for columns).  load_first(v, i, e) gives
 // the round-0 input of register i / element e of vector v; store_last(v, i, e, val)
 // consumes the final values.  The buffers must be free for writes on entry.
-template <int LOGN, bool INV, int CB, int NV, class LoadF, class StoreF>
+template <int LOGN, bool INV, int CB, int NV, int LOGE = 4, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                               LoadF&& load_first, StoreF&& store_last) {
@@ -458,18 +468,19 @@ __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV],
 #pragma unroll
       for (int v = 0; v < NV; ++v) store_last(v, 0, 0u, load_first(v, 0, 0u));
   } else {
-    uint32_t x[NV][16];
-    sub_ntt_rounds<LOGN, INV, 0, CB, NV>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
+    uint32_t x[NV][1 << LOGE];
+    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE>(x, tv, sm, gb_mod, gs, T, p, load_first,
+                                               store_last);
   }
 }
 
 // Single-vector form: load_first(i, e), store_last(i, e, val).
-template <int LOGN, bool INV, int CB, class LoadF, class StoreF>
+template <int LOGN, bool INV, int CB, int LOGE = 4, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, uint32_t gb_mod,
                                         uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                         LoadF&& load_first, StoreF&& store_last) {
   uint32_t* const sms[1] = {sm};
-  sub_ntt_multi<LOGN, INV, CB, 1>(
+  sub_ntt_multi<LOGN, INV, CB, 1, LOGE>(
       tv, sms, gb_mod, gs, T, p, [&](int, int i, uint32_t e) { return load_first(i, e); },
       [&](int, int i, uint32_t e, uint32_t v) { store_last(i, e, v); });
 }
@@ -498,26 +509,45 @@ struct ColParams {
   uint32_t unit_mask;
 };
 
-// Column tile geometry: R x Cb columns with R*Cb/16 = 256 threads (Cb >= 8 so that each
+// Elements per thread per round (log2) of the row and column sub-transforms: 32 for the
+// one-warp rows of C = 2^10 (two-pass plans) and for columns of R >= 2^9, else 16.
+__host__ __device__ constexpr int row_loge(int logC, bool two_pass) {
+  return two_pass && logC == 10 ? 5 : 4;
+}
+#ifndef OZ_COL_E32_MIN_LOGR
+#define OZ_COL_E32_MIN_LOGR 9
+#endif
+__host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32_MIN_LOGR ? 5 : 4; }
+
+template <int LOGR>
+struct ColCfg {
+  static constexpr int min_blocks_fwd = col_loge(LOGR) == 5 ? 1 : 5;
+};
+
+// Column tile geometry: R x Cb columns with (R / E) * Cb = 256 threads (Cb >= 8 so that each
 // row segment is at least one 32-byte sector).
 __host__ __device__ constexpr int col_log_cb(int logR, int logC) {
-  return (logR >= 4 ? (12 - logR < 3 ? 3 : 12 - logR) : 8) > logC
+  return (logR >= col_loge(logR) ? (8 - (logR - col_loge(logR)) < 3 ? 3 : 8 - (logR - col_loge(logR)))
+                                 : 8) > logC
              ? logC
-             : (logR >= 4 ? (12 - logR < 3 ? 3 : 12 - logR) : 8);
+             : (logR >= col_loge(logR) ? (8 - (logR - col_loge(logR)) < 3 ? 3 : 8 - (logR - col_loge(logR)))
+                                       : 8);
 }
 
 // Forward column pass: global DIF stages len = m .. 2C on columns of the R x C view.
 // One CTA per (transform, prime, part, column block) loops over the part's slices; the
 // next slice's column tile is loaded while the current one is transformed.
 template <int LOGR, int LOGC>
-__global__ void __launch_bounds__(256, 5) k_col_fwd(ColParams P) {
+__global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(ColParams P) {
   extern __shared__ uint32_t smem[];
   constexpr int LOGCB = col_log_cb(LOGR, LOGC);
+  constexpr int LOGE = col_loge(LOGR);
+  constexpr int E = 1 << LOGE;
   constexpr int Cb = 1 << LOGCB;
   constexpr uint32_t C = 1u << LOGC;
   constexpr uint32_t m = 1u << (LOGR + LOGC);
   constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
-  constexpr int CNT = RoundT<LOGR, false, 0>::cnt;
+  constexpr int CNT = RoundT<LOGR, false, 0, LOGE>::cnt;
   const uint32_t cb = blockIdx.x % ncb;
   uint32_t v = blockIdx.x / ncb;  // (b * 2 + q) * 2 + a
   const int a = (int)(v & 1); v >>= 1;
@@ -535,24 +565,24 @@ __global__ void __launch_bounds__(256, 5) k_col_fwd(ColParams P) {
   const uint32_t col = (cb << LOGCB) + c;
   const uint2* T = P.tw + (size_t)(q * 2 + 0) * m;
   const uint32_t lim = P.in_len > col ? (uint32_t)(P.in_len - col) : 0u;  // e*C < lim <=> i < in_len
-  uint32_t nxt[16];
+  uint32_t nxt[E];
   auto fetch = [&](int s) {
     const int32_t* D = P.digits + ((b * 2 + a) * P.K + s) * P.in_len + col;
 #pragma unroll
     for (int i = 0; i < CNT; ++i) {
-      const uint32_t e = round_elem<LOGR, false, 0>(tv, i);
+      const uint32_t e = round_elem<LOGR, false, 0, LOGE>(tv, i);
       nxt[i] = e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u;
     }
   };
   fetch(0);
   for (int s = 0; s < ka; ++s) {
-    uint32_t cur[16];
+    uint32_t cur[E];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+    for (int i = 0; i < E; ++i) cur[i] = nxt[i];
     if (s + 1 < ka) fetch(s + 1);
     if (s > 0) __syncthreads();  // smem tile free
     uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (int64_t)m + col;
-    sub_ntt<LOGR, false, Cb>(
+    sub_ntt<LOGR, false, Cb, LOGE>(
         tv, smem + c, col, C, T, p, [&](int i, uint32_t) -> uint32_t { return cur[i]; },
         [&](int, uint32_t e, uint32_t val) { out[e * C] = val; });
   }
@@ -565,11 +595,13 @@ template <int LOGR, int LOGC>
 __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   extern __shared__ uint32_t smem[];
   constexpr int LOGCB = col_log_cb(LOGR, LOGC);
+  constexpr int LOGE = col_loge(LOGR);
+  constexpr int E = 1 << LOGE;
   constexpr int Cb = 1 << LOGCB;
   constexpr uint32_t C = 1u << LOGC;
   constexpr uint32_t m = 1u << (LOGR + LOGC);
   constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
-  constexpr int CNT = RoundT<LOGR, true, 0>::cnt;
+  constexpr int CNT = RoundT<LOGR, true, 0, LOGE>::cnt;
   const int G = P.K * P.K;
   const uint32_t cb = blockIdx.x % ncb;
   uint32_t v = blockIdx.x / ncb;  // (b * 2 + q) * 4 + cv
@@ -585,21 +617,21 @@ __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
   const uint32_t col = (cb << LOGCB) + c;
   const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
   const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
-  uint32_t nxt[16];
+  uint32_t nxt[E];
   auto fetch = [&](int g) {
     const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * (int64_t)m + col;
 #pragma unroll
-    for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0>(tv, i) * C]);
+    for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0, LOGE>(tv, i) * C]);
   };
   fetch(0);
   for (int g = 0; g < ng; ++g) {
-    uint32_t cur[16];
+    uint32_t cur[E];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+    for (int i = 0; i < E; ++i) cur[i] = nxt[i];
     if (g + 1 < ng) fetch(g + 1);
     if (g > 0) __syncthreads();  // smem tile free
     uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
-    sub_ntt<LOGR, true, Cb>(
+    sub_ntt<LOGR, true, Cb, LOGE>(
         tv, smem + c, col, C, T, p, [&](int i, uint32_t) -> uint32_t { return cur[i]; },
         [&](int, uint32_t e, uint32_t val) {
           if (e * C < lim) out[e * C] = val;
@@ -630,15 +662,17 @@ struct RowParams {
   uint32_t* Zout;         // tap: [nb][2 q][4][K*K][m] (internal order, W m^{-1} scaled)
 };
 
-template <int LOGC>
+template <int LOGC, bool TWO_PASS>
 struct RowCfg {
-  static constexpr int threads = LOGC >= 4 ? (1 << (LOGC - 4)) : 1;
+  static constexpr int LOGE = row_loge(LOGC, TWO_PASS);
+  static constexpr int E = 1 << LOGE;
+  static constexpr int threads = LOGC >= LOGE ? (1 << (LOGC - LOGE)) : 1;
 #ifndef OZ_ROW_MINB
 #define OZ_ROW_MINB 5
 #endif
-  static constexpr int min_blocks = LOGC == 11 ? OZ_ROW_MINB : 1;
+  static constexpr int min_blocks = LOGC == 11 ? OZ_ROW_MINB : (LOGC == 10 && TWO_PASS ? 12 : 1);
   // stages of the first DIT round (= last DIF round): its groups are contiguous blocks
-  static constexpr int S0 = LOGC >= 4 ? 4 : LOGC;
+  static constexpr int S0 = LOGC >= LOGE ? LOGE : LOGC;
 };
 
 // Row-local storage order used for the X rows in shared memory and for the cached W
@@ -651,15 +685,15 @@ __host__ __device__ __forceinline__ uint32_t row_perm(uint32_t e, int logC, int 
 
 // row_perm of the element held in register i by thread tv in the first DIT round (element
 // g*2^S0 + k, g = tv + u*Tv, i = u*2^S0 + k): tv + compile-time offset.
-template <int LOGC>
+template <int LOGC, bool TWO_PASS>
 __device__ __forceinline__ uint32_t row_slot(int tv, int i) {
-  constexpr int S0 = RowCfg<LOGC>::S0;
-  constexpr int Tv = RowCfg<LOGC>::threads;
+  constexpr int S0 = RowCfg<LOGC, TWO_PASS>::S0;
+  constexpr int Tv = RowCfg<LOGC, TWO_PASS>::threads;
   return (uint32_t)tv + ((uint32_t)(i & ((1 << S0) - 1)) << (LOGC - S0)) + (uint32_t)(i >> S0) * Tv;
 }
 
 template <int LOGC, bool TWO_PASS>
-__global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_blocks)
+__global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, TWO_PASS>::min_blocks)
     k_row_fused(RowParams P) {
   extern __shared__ uint32_t smem[];
   __shared__ int s_ng[2];
@@ -669,7 +703,9 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
   const uint32_t row = blockIdx.y >> 2;
   constexpr int logC = LOGC;
   constexpr uint32_t C = 1u << logC;
-  constexpr uint32_t padC = C + (C >> 4) + 1;
+  constexpr int LOGE = RowCfg<LOGC, TWO_PASS>::LOGE;
+  constexpr int E = 1 << LOGE;
+  constexpr uint32_t padC = C + (C >> LOGE) + 1;
   const int tv = threadIdx.x;
   const int64_t m = 1ll << P.logm;
   const uint32_t p = q ? P.p[1] : P.p[0];
@@ -712,17 +748,17 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
     uint32_t* outX = P.Xout ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff : nullptr;
     __syncthreads();  // `work` is free (previous sub-transform's last reads are done)
     auto store_x = [&](int i, uint32_t e, uint32_t v) {
-      xs[row_slot<LOGC>(tv, i)] = v;  // == row_perm(e)
+      xs[row_slot<LOGC, TWO_PASS>(tv, i)] = v;  // == row_perm(e)
       if (outX) outX[e] = v;
     };
     if constexpr (TWO_PASS) {
       const uint32_t* y = P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff;
-      sub_ntt<LOGC, false, 1>(tv, work, 0u, 1u, Tf, p,
+      sub_ntt<LOGC, false, 1, LOGE>(tv, work, 0u, 1u, Tf, p,
                            [&](int, uint32_t e) -> uint32_t { return __ldg(&y[e]); }, store_x);
     } else {
       const int32_t* D = P.digits + ((b * 2 + a) * K + s) * P.in_len;
       const uint32_t in_len = (uint32_t)P.in_len;
-      sub_ntt<LOGC, false, 1>(
+      sub_ntt<LOGC, false, 1, LOGE>(
           tv, work, 0u, 1u, Tf, p,
           [&](int, uint32_t e) -> uint32_t { return e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
           store_x);
@@ -732,7 +768,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
   // ---- per group: Z = sum X_s (.) W_t (Alg.8 l.981-982), then the first log2(C) DIT
   // stages of its inverse NTT (l.973).  The (conv, group) items of both convolutions are
   // processed two at a time: their twiddles are shared and one barrier serves both.
-  constexpr int CNT = RoundT<LOGC, true, 0>::cnt;
+  constexpr int CNT = RoundT<LOGC, true, 0, LOGE>::cnt;
   const uint32_t pinv = q ? P.pinv[1] : P.pinv[0];
   __syncthreads();  // group table visible
   const int ng0 = s_ng[0], nitems = s_ng[0] + s_ng[1];
@@ -742,24 +778,24 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
   };
   // pointwise products for this thread's round-0 elements: 64-bit lazy sums of up to 3
   // products X * W~ (W~ = W m^{-1} 2^32, sums < 3 p^2 < 2^64), one Montgomery reduction each
-  auto pointwise = [&](int ci, int g, uint32_t (&z)[16]) {
+  auto pointwise = [&](int ci, int g, uint32_t (&z)[E]) {
     const int cv = ci ? cv1 : cv0;
     const uint32_t* Wb = P.W + (size_t)(q * 2 + conv_b(cv)) * K * m + rowoff;
     const uint32_t* tg = tab + (ci * G + g) * tstride;
     const int np = (int)tg[0];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) z[i] = 0;
+    for (int i = 0; i < E; ++i) z[i] = 0;
     for (int ip0 = 0; ip0 < np; ip0 += 3) {
-      unsigned long long T[16];
+      unsigned long long T[E];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) T[i] = 0ull;
+      for (int i = 0; i < E; ++i) T[i] = 0ull;
       const int ipe = min(np, ip0 + 3);
       for (int ip = ip0; ip < ipe; ++ip) {
         const uint32_t* xr = Xs + tg[1 + 2 * ip];
         const uint32_t* wr = Wb + tg[2 + 2 * ip];
 #pragma unroll
         for (int i = 0; i < CNT; ++i) {
-          const uint32_t pe = row_slot<LOGC>(tv, i);  // == row_perm(round-0 element)
+          const uint32_t pe = row_slot<LOGC, TWO_PASS>(tv, i);  // == row_perm(round-0 element)
           T[i] += (unsigned long long)xr[pe] * __ldg(&wr[pe]);
         }
       }
@@ -786,11 +822,11 @@ __global__ void __launch_bounds__(RowCfg<LOGC>::threads, RowCfg<LOGC>::min_block
     if (it > 0) __syncthreads();  // exchange buffer free
     int ci0, g0;
     item(it, ci0, g0);
-    uint32_t z[16];
+    uint32_t z[E];
     pointwise(ci0, g0, z);
     uint32_t* const zt = ztap_ptr(ci0, g0);
     uint32_t* const op = out_ptr(ci0, g0);
-    sub_ntt<LOGC, true, 1>(
+    sub_ntt<LOGC, true, 1, LOGE>(
         tv, work, 0u, 1u, Ti, p,
         [&](int i, uint32_t e) -> uint32_t {
           if (zt) zt[e] = z[i];
@@ -931,19 +967,21 @@ template <int LOGR, int LOGC>
 __global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
   extern __shared__ uint32_t smem[];
   constexpr int LOGCB = col_log_cb(LOGR, LOGC);
+  constexpr int LOGE = col_loge(LOGR);
+  constexpr int E = 1 << LOGE;
   constexpr int Cb = 1 << LOGCB;
   constexpr uint32_t C = 1u << LOGC;
   constexpr uint32_t m = 1u << (LOGR + LOGC);
   constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
-  constexpr int CNT = RoundT<LOGR, true, 0>::cnt;
-  constexpr int NR = RoundT<LOGR, true, 0>::nr;
+  constexpr int CNT = RoundT<LOGR, true, 0, LOGE>::cnt;
+  constexpr int NR = RoundT<LOGR, true, 0, LOGE>::nr;
   // last DIT round: registers i with (i mod 2^S) < 2^(S-1) hold rows < R/2 (the only rows
   // needed, n <= m/2); they are packed into NH slots by hslot(i)
-  constexpr int SL = RoundT<LOGR, true, NR - 1>::S;
-  constexpr int NH = RoundT<LOGR, true, NR - 1>::cnt / 2;
+  constexpr int SL = RoundT<LOGR, true, NR - 1, LOGE>::S;
+  constexpr int NH = RoundT<LOGR, true, NR - 1, LOGE>::cnt / 2;
   auto needed = [](int i) { return (i & ((1 << SL) - 1)) < (1 << (SL - 1)); };
   auto hslot = [](int i) { return ((i >> SL) << (SL - 1)) + (i & ((1 << (SL - 1)) - 1)); };
-  constexpr int THREADS = RoundT<LOGR, true, 0>::Tv << LOGCB;
+  constexpr int THREADS = RoundT<LOGR, true, 0, LOGE>::Tv << LOGCB;
   const int G = P.K * P.K;
   const uint32_t cb = blockIdx.x % ncb;
   uint32_t v = blockIdx.x / ncb;  // b * 4 + cv
@@ -957,32 +995,32 @@ __global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
   const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(P.K, P.L);
   const int ng = srow[0];
   for (int g = tid; g < ng; g += blockDim.x) s_sc[g] = scalbn(1.0, -srow[1 + g * (2 + 2 * P.L)]);
-  constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / 16 + 1) * Cb;
+  constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;
   double2* Sacc = reinterpret_cast<double2*>(smem + TILE + (TILE & 1));  // [NH][THREADS]
 #pragma unroll
   for (int i = 0; i < NH; ++i) Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
   const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
-  uint32_t nxt[16];
+  uint32_t nxt[E];
   auto fetch = [&](int t) {  // tile t = 2 g + q
     const int g = t >> 1, q = t & 1;
     const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * (int64_t)m + col;
 #pragma unroll
-    for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0>(tv, i) * C]);
+    for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0, LOGE>(tv, i) * C]);
   };
   if (ng > 0) fetch(0);
   __syncthreads();  // s_sc ready
   uint32_t r0[NH];
   for (int t = 0; t < 2 * ng; ++t) {
     const int g = t >> 1, q = t & 1;
-    uint32_t cur[16];
+    uint32_t cur[E];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+    for (int i = 0; i < E; ++i) cur[i] = nxt[i];
     if (t + 1 < 2 * ng) fetch(t + 1);
     if (t > 0) __syncthreads();  // smem tile free
     const uint32_t p = q ? P.F.p1 : P.F.p0;
     const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
     uint32_t rr[NH];
-    sub_ntt<LOGR, true, Cb>(tv, smem + c, col, C, T, p,
+    sub_ntt<LOGR, true, Cb, LOGE>(tv, smem + c, col, C, T, p,
                             [&](int i, uint32_t) -> uint32_t { return cur[i]; },
                             [&](int i, uint32_t, uint32_t val) {
                               if (needed(i)) rr[hslot(i)] = val;  // rows >= R/2 never needed
@@ -992,7 +1030,7 @@ __global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
 #pragma unroll
       for (int i = 0; i < 2 * NH; ++i) {
         if (!needed(i)) continue;
-        const uint32_t e = round_elem<LOGR, true, NR - 1>(tv, i);
+        const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
         if (e * C < lim) rt[e * C] = rr[hslot(i)];
       }
     }
@@ -1004,7 +1042,7 @@ __global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
 #pragma unroll
       for (int i = 0; i < 2 * NH; ++i) {
         if (!needed(i)) continue;
-        const uint32_t e = round_elem<LOGR, true, NR - 1>(tv, i);
+        const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
         const int h = hslot(i);
         if (e * C < lim) {
           const long long Z = garner2(r0[h], rr[h], P.F);  // l.974
@@ -1022,7 +1060,7 @@ __global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
 #pragma unroll
   for (int i = 0; i < 2 * NH; ++i) {
     if (!needed(i)) continue;
-    const uint32_t e = round_elem<LOGR, true, NR - 1>(tv, i);
+    const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
     if (e * C < lim) So[e * C] = Sacc[hslot(i) * THREADS + tid];
   }
 }
@@ -1129,13 +1167,13 @@ static ozfft_status cuda_check(const char* what) {
 static int col_logCb(int logR, int logC) { return col_log_cb(logR, logC); }
 static size_t col_smem(int logR, int logCb) {
   const size_t R = 1ull << logR;
-  return (R + (R >> 4) + 1) * (1ull << logCb) * sizeof(uint32_t);
+  return (R + (R >> col_loge(logR)) + 1) * (1ull << logCb) * sizeof(uint32_t);
 }
 static int col_threads(int logR, int logCb) {
-  const int Tv = logR >= 4 ? (1 << (logR - 4)) : 1;
+  const int le = col_loge(logR);
+  const int Tv = logR >= le ? (1 << (logR - le)) : 1;
   return Tv << logCb;
 }
-
 static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cudaStream_t st) {
   const int threads = 256;
   int64_t blocks_per = (SP.len + threads * 4 - 1) / (threads * 4);
@@ -1165,9 +1203,10 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   c.col_smem = col_smem(pl.logR, c.logCb);
   c.col_threads = col_threads(pl.logR, c.logCb);
   const size_t C = 1ull << pl.logC;
-  const size_t padC = C + (C >> 4) + 1;
+  const int rle = row_loge(pl.logC, pl.logR > 0);
+  const size_t padC = C + (C >> rle) + 1;
   c.row_smem = ((size_t)pl.K * C + padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
-  c.row_threads = pl.logC >= 4 ? (1 << (pl.logC - 4)) : 1;  // exactly Tv: every thread active
+  c.row_threads = pl.logC >= rle ? (1 << (pl.logC - rle)) : 1;  // exactly Tv: every thread active
   return c;
 }
 
@@ -1191,7 +1230,7 @@ static void set_smem(K kern, size_t bytes) {
 template <int LOGR>
 static void launch_col_fwd_r(int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
                              const ColParams& CP) {
-  dispatch_log<11, 12>(logC, [&](auto J) {
+  dispatch_log<10, 12>(logC, [&](auto J) {
     set_smem(k_col_fwd<LOGR, J.value>, c.col_smem);
     k_col_fwd<LOGR, J.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
   });
@@ -1199,23 +1238,23 @@ static void launch_col_fwd_r(int logC, unsigned nblk, const NttLaunch& c, cudaSt
 template <int LOGR>
 static void launch_col_inv_r(int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
                              const ColParams& CP) {
-  dispatch_log<11, 12>(logC, [&](auto J) {
+  dispatch_log<10, 12>(logC, [&](auto J) {
     set_smem(k_col_inv<LOGR, J.value>, c.col_smem);
     k_col_inv<LOGR, J.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
   });
 }
 static void launch_col_fwd(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
                            const ColParams& CP) {
-  dispatch_log<1, 8>(logR, [&](auto I) { launch_col_fwd_r<I.value>(logC, nblk, c, st, CP); });
+  dispatch_log<1, 10>(logR, [&](auto I) { launch_col_fwd_r<I.value>(logC, nblk, c, st, CP); });
 }
 static void launch_col_inv(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
                            const ColParams& CP) {
-  dispatch_log<1, 8>(logR, [&](auto I) { launch_col_inv_r<I.value>(logC, nblk, c, st, CP); });
+  dispatch_log<1, 10>(logR, [&](auto I) { launch_col_inv_r<I.value>(logC, nblk, c, st, CP); });
 }
 static void launch_row(int logC, int logR, dim3 grid, const NttLaunch& c, cudaStream_t st,
                        const RowParams& RP) {
   if (logR > 0) {
-    dispatch_log<11, 12>(logC, [&](auto I) {
+    dispatch_log<10, 12>(logC, [&](auto I) {
       set_smem(k_row_fused<I.value, true>, c.row_smem);
       k_row_fused<I.value, true><<<grid, c.row_threads, c.row_smem, st>>>(RP);
     });
@@ -1226,7 +1265,10 @@ static void launch_row(int logC, int logR, dim3 grid, const NttLaunch& c, cudaSt
     });
   }
 }
-static int row_s0(int logC) { return logC >= 4 ? 4 : logC; }
+static int row_s0(int logC, bool two_pass) {
+  const int le = row_loge(logC, two_pass);
+  return logC >= le ? le : logC;
+}
 
 // Forward NTT of digit vectors [nb][2][K][in_len] into internal-order spectra Xout
 // [nb][2 q][2 a][K][m] (used at plan time for omega~*; the hot path fuses the row part).
@@ -1310,7 +1352,7 @@ ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
     cudaMemcpyAsync(pl.pers + pl.poff.wsplit, wsplit, sizeof(int32_t) * (2 + 2 * K),
                     cudaMemcpyHostToDevice, st);
     k_w_finalize<<<592, 256, 0, st>>>(X, reinterpret_cast<uint32_t*>(pl.pers + pl.poff.W), K, m,
-                                      pl.logC, row_s0(pl.logC), pl.p[0], pl.p[1], pl.minv[0],
+                                      pl.logC, row_s0(pl.logC, pl.logR > 0), pl.p[0], pl.p[1], pl.minv[0],
                                       pl.minv[1]);
     s = cuda_check("W finalize");
     if (!s && cudaStreamSynchronize(st) != cudaSuccess) s = cuda_check("plan precompute sync");
@@ -1407,13 +1449,14 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     XP.S = reinterpret_cast<double2*>(ws + pl.woff.S);
     XP.res_tap = taps && taps->res ? res : nullptr;
     XP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
-    const size_t tile = ((1ull << pl.logR) + (1ull << pl.logR) / 16 + 1) * (1ull << c.logCb);
-    const int nh = (pl.logR >= 4 ? 16 : (1 << pl.logR)) / 2;
+    const int cle = col_loge(pl.logR);
+    const size_t tile = ((1ull << pl.logR) + ((1ull << pl.logR) >> cle) + 1) * (1ull << c.logCb);
+    const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / 2;
     const size_t smem = (tile + (tile & 1)) * 4 + (size_t)nh * c.col_threads * 16;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
-    dispatch_log<1, 8>(pl.logR, [&](auto I) {
-      dispatch_log<11, 12>(pl.logC, [&](auto J) {
+    dispatch_log<1, 10>(pl.logR, [&](auto I) {
+      dispatch_log<10, 12>(pl.logC, [&](auto J) {
         set_smem(k_col_inv_crt<I.value, J.value>, smem);
         k_col_inv_crt<I.value, J.value><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
       });
@@ -1484,7 +1527,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
       if (mult) cudaMemcpyAsync(dvm, vm.data(), sizeof(uint32_t) * nvec, cudaMemcpyHostToDevice, st);
       k_tap_permute<<<1184, 256, 0, st>>>(src, reinterpret_cast<uint32_t*>(dst), nvec, pl.logm,
                                           doff, dvp, mult ? dvm : nullptr, rowperm ? pl.logC : -1,
-                                          row_s0(pl.logC));
+                                          row_s0(pl.logC, pl.logR > 0));
       cudaStreamSynchronize(st);
       cudaFree(doff);
       cudaFree(dvp);
