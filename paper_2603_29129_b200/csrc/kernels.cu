@@ -302,9 +302,15 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
 // rmod = gbase mod gstep.  DIF stages h = gstep*2^(S-1) .. gstep (block length 2h):
 //   (u, v) -> (u + v, (u - v) * T[h + (pos mod h)]),  T[h + j] = w_{2h}^j.
 // x is [NV][E] (E = elements per thread); the group occupies x[v][off .. off + 2^S).
-template <int S, int NV, int E>
+// UNIT: the caller guarantees rmod == 0 and gstep == 1 (the step-1 round of a row), so the
+// twiddle index is compile-time and the butterflies with T[h] = w^0 = 1 skip the product.
+template <int S, int NV, int E, bool UNIT = false>
 __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_t rmod,
                                           uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
+  if constexpr (UNIT) {
+    rmod = 0u;
+    gstep = 1u;
+  }
 #pragma unroll
   for (int st = S - 1; st >= 0; --st) {
     const int d = 1 << st;
@@ -312,6 +318,15 @@ __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_
 #pragma unroll
     for (int k = 0; k < (1 << S); ++k) {
       if (k & d) continue;
+      if (UNIT && (k & (d - 1)) == 0) {  // (u - v) * 1
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const uint32_t a = x[v][off + k], b = x[v][off + k + d];
+          x[v][off + k] = add_mod(a, b, p);
+          x[v][off + k + d] = sub_mod(a, b, p);
+        }
+        continue;
+      }
       const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);  // shared by NV
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
@@ -323,9 +338,13 @@ __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_
   }
 }
 // DIT stages h = gstep .. gstep*2^(S-1): v' = v * Tinv[h + (pos mod h)]; (u + v', u - v')
-template <int S, int NV, int E>
+template <int S, int NV, int E, bool UNIT = false>
 __device__ __forceinline__ void dit_group(uint32_t (&x)[NV][E], int off, uint32_t rmod,
                                           uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
+  if constexpr (UNIT) {
+    rmod = 0u;
+    gstep = 1u;
+  }
 #pragma unroll
   for (int st = 0; st < S; ++st) {
     const int d = 1 << st;
@@ -333,11 +352,13 @@ __device__ __forceinline__ void dit_group(uint32_t (&x)[NV][E], int off, uint32_
 #pragma unroll
     for (int k = 0; k < (1 << S); ++k) {
       if (k & d) continue;
-      const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);  // shared by NV
+      const bool one = UNIT && (k & (d - 1)) == 0;  // twiddle w^0 = 1
+      const uint2 w = one ? make_uint2(1u, 0u) : __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const uint32_t a = x[v][off + k];  // always canonical: it was a "u" of this stage
-        const uint32_t b = mul_shoup(x[v][off + k + d], w, p);  // input may be lazy (< 2p)
+        const uint32_t vin = x[v][off + k + d];  // may be lazy (< 2p)
+        const uint32_t b = one ? min(vin, vin - p) : mul_shoup(vin, w, p);
         if (st + 1 < S && (k & (2 * d))) {
           // both outputs are the "v" operand of the next stage, whose Shoup product
           // accepts any 32-bit input: keep them in [0, 2p), skip the subtractions
@@ -395,7 +416,22 @@ __device__ __forceinline__ uint32_t* round_slot(uint32_t* sm, int tv, int i) {
   return sm + (pad_idx<LOGE>(base) + ks + (ks >> LOGE)) * CB;
 }
 
-template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, class LoadF, class StoreF>
+// Is the exchange between rounds R and R + 1 confined to one warp?  With one group per
+// thread in both rounds, the values of a block of the coarser round (larger block length,
+// round R in DIF order, R + 1 in DIT order) are read and written only by the 2^logstep * CB
+// threads that own it in either round; if they fit in an aligned warp, __syncwarp suffices.
+template <int LOGN, bool INV, int R, int CB, int LOGE>
+struct RoundSync {
+  using A = RoundT<LOGN, INV, R, LOGE>;
+  using B = RoundT<LOGN, INV, R + 1, LOGE>;
+  static constexpr bool one_group = A::cnt == (1 << A::S) && B::cnt == (1 << B::S);
+  static constexpr int coarse_logstep = INV ? B::logstep : A::logstep;
+  static constexpr bool warp_local =
+      A::Tv * CB <= 32 || (one_group && (1 << coarse_logstep) * CB <= 32);
+};
+
+template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, class LoadF,
+          class StoreF>
 __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int tv,
                                               uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, uint32_t p,
@@ -416,10 +452,11 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
   for (int u = 0; u < (RT::cnt >> RT::S); ++u) {
     const uint32_t g = (uint32_t)(tv + u * RT::Tv);
     const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
+    constexpr bool unit = UNIT && RT::logstep == 0;  // rmod == gb_mod == 0, gstep == gs == 1
     if constexpr (INV)
-      dit_group<RT::S, NV, E>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+      dit_group<RT::S, NV, E, unit>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     else
-      dif_group<RT::S, NV, E>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+      dif_group<RT::S, NV, E, unit>(x, u * (1 << RT::S), rmod, step * gs, T, p);
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v)
@@ -431,21 +468,23 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
         *round_slot<LOGN, INV, R, CB, LOGE>(sm[v], tv, i) = x[v][i];
     }
   if constexpr (R != RT::nr - 1) {
-    if constexpr (RT::Tv * CB <= 32)
-      __syncwarp();  // the whole sub-transform lives in one warp
+    if constexpr (RoundSync<LOGN, INV, R, CB, LOGE>::warp_local)
+      __syncwarp();  // every value read in round R + 1 was written by the same warp
     else
       __syncthreads();
   }
 }
 
-template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, class LoadF, class StoreF>
+template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, class LoadF,
+          class StoreF>
 __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int tv,
                                                uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                                uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                                LoadF& load_first, StoreF& store_last) {
   if constexpr (R < RoundT<LOGN, INV, 0, LOGE>::nr) {
-    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE>(x, tv, sm, gb_mod, gs, T, p, load_first, store_last);
-    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE>(x, tv, sm, gb_mod, gs, T, p, load_first,
+    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE, UNIT>(x, tv, sm, gb_mod, gs, T, p, load_first,
+                                                    store_last);
+    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE, UNIT>(x, tv, sm, gb_mod, gs, T, p, load_first,
                                                    store_last);
   }
 }
@@ -458,8 +497,10 @@ __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int
 // Element e has global position gbase_vec + e*gs; gb_mod = gbase_vec mod (gs*step) for
 // every step used (0 for rows, the column index for columns).  load_first(v, i, e) gives
 // the round-0 input of register i / element e of vector v; store_last(v, i, e, val)
-// consumes the final values.  The buffers must be free for writes on entry.
-template <int LOGN, bool INV, int CB, int NV, int LOGE = 4, class LoadF, class StoreF>
+// consumes the final values.  The buffers must be free for writes on entry.  UNIT: the
+// caller passes gb_mod == 0 and gs == 1 (rows), enabling the compile-time step-1 round.
+template <int LOGN, bool INV, int CB, int NV, int LOGE = 4, bool UNIT = false, class LoadF,
+          class StoreF>
 __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                               LoadF&& load_first, StoreF&& store_last) {
@@ -469,18 +510,18 @@ __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV],
       for (int v = 0; v < NV; ++v) store_last(v, 0, 0u, load_first(v, 0, 0u));
   } else {
     uint32_t x[NV][1 << LOGE];
-    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE>(x, tv, sm, gb_mod, gs, T, p, load_first,
-                                               store_last);
+    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE, UNIT>(x, tv, sm, gb_mod, gs, T, p, load_first,
+                                                     store_last);
   }
 }
 
 // Single-vector form: load_first(i, e), store_last(i, e, val).
-template <int LOGN, bool INV, int CB, int LOGE = 4, class LoadF, class StoreF>
+template <int LOGN, bool INV, int CB, int LOGE = 4, bool UNIT = false, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, uint32_t gb_mod,
                                         uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                         LoadF&& load_first, StoreF&& store_last) {
   uint32_t* const sms[1] = {sm};
-  sub_ntt_multi<LOGN, INV, CB, 1, LOGE>(
+  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, UNIT>(
       tv, sms, gb_mod, gs, T, p, [&](int, int i, uint32_t e) { return load_first(i, e); },
       [&](int, int i, uint32_t e, uint32_t v) { store_last(i, e, v); });
 }
@@ -519,9 +560,16 @@ __host__ __device__ constexpr int row_loge(int logC, bool two_pass) {
 #endif
 __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32_MIN_LOGR ? 5 : 4; }
 
+#ifndef OZ_CI_MINB
+#define OZ_CI_MINB 3
+#endif
+#ifndef OZ_CF_MINB
+#define OZ_CF_MINB 5
+#endif
 template <int LOGR>
 struct ColCfg {
-  static constexpr int min_blocks_fwd = col_loge(LOGR) == 5 ? 1 : 5;
+  static constexpr int min_blocks_fwd = col_loge(LOGR) == 5 ? 1 : OZ_CF_MINB;
+  static constexpr int min_blocks_inv_crt = col_loge(LOGR) == 5 ? 1 : OZ_CI_MINB;
 };
 
 // Column tile geometry: R x Cb columns with (R / E) * Cb = 256 threads (Cb >= 8 so that each
@@ -662,13 +710,32 @@ struct RowParams {
   uint32_t* Zout;         // tap: [nb][2 q][4][K*K][m] (internal order, W m^{-1} scaled)
 };
 
+#ifndef OZ_ROW_DBUF
+#define OZ_ROW_DBUF 0
+#endif
+#ifndef OZ_ROW_QMAJOR
+#define OZ_ROW_QMAJOR 1
+#endif
+#ifndef OZ_ROW_NA
+#define OZ_ROW_NA 1
+#endif
+// streaming read-only load that does not allocate in L1 (keeps the twiddle tables there)
+__device__ __forceinline__ uint32_t ldg_stream(const uint32_t* p) {
+#if OZ_ROW_NA
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
 template <int LOGC, bool TWO_PASS>
 struct RowCfg {
   static constexpr int LOGE = row_loge(LOGC, TWO_PASS);
   static constexpr int E = 1 << LOGE;
   static constexpr int threads = LOGC >= LOGE ? (1 << (LOGC - LOGE)) : 1;
 #ifndef OZ_ROW_MINB
-#define OZ_ROW_MINB 5
+#define OZ_ROW_MINB 6
 #endif
   static constexpr int min_blocks = LOGC == 11 ? OZ_ROW_MINB : (LOGC == 10 && TWO_PASS ? 12 : 1);
   // stages of the first DIT round (= last DIF round): its groups are contiguous blocks
@@ -699,8 +766,15 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   __shared__ int s_ng[2];
   const int64_t b = blockIdx.x;
   const int a = blockIdx.y & 1;
+#if OZ_ROW_QMAJOR
+  // prime-major CTA order: the CTAs resident at any time mostly share one prime, so the
+  // L1 holds one prime's twiddle tables
+  const uint32_t row = (blockIdx.y >> 1) & ((1u << P.logR) - 1);
+  const int q = (int)(blockIdx.y >> (P.logR + 1));
+#else
   const int q = (blockIdx.y >> 1) & 1;
   const uint32_t row = blockIdx.y >> 2;
+#endif
   constexpr int logC = LOGC;
   constexpr uint32_t C = 1u << logC;
   constexpr int LOGE = RowCfg<LOGC, TWO_PASS>::LOGE;
@@ -719,9 +793,14 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   if (!P.fwd_only && !want0 && !want1) return;
   if (ka == 0 && !P.fwd_only) return;  // no slices: the schedule has no groups here
   uint32_t* Xs = smem;               // [K][C] forward spectra rows (row_perm order)
-  uint32_t* work = smem + K * C;     // [padC]: inter-round exchange buffer
+  // [2][padC]: inter-round exchange buffers, alternating between consecutive sub-transforms
+  // so that a sub-transform's first writes never race the previous one's last reads (the
+  // sub-transform before that one ended before the CTA barrier of the previous one)
+  uint32_t* work = smem + K * C;
+  int nsub = 0;  // sub-transforms issued so far (buffer = nsub & 1)
+  constexpr uint32_t dbuf = OZ_ROW_DBUF ? padC : 0u;  // 0: one buffer, CTA barrier per sub-transform
   // group table for 2 convs x K*K groups: npairs, then (X row offset, W row offset) x L
-  uint32_t* tab = work + padC;
+  uint32_t* tab = work + padC + dbuf;
   const int tstride = 1 + 2 * L;
   for (int ci = tv; ci < 2 && !P.fwd_only; ci += blockDim.x) {  // blockDim may be 1 (C < 32)
     const int cv = ci ? cv1 : cv0;
@@ -746,20 +825,21 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   for (int s = 0; s < ka; ++s) {
     uint32_t* xs = Xs + s * C;
     uint32_t* outX = P.Xout ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff : nullptr;
-    __syncthreads();  // `work` is free (previous sub-transform's last reads are done)
+    uint32_t* wk = work + (nsub++ & 1) * dbuf;
+    if (!OZ_ROW_DBUF && s > 0) __syncthreads();  // `work` free (previous last reads done)
     auto store_x = [&](int i, uint32_t e, uint32_t v) {
       xs[row_slot<LOGC, TWO_PASS>(tv, i)] = v;  // == row_perm(e)
       if (outX) outX[e] = v;
     };
     if constexpr (TWO_PASS) {
       const uint32_t* y = P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff;
-      sub_ntt<LOGC, false, 1, LOGE>(tv, work, 0u, 1u, Tf, p,
-                           [&](int, uint32_t e) -> uint32_t { return __ldg(&y[e]); }, store_x);
+      sub_ntt<LOGC, false, 1, LOGE, true>(tv, wk, 0u, 1u, Tf, p,
+                           [&](int, uint32_t e) -> uint32_t { return ldg_stream(&y[e]); }, store_x);
     } else {
       const int32_t* D = P.digits + ((b * 2 + a) * K + s) * P.in_len;
       const uint32_t in_len = (uint32_t)P.in_len;
-      sub_ntt<LOGC, false, 1, LOGE>(
-          tv, work, 0u, 1u, Tf, p,
+      sub_ntt<LOGC, false, 1, LOGE, true>(
+          tv, wk, 0u, 1u, Tf, p,
           [&](int, uint32_t e) -> uint32_t { return e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
           store_x);
     }
@@ -796,7 +876,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
 #pragma unroll
         for (int i = 0; i < CNT; ++i) {
           const uint32_t pe = row_slot<LOGC, TWO_PASS>(tv, i);  // == row_perm(round-0 element)
-          T[i] += (unsigned long long)xr[pe] * __ldg(&wr[pe]);
+          T[i] += (unsigned long long)xr[pe] * ldg_stream(&wr[pe]);
         }
       }
 #pragma unroll
@@ -819,15 +899,16 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   // (processing two items at once with sub_ntt_multi<..., 2> shares twiddles and barriers
   // but measured slower on B200 -- fewer resident CTAs -- so items run one at a time)
   for (int it = 0; it < nitems; ++it) {
-    if (it > 0) __syncthreads();  // exchange buffer free
+    uint32_t* wk = work + (nsub++ & 1) * dbuf;
+    if (!OZ_ROW_DBUF && it > 0) __syncthreads();  // exchange buffer free
     int ci0, g0;
     item(it, ci0, g0);
     uint32_t z[E];
     pointwise(ci0, g0, z);
     uint32_t* const zt = ztap_ptr(ci0, g0);
     uint32_t* const op = out_ptr(ci0, g0);
-    sub_ntt<LOGC, true, 1, LOGE>(
-        tv, work, 0u, 1u, Ti, p,
+    sub_ntt<LOGC, true, 1, LOGE, true>(
+        tv, wk, 0u, 1u, Ti, p,
         [&](int i, uint32_t e) -> uint32_t {
           if (zt) zt[e] = z[i];
           return z[i];
@@ -964,7 +1045,7 @@ struct ColCrtParams {
 };
 
 template <int LOGR, int LOGC>
-__global__ void __launch_bounds__(256) k_col_inv_crt(ColCrtParams P) {
+__global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_inv_crt(ColCrtParams P) {
   extern __shared__ uint32_t smem[];
   constexpr int LOGCB = col_log_cb(LOGR, LOGC);
   constexpr int LOGE = col_loge(LOGR);
@@ -1205,7 +1286,7 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   const size_t C = 1ull << pl.logC;
   const int rle = row_loge(pl.logC, pl.logR > 0);
   const size_t padC = C + (C >> rle) + 1;
-  c.row_smem = ((size_t)pl.K * C + padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
+  c.row_smem = ((size_t)pl.K * C + (OZ_ROW_DBUF ? 2 : 1) * padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
   c.row_threads = pl.logC >= rle ? (1 << (pl.logC - rle)) : 1;  // exactly Tv: every thread active
   return c;
 }
