@@ -40,9 +40,26 @@ UNIT = "GFLOP/s"
 # roofline denominators
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0        # B200_PROFILING.md fallback
-# In-register Shoup DIF butterfly rate measured on this pool's B200
-# (tools/microbench_int.cu, profiles/r01_microbench_int.txt): 3343 G butterflies/s.
-ALU_BFLY_PEAK_GPS = 3343.3
+# Integer-pipe roofline, derived from unit counts and clocks: the ALU
+# and FMA pipes each retire 64 lanes/clk/SM (B300_MICROARCH.md "rt_SMSP=2"; confirmed for
+# IADD3, VIADDMNMX and IMAD on this pool's B200, IMAD.HI at half that rate,
+# profiles/r01_microbench_bfly.txt).  A canonical Shoup butterfly needs IMAD.HI (2 slots)
+# + 2 IMAD + 2 VIADDMNMX + 2 adds = 8 lane-slots of the 128 per clock -> 16 per SM per clock.
+BFLY_PER_SM_CLK = 16
+SMS = 148
+
+
+def alu_peak_gbfly():
+    mhz = 1965.0
+    try:
+        with open(MEASURED_PEAKS) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return BFLY_PER_SM_CLK * SMS * mhz * 1e6 / 1e9
+
+
+ALU_BFLY_PEAK_GPS = alu_peak_gbfly()
 
 
 def hbm_peak():
@@ -301,7 +318,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     if d["frac_alu"] >= d["frac_hbm"]:
         roof = {"bound": "alu", "achieved": d["Gbfly_s"], "peak": ALU_BFLY_PEAK_GPS,
                 "unit": "Gbutterfly/s", "frac": d["frac_alu"], "traffic": traffic,
-                "peak_kind": "measured in-register Shoup butterfly rate (tools/microbench_int.cu)",
+                "peak_kind": "derived: 16 Shoup butterflies/clk/SM (64-lane ALU + 64-lane FMA "
+                             "pipes, 8 lane-slots per butterfly) x 148 SMs x sm_max clock; "
+                             "in-register radix-16 measured 13.1/clk/SM (tools/microbench_bfly.cu)",
                 "kernel": dom, "hbm_GB_s": d["GB_s"], "hbm_frac": d["frac_hbm"]}
     else:
         roof = {"bound": "hbm", "achieved": d["GB_s"], "peak": hbm, "unit": "GB/s",

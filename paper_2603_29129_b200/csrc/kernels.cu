@@ -489,6 +489,29 @@ __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int
   }
 }
 
+// L1 prefetch of every twiddle a thread reads in the sub-transform (same addressing as
+// dif_group / dit_group), so that the loads of a later sub-transform hit L1 instead of L2.
+template <int LOGN, bool INV, int LOGE, int R = 0>
+__device__ __forceinline__ void prefetch_sub_ntt_tw(int tv, uint32_t gb_mod, uint32_t gs,
+                                                    const uint2* __restrict__ T) {
+  if constexpr (LOGN > 0 && R < RoundT<LOGN, INV, 0, LOGE>::nr) {
+    using RT = RoundT<LOGN, INV, R, LOGE>;
+    constexpr uint32_t step = 1u << RT::logstep;
+#pragma unroll
+    for (int u = 0; u < (RT::cnt >> RT::S); ++u) {
+      const uint32_t g = (uint32_t)(tv + u * RT::Tv);
+      const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
+      const uint32_t gstep = step * gs;
+#pragma unroll
+      for (int st = 0; st < RT::S; ++st)
+#pragma unroll
+        for (int j = 0; j < (1 << st); ++j)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(&T[(gstep << st) + rmod + (uint32_t)j * gstep]));
+    }
+    prefetch_sub_ntt_tw<LOGN, INV, LOGE, R + 1>(tv, gb_mod, gs, T);
+  }
+}
+
 // Length-2^LOGN sub-transforms of NV vectors at the same positions, executed cooperatively
 // by 2^max(LOGN-LOGE,0) threads (index tv), 2^LOGE elements per thread and vector per round
 // in rounds of <= LOGE radix-2 stages; twiddles are loaded once for the NV vectors, and
@@ -560,6 +583,9 @@ __host__ __device__ constexpr int row_loge(int logC, bool two_pass) {
 #endif
 __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32_MIN_LOGR ? 5 : 4; }
 
+#ifndef OZ_CI_PF
+#define OZ_CI_PF 0
+#endif
 #ifndef OZ_CI_MINB
 #define OZ_CI_MINB 3
 #endif
@@ -1096,7 +1122,12 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
     uint32_t cur[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) cur[i] = nxt[i];
-    if (t + 1 < 2 * ng) fetch(t + 1);
+    if (t + 1 < 2 * ng) {
+      fetch(t + 1);
+#if OZ_CI_PF
+      prefetch_sub_ntt_tw<LOGR, true, LOGE>(tv, col, C, P.tw + (size_t)(((t + 1) & 1) * 2 + 1) * m);
+#endif
+    }
     if (t > 0) __syncthreads();  // smem tile free
     const uint32_t p = q ? P.F.p1 : P.F.p0;
     const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
