@@ -200,7 +200,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     x_np = workloads.draw(cfg.dist, cfg.seed, world * B, n, rows=slice(rank * B, (rank + 1) * B)) \
         if world > 1 else workloads.config_input(cfg)
     x = torch.from_numpy(x_np).to(dev)
-    plan = oz.Plan(n, B, device=dev)
+    plan = oz.Plan(n, B, device=dev, conv=args.conv)
     out = torch.empty_like(x)
     back = torch.empty_like(x) if cfg.roundtrip else None
     stream = torch.cuda.current_stream(dev)
@@ -337,6 +337,42 @@ def run_ours(args, cfg, rank, world, local_rank):
                "kind": "oracle",
                "sample": f"{ntr} transforms of {cfg.name} ({'fwd+inv' if cfg.roundtrip else 'fwd'}), "
                          f"{ts[0]:.1f} s wall, OpenMP over transforms"}
+    # ---- the paper's own cyclic convention for power-of-two n:
+    # m = n, bitwise-identical output; timed with the same protocol, reported beside
+    # the headline (which follows the north star's m >= 2n-1)
+    cyc = None
+    if args.conv == "padded" and n > 1 and n & (n - 1) == 0 and not args.no_extra:
+        pc = oz.Plan(n, B, device=dev, conv="cyclic")
+
+        def cstep():
+            pc.forward(x, out=out)
+            if cfg.roundtrip:
+                pc.inverse(out, out=back)
+
+        for _ in range(max(args.warmup, 3)):
+            cstep()
+        cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            cev[i][0].record(stream)
+            cstep()
+            cev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        c_ms = sum(a.elapsed_time(b) for a, b in cev)
+        if dist:
+            t = torch.tensor([c_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            c_ms = float(t.item())
+        cyc = {"value": total_transforms * flops_per_transform(n) / (c_ms * 1e-3) / 1e9,
+               "unit": UNIT, "ms_per_step": c_ms / args.steps, "m": pc.m,
+               "ntt_split": f"m = 2^{pc.log2_rows} x 2^{pc.log2_cols}",
+               "note": "paper's N = n cyclic Bluestein (P:238-241); output bitwise equal to the "
+                       "headline's (tests/test_gpu_cyclic.py)"}
+        del pc
     clocks = sampler.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -347,7 +383,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "ntt_split": f"m = 2^{logR} x 2^{logC}", "parallelism": f"batch-sharded x{world}",
                    "directions": "fwd+inv" if cfg.roundtrip else "fwd",
                    "l2": "flushed between timed steps (512 MiB write outside the events)",
-                   "io_dtype": "complex128"},
+                   "io_dtype": "complex128", "conv": args.conv},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
                 "d2h_bytes_per_step": io_bytes, "steps": e2e_steps},
         "gpu_launches": int(launches),
@@ -357,6 +393,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "stages": stages,
         "ntt_counts_per_transform": {"fwd": stats["fwd_ntts"] / B, "inv": stats["inv_ntts"] / B,
                                      "cached": stats["cached_ntts"]},
+        "f1_cyclic": cyc,
     }
     print(json.dumps(line), flush=True)
 
@@ -369,6 +406,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(workloads.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    ap.add_argument("--conv", default="padded", choices=["padded", "cyclic"],
+                    help="Bluestein length: m >= 2n-1 (north star) or m = n (P:238-241)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the f1_cyclic side measurement")
     args = ap.parse_args()
     cfg = workloads.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -58,9 +58,20 @@ typedef struct {
   int32_t L;                  /* NTT-domain accumulation bound, 1..8   */
   uint32_t p0, p1;            /* NTT primes, < 2^31, p-1 divisible by m            */
   int32_t device;             /* CUDA device ordinal, -1 = current                 */
-  int32_t reserved;
+  int32_t conv_mode;          /* OZFFT_CONV_PADDED (0) or OZFFT_CONV_CYCLIC (1), below */
   uint64_t max_workspace_bytes;
 } ozfft_plan_desc;
+
+/* Bluestein convolution length (desc.conv_mode).
+ *  OZFFT_CONV_PADDED: m = 2^ceil(log2(2n-1)) >= 2n-1, x' zero-padded and omega* padded with
+ *    index reversal (ZeroPad / ZeroPad_pm, Alg.4) -- any n; the north star's path.
+ *  OZFFT_CONV_CYCLIC: m = n for a power-of-two n (the Bluestein convolution is
+ *    then already cyclic -- omega*(j) = omega_2n^{-j^2} has period n for even n -- so "the FFT
+ *    length N can be kept equal to n").  Same alpha, digits and schedule as the padded plan;
+ *    the CRT integers and the fp64 output are bitwise identical to it, at half the NTT
+ *    length.  OZFFT_ERR_UNSUPPORTED_LENGTH if n is not a power of two. */
+#define OZFFT_CONV_PADDED 0
+#define OZFFT_CONV_CYCLIC 1
 
 typedef struct {
   int64_t n, m, batch, chunk;   /* m: Bluestein cyclic length; chunk: transforms per pass */
@@ -69,7 +80,7 @@ typedef struct {
   uint64_t persistent_bytes;    /* caller allocates; 256-byte aligned              */
   uint64_t workspace_bytes;     /* caller allocates; 256-byte aligned              */
   int32_t cached_ntts;          /* forward NTTs of omega~* slices done at bind */
-  int32_t reserved;
+  int32_t conv_mode;            /* as in the descriptor                                */
 } ozfft_plan_info;
 
 typedef struct {

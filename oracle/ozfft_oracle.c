@@ -402,12 +402,18 @@ void orc_plan_destroy(orc_plan* pl) {
   free(pl);
 }
 
-/* Bluestein length m = 2^ceil(log2(2n-1)) >= 2n-1 (north star). */
-orc_plan* orc_plan_create(int64_t n, int K, int L, uint32_t p0, uint32_t p1) {
+/* Bluestein length (Alg.4 Require): cyclic == 0 -> m = 2^ceil(log2(2n-1)) >= 2n-1
+ * (north star).  cyclic == 1 -> m = n for a power-of-two n: "the convolution in
+ * eq:bluestein_convolution becomes a cyclic convolution; therefore, zero-padding is
+ * unnecessary and the FFT length N can be kept equal to n".  The ZeroPad_pm
+ * formula below then reduces to omega~*(j) = omega*(j), j < n (its two ranges coincide
+ * because omega*(n - j) = omega*(j) for even n). */
+orc_plan* orc_plan_create_conv(int64_t n, int K, int L, uint32_t p0, uint32_t p1, int cyclic) {
   if (n < 1 || K < 1 || K > ORC_MAXK || L < 1 || L > ORC_MAXL) return NULL;
+  if (cyclic && (n & (n - 1))) return NULL;
   orc_plan* pl = (orc_plan*)calloc(1, sizeof(orc_plan));
   pl->n = n;
-  pl->m = pow2_ceil(2 * n - 1);
+  pl->m = cyclic ? n : pow2_ceil(2 * n - 1);
   pl->K = K;
   pl->L = L;
   pl->p[0] = p0;
@@ -448,6 +454,10 @@ orc_plan* orc_plan_create(int64_t n, int K, int L, uint32_t p0, uint32_t p1) {
         orc_ntt(dst, m, pl->p[q], 0);
       }
   return pl;
+}
+
+orc_plan* orc_plan_create(int64_t n, int K, int L, uint32_t p0, uint32_t p1) {
+  return orc_plan_create_conv(n, K, L, p0, p1, 0);
 }
 
 int64_t orc_plan_m(const orc_plan* pl) { return pl->m; }

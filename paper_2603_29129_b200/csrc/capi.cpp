@@ -171,8 +171,21 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
   pl->p[0] = p0;
   pl->p[1] = p1;
   pl->max_ws = desc.max_workspace_bytes;
+  if (desc.conv_mode != OZFFT_CONV_PADDED && desc.conv_mode != OZFFT_CONV_CYCLIC) {
+    delete pl;
+    return fail(OZFFT_ERR_INVALID_ARGUMENT, "conv_mode must be OZFFT_CONV_PADDED or OZFFT_CONV_CYCLIC");
+  }
   int64_t m = 1;
-  while (m < 2 * desc.n - 1) m <<= 1;  // Bluestein length, N >= 2n-1
+  if (desc.conv_mode == OZFFT_CONV_CYCLIC) {  // N = n for power-of-two n
+    if (desc.n & (desc.n - 1)) {
+      delete pl;
+      return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "OZFFT_CONV_CYCLIC needs a power-of-two n");
+    }
+    m = desc.n;
+  } else {
+    while (m < 2 * desc.n - 1) m <<= 1;  // Bluestein length, N >= 2n-1
+  }
+  pl->conv_mode = desc.conv_mode;
   pl->m = m;
   int logm = 0;
   while ((1ll << logm) < m) ++logm;
@@ -231,6 +244,7 @@ ozfft_status ozfft_plan_get_info(const ozfft_plan* pl, ozfft_plan_info* info) {
   info->persistent_bytes = pl->persistent_bytes;
   info->workspace_bytes = pl->workspace_bytes;
   info->cached_ntts = pl->bound ? 2 * (pl->kw[0] + pl->kw[1]) : 4 * pl->K;
+  info->conv_mode = pl->conv_mode;
   return OZFFT_OK;
 }
 

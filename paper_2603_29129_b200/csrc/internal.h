@@ -31,6 +31,7 @@ struct Plan {
   int K = 3, L = 3, alpha = 0, rho = 0;
   uint32_t p[2] = {0, 0};
   int logm = 0, logC = 0, logR = 0;  // m = R * C
+  int conv_mode = 0;                 // OZFFT_CONV_PADDED (m >= 2n-1) or OZFFT_CONV_CYCLIC (m = n)
   int device = 0;
   uint64_t max_ws = 0;
   // host tables (built at create)

@@ -1054,9 +1054,9 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
 // ============================================================== fused inverse column pass + CRT
 // For R > 1 the last log2(R) DIT stages, Garner's CRT and the scaled DD accumulation
 // of one real convolution run in one kernel: CTA = (transform, conv, column block),
-// looping over the conv's Alg.8 groups and both primes (next tile prefetched).  Only
-// the output rows i1 < R/2 are needed (n <= m/2), so the upper half of the last
-// stage is pruned.  Output: the conv's DD sum S_cv(j) = sum_g Z_g(j) 2^-cexp_g in
+// looping over the conv's Alg.8 groups and both primes (next tile prefetched).  PRUNE
+// (padded plans, n <= m/2): only the output rows i1 < R/2 are needed, so the
+// upper half of the last stage is pruned; cyclic plans (m = n) keep all rows.  Output: the conv's DD sum S_cv(j) = sum_g Z_g(j) 2^-cexp_g in
 // flush order (Alg.8 l.975-976), [nb][4][n] double2 (hi, lo).
 struct ColCrtParams {
   int logm, K, L;
@@ -1070,7 +1070,7 @@ struct ColCrtParams {
   int64_t* crt_tap;        // null, or [nb][4][K*K][n]
 };
 
-template <int LOGR, int LOGC>
+template <int LOGR, int LOGC, bool PRUNE>
 __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_inv_crt(ColCrtParams P) {
   extern __shared__ uint32_t smem[];
   constexpr int LOGCB = col_log_cb(LOGR, LOGC);
@@ -1085,10 +1085,13 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   // last DIT round: registers i with (i mod 2^S) < 2^(S-1) hold rows < R/2 (the only rows
   // needed, n <= m/2); they are packed into NH slots by hslot(i)
   constexpr int SL = RoundT<LOGR, true, NR - 1, LOGE>::S;
-  constexpr int NH = RoundT<LOGR, true, NR - 1, LOGE>::cnt / 2;
-  auto needed = [](int i) { return (i & ((1 << SL) - 1)) < (1 << (SL - 1)); };
-  auto hslot = [](int i) { return ((i >> SL) << (SL - 1)) + (i & ((1 << (SL - 1)) - 1)); };
+  constexpr int NH = RoundT<LOGR, true, NR - 1, LOGE>::cnt / (PRUNE ? 2 : 1);
+  auto needed = [](int i) { return !PRUNE || (i & ((1 << SL) - 1)) < (1 << (SL - 1)); };
+  auto hslot = [](int i) {
+    return PRUNE ? ((i >> SL) << (SL - 1)) + (i & ((1 << (SL - 1)) - 1)) : i;
+  };
   constexpr int THREADS = RoundT<LOGR, true, 0, LOGE>::Tv << LOGCB;
+  constexpr int CNTL = RoundT<LOGR, true, NR - 1, LOGE>::cnt;  // registers of the last round
   const int G = P.K * P.K;
   const uint32_t cb = blockIdx.x % ncb;
   uint32_t v = blockIdx.x / ncb;  // b * 4 + cv
@@ -1140,7 +1143,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
     if (P.res_tap) {
       uint32_t* rt = P.res_tap + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
 #pragma unroll
-      for (int i = 0; i < 2 * NH; ++i) {
+      for (int i = 0; i < CNTL; ++i) {
         if (!needed(i)) continue;
         const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
         if (e * C < lim) rt[e * C] = rr[hslot(i)];
@@ -1152,7 +1155,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
     } else {
       const double sc = s_sc[g];
 #pragma unroll
-      for (int i = 0; i < 2 * NH; ++i) {
+      for (int i = 0; i < CNTL; ++i) {
         if (!needed(i)) continue;
         const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
         const int h = hslot(i);
@@ -1170,7 +1173,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   }
   double2* So = P.S + (b * 4 + cv) * P.n + col;
 #pragma unroll
-  for (int i = 0; i < 2 * NH; ++i) {
+  for (int i = 0; i < CNTL; ++i) {
     if (!needed(i)) continue;
     const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
     if (e * C < lim) So[e * C] = Sacc[hslot(i) * THREADS + tid];
@@ -1563,14 +1566,20 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     XP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
     const int cle = col_loge(pl.logR);
     const size_t tile = ((1ull << pl.logR) + ((1ull << pl.logR) >> cle) + 1) * (1ull << c.logCb);
-    const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / 2;
+    const bool prune = 2 * n <= m;  // padded plans; cyclic plans (m = n) need every row
+    const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / (prune ? 2 : 1);
     const size_t smem = (tile + (tile & 1)) * 4 + (size_t)nh * c.col_threads * 16;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
     dispatch_log<1, 10>(pl.logR, [&](auto I) {
       dispatch_log<10, 12>(pl.logC, [&](auto J) {
-        set_smem(k_col_inv_crt<I.value, J.value>, smem);
-        k_col_inv_crt<I.value, J.value><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+        if (prune) {
+          set_smem(k_col_inv_crt<I.value, J.value, true>, smem);
+          k_col_inv_crt<I.value, J.value, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+        } else {
+          set_smem(k_col_inv_crt<I.value, J.value, false>, smem);
+          k_col_inv_crt<I.value, J.value, false><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+        }
       });
     });
     prof_mark(pl, OZFFT_STAGE_COL_INV, false, st);

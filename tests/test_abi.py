@@ -55,7 +55,7 @@ def test_plan_create_validation(lib):
 
     def create(**kw):
         d = oz.PlanDesc(**{"n": 1024, "batch": 1, "K": 3, "L": 3, "p0": 0, "p1": 0,
-                           "device": 0, "reserved": 0, "max_workspace_bytes": 0, **kw})
+                           "device": 0, "conv_mode": 0, "max_workspace_bytes": 0, **kw})
         h = ctypes.c_void_p()
         st = L.ozfft_plan_create(ctypes.byref(d), ctypes.byref(h))
         if st == 0:
@@ -80,3 +80,11 @@ def test_plan_create_validation(lib):
     assert create(n=1 << 22)[0] == 2              # m = 2^23 > this build's limit
     st, info = create(n=1)
     assert st == 0 and info.m == 1
+    # cyclic Bluestein: m = n for power-of-two n, same alpha as the padded plan
+    st, info = create(n=1 << 18, batch=16, conv_mode=1)
+    assert st == 0 and info.m == 1 << 18 and info.alpha == 20 and info.conv_mode == 1
+    st, info = create(n=1 << 20, conv_mode=1)     # m = 2^20 fits where the padded 2^21 does not
+    assert st == 0 and info.m == 1 << 20
+    assert create(n=1 << 20)[0] == 2
+    assert create(n=100003, conv_mode=1)[0] == 2  # not a power of two
+    assert create(n=1024, conv_mode=2)[0] == 1    # unknown mode
