@@ -298,13 +298,22 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
 }
 
 // ============================================================== NTT building blocks
+// twiddle load: read-only global path, or a shared-memory table (generic load)
+template <bool SMEM>
+__device__ __forceinline__ uint2 tw_load(const uint2* p) {
+  if constexpr (SMEM)
+    return *p;
+  else
+    return __ldg(p);
+}
+
 // A group of 2^S registers x[k] holding global positions gbase + k*gstep, with
 // rmod = gbase mod gstep.  DIF stages h = gstep*2^(S-1) .. gstep (block length 2h):
 //   (u, v) -> (u + v, (u - v) * T[h + (pos mod h)]),  T[h + j] = w_{2h}^j.
 // x is [NV][E] (E = elements per thread); the group occupies x[v][off .. off + 2^S).
 // UNIT: the caller guarantees rmod == 0 and gstep == 1 (the step-1 round of a row), so the
 // twiddle index is compile-time and the butterflies with T[h] = w^0 = 1 skip the product.
-template <int S, int NV, int E, bool UNIT = false>
+template <int S, int NV, int E, bool UNIT = false, bool SMEM_T = false>
 __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_t rmod,
                                           uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
   if constexpr (UNIT) {
@@ -327,7 +336,7 @@ __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_
         }
         continue;
       }
-      const uint2 w = __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);  // shared by NV
+      const uint2 w = tw_load<SMEM_T>(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);  // shared by NV
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const uint32_t a = x[v][off + k], b = x[v][off + k + d];
@@ -338,7 +347,7 @@ __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_
   }
 }
 // DIT stages h = gstep .. gstep*2^(S-1): v' = v * Tinv[h + (pos mod h)]; (u + v', u - v')
-template <int S, int NV, int E, bool UNIT = false>
+template <int S, int NV, int E, bool UNIT = false, bool SMEM_T = false>
 __device__ __forceinline__ void dit_group(uint32_t (&x)[NV][E], int off, uint32_t rmod,
                                           uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
   if constexpr (UNIT) {
@@ -353,7 +362,8 @@ __device__ __forceinline__ void dit_group(uint32_t (&x)[NV][E], int off, uint32_
     for (int k = 0; k < (1 << S); ++k) {
       if (k & d) continue;
       const bool one = UNIT && (k & (d - 1)) == 0;  // twiddle w^0 = 1
-      const uint2 w = one ? make_uint2(1u, 0u) : __ldg(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);
+      const uint2 w =
+          one ? make_uint2(1u, 0u) : tw_load<SMEM_T>(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const uint32_t a = x[v][off + k];  // always canonical: it was a "u" of this stage
@@ -430,12 +440,20 @@ struct RoundSync {
       A::Tv * CB <= 32 || (one_group && (1 << coarse_logstep) * CB <= 32);
 };
 
-template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, class LoadF,
+// Staged copy of the step-1 round's twiddles (logstep == 0): in that round every thread
+// reads T[h + gb_mod + j * gs] (h = gs 2^st), which depends only on gb_mod; a kernel may
+// stage these entries (e.g. per column in shared memory) as T0[(gs0 << st) + gb0 + j gs0].
+struct Tw0 {
+  const uint2* T;
+  uint32_t gb, gs;
+};
+
+template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, class LoadF,
           class StoreF>
 __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int tv,
                                               uint32_t* const (&sm)[NV], uint32_t gb_mod,
-                                              uint32_t gs, const uint2* __restrict__ T, uint32_t p,
-                                              LoadF& load_first, StoreF& store_last) {
+                                              uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
+                                              uint32_t p, LoadF& load_first, StoreF& store_last) {
   using RT = RoundT<LOGN, INV, R, LOGE>;
   constexpr int E = 1 << LOGE;
   constexpr uint32_t step = 1u << RT::logstep;
@@ -453,10 +471,16 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
     const uint32_t g = (uint32_t)(tv + u * RT::Tv);
     const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
     constexpr bool unit = UNIT && RT::logstep == 0;  // rmod == gb_mod == 0, gstep == gs == 1
-    if constexpr (INV)
+    if constexpr (T0S && RT::logstep == 0) {  // staged step-1 twiddles
+      if constexpr (INV)
+        dit_group<RT::S, NV, E, false, true>(x, u * (1 << RT::S), t0.gb, t0.gs, t0.T, p);
+      else
+        dif_group<RT::S, NV, E, false, true>(x, u * (1 << RT::S), t0.gb, t0.gs, t0.T, p);
+    } else if constexpr (INV) {
       dit_group<RT::S, NV, E, unit>(x, u * (1 << RT::S), rmod, step * gs, T, p);
-    else
+    } else {
       dif_group<RT::S, NV, E, unit>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+    }
   }
 #pragma unroll
   for (int v = 0; v < NV; ++v)
@@ -475,16 +499,17 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
   }
 }
 
-template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, class LoadF,
+template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, class LoadF,
           class StoreF>
 __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int tv,
                                                uint32_t* const (&sm)[NV], uint32_t gb_mod,
-                                               uint32_t gs, const uint2* __restrict__ T, uint32_t p,
-                                               LoadF& load_first, StoreF& store_last) {
+                                               uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
+                                               uint32_t p, LoadF& load_first, StoreF& store_last) {
   if constexpr (R < RoundT<LOGN, INV, 0, LOGE>::nr) {
-    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE, UNIT>(x, tv, sm, gb_mod, gs, T, p, load_first,
-                                                    store_last);
-    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE, UNIT>(x, tv, sm, gb_mod, gs, T, p, load_first,
+    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE, UNIT, T0S>(x, tv, sm, gb_mod, gs, T, t0, p,
+                                                         load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE, UNIT, T0S>(x, tv, sm, gb_mod, gs, T, t0, p,
+                                                              load_first,
                                                    store_last);
   }
 }
@@ -522,19 +547,19 @@ __device__ __forceinline__ void prefetch_sub_ntt_tw(int tv, uint32_t gb_mod, uin
 // the round-0 input of register i / element e of vector v; store_last(v, i, e, val)
 // consumes the final values.  The buffers must be free for writes on entry.  UNIT: the
 // caller passes gb_mod == 0 and gs == 1 (rows), enabling the compile-time step-1 round.
-template <int LOGN, bool INV, int CB, int NV, int LOGE = 4, bool UNIT = false, class LoadF,
-          class StoreF>
+template <int LOGN, bool INV, int CB, int NV, int LOGE = 4, bool UNIT = false, bool T0S = false,
+          class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV], uint32_t gb_mod,
-                                              uint32_t gs, const uint2* __restrict__ T, uint32_t p,
-                                              LoadF&& load_first, StoreF&& store_last) {
+                                              uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
+                                              uint32_t p, LoadF&& load_first, StoreF&& store_last) {
   if constexpr (LOGN == 0) {  // N == 1: identity
     if (tv == 0)
 #pragma unroll
       for (int v = 0; v < NV; ++v) store_last(v, 0, 0u, load_first(v, 0, 0u));
   } else {
     uint32_t x[NV][1 << LOGE];
-    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE, UNIT>(x, tv, sm, gb_mod, gs, T, p, load_first,
-                                                     store_last);
+    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE, UNIT, T0S>(x, tv, sm, gb_mod, gs, T, t0, p,
+                                                          load_first, store_last);
   }
 }
 
@@ -544,9 +569,32 @@ __device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, uint3
                                         uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                         LoadF&& load_first, StoreF&& store_last) {
   uint32_t* const sms[1] = {sm};
-  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, UNIT>(
-      tv, sms, gb_mod, gs, T, p, [&](int, int i, uint32_t e) { return load_first(i, e); },
+  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, UNIT, false>(
+      tv, sms, gb_mod, gs, T, Tw0{nullptr, 0u, 0u}, p,
+      [&](int, int i, uint32_t e) { return load_first(i, e); },
       [&](int, int i, uint32_t e, uint32_t v) { store_last(i, e, v); });
+}
+// ... with the step-1 round's twiddles read from a staged copy (Tw0).
+template <int LOGN, bool INV, int CB, int LOGE = 4, class LoadF, class StoreF>
+__device__ __forceinline__ void sub_ntt_t0(int tv, uint32_t* __restrict__ sm, uint32_t gb_mod,
+                                           uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
+                                           uint32_t p, LoadF&& load_first, StoreF&& store_last) {
+  uint32_t* const sms[1] = {sm};
+  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, false, true>(
+      tv, sms, gb_mod, gs, T, t0, p, [&](int, int i, uint32_t e) { return load_first(i, e); },
+      [&](int, int i, uint32_t e, uint32_t v) { store_last(i, e, v); });
+}
+
+// Stage the step-1 round twiddles of the Cb columns [col0, col0 + Cb) of a column pass:
+// dst[(Cb << st) + c + j Cb] = T[(C << st) + col0 + c + j C], st < S1, j < 2^st (indices
+// 1 .. 2^S1 - 1 in units of Cb; S1 = stages of that round).  All threads of the CTA.
+template <int S1, int Cb>
+__device__ __forceinline__ void stage_col_tw0(uint2* dst, const uint2* __restrict__ T, uint32_t C,
+                                              uint32_t col0) {
+  for (int i = threadIdx.x; i < ((1 << S1) - 1) * Cb; i += blockDim.x) {
+    const uint32_t r = 1u + (uint32_t)i / Cb, c = (uint32_t)i % Cb;  // r = 2^st + j
+    dst[r * Cb + c] = T[r * C + col0 + c];
+  }
 }
 
 __device__ __forceinline__ uint32_t lift(int32_t D, uint32_t p) {
@@ -608,6 +656,11 @@ __host__ __device__ constexpr int col_log_cb(int logR, int logC) {
                                        : 8);
 }
 
+// Stages of the column pass's step-1 round (DIF: the last round; DIT: the first).
+__host__ __device__ constexpr int col_s1(int logR) {
+  return logR >= col_loge(logR) ? col_loge(logR) : logR;
+}
+
 // Forward column pass: global DIF stages len = m .. 2C on columns of the R x C view.
 // One CTA per (transform, prime, part, column block) loops over the part's slices; the
 // next slice's column tile is loaded while the current one is transformed.
@@ -639,6 +692,11 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(C
   const uint32_t col = (cb << LOGCB) + c;
   const uint2* T = P.tw + (size_t)(q * 2 + 0) * m;
   const uint32_t lim = P.in_len > col ? (uint32_t)(P.in_len - col) : 0u;  // e*C < lim <=> i < in_len
+  constexpr int S1 = col_s1(LOGR);
+  constexpr uint32_t TILEW = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;  // even (Cb >= 8)
+  uint2* tw0 = reinterpret_cast<uint2*>(smem + TILEW);  // [2^S1][Cb] step-1 twiddles
+  stage_col_tw0<S1, Cb>(tw0, T, C, cb << LOGCB);
+  __syncthreads();
   uint32_t nxt[E];
   auto fetch = [&](int s) {
     const int32_t* D = P.digits + ((b * 2 + a) * P.K + s) * P.in_len + col;
@@ -656,8 +714,9 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(C
     if (s + 1 < ka) fetch(s + 1);
     if (s > 0) __syncthreads();  // smem tile free
     uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (int64_t)m + col;
-    sub_ntt<LOGR, false, Cb, LOGE>(
-        tv, smem + c, col, C, T, p, [&](int i, uint32_t) -> uint32_t { return cur[i]; },
+    sub_ntt_t0<LOGR, false, Cb, LOGE>(
+        tv, smem + c, col, C, T, Tw0{tw0, (uint32_t)c, (uint32_t)Cb}, p,
+        [&](int i, uint32_t) -> uint32_t { return cur[i]; },
         [&](int, uint32_t e, uint32_t val) { out[e * C] = val; });
   }
 }
@@ -1107,6 +1166,8 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   for (int g = tid; g < ng; g += blockDim.x) s_sc[g] = scalbn(1.0, -srow[1 + g * (2 + 2 * P.L)]);
   constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;
   double2* Sacc = reinterpret_cast<double2*>(smem + TILE + (TILE & 1));  // [NH][THREADS]
+  // (staging the step-1 round twiddles in shared memory, as k_col_fwd does, measured slower
+  // here: 833 vs 813 us at c3 -- they already hit L1, shared by the 16 threads of a column)
 #pragma unroll
   for (int i = 0; i < NH; ++i) Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
   const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
@@ -1308,6 +1369,7 @@ static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cud
 struct NttLaunch {
   int logCb;
   size_t col_smem;
+  size_t col_fwd_smem;  // + staged step-1 twiddles
   int col_threads;
   size_t row_smem;
   int row_threads;
@@ -1316,6 +1378,7 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   NttLaunch c;
   c.logCb = col_logCb(pl.logR, pl.logC);
   c.col_smem = col_smem(pl.logR, c.logCb);
+  c.col_fwd_smem = c.col_smem + ((size_t)1 << col_s1(pl.logR)) * ((size_t)1 << c.logCb) * 8;
   c.col_threads = col_threads(pl.logR, c.logCb);
   const size_t C = 1ull << pl.logC;
   const int rle = row_loge(pl.logC, pl.logR > 0);
@@ -1346,8 +1409,8 @@ template <int LOGR>
 static void launch_col_fwd_r(int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
                              const ColParams& CP) {
   dispatch_log<10, 12>(logC, [&](auto J) {
-    set_smem(k_col_fwd<LOGR, J.value>, c.col_smem);
-    k_col_fwd<LOGR, J.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
+    set_smem(k_col_fwd<LOGR, J.value>, c.col_fwd_smem);
+    k_col_fwd<LOGR, J.value><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
   });
 }
 template <int LOGR>
