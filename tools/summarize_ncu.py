@@ -23,22 +23,26 @@ for r in rows:
         k = d["Kernel Name"].split("(")[0].replace("void ", "")
         if k not in agg:
             order.append(k)
-        agg.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+        a = agg.setdefault(k, {})
+        a[d["Metric Name"]] = a.get(d["Metric Name"], 0.0) + float(d["Metric Value"].replace(",", ""))
+        a.setdefault("_ids", set()).add(d["ID"])
 tot = sum(v.get("gpu__time_duration.sum", 0) for v in agg.values())
 stage_of = {"k_split_max": "split_max", "k_split_digits": "split_digits", "k_col_fwd": "col_fwd",
             "k_row_fused": "row_fused", "k_col_inv_crt": "col_inv", "k_col_inv": "col_inv",
             "k_finish_dd": "crt_finish", "k_crt_finish": "crt_finish"}
 traffic = {}
 lines = [f"# ncu launch list, c3 forward execute ({tag}); cold-cache, serialised: compare shares\n",
-         "| kernel | time (us) | share | DRAM read (MB) | DRAM write (MB) |", "|---|---|---|---|---|"]
+         "| kernel | launches | time (us) | share | DRAM read (MB) | DRAM write (MB) |",
+         "|---|---|---|---|---|---|"]
 for k in order:
     v = agg[k]
+    nl = len(v["_ids"])
     t = v.get("gpu__time_duration.sum", 0)
     rd, wr = v.get("dram__bytes_read.sum", 0), v.get("dram__bytes_write.sum", 0)
-    lines.append(f"| {k} | {t / 1e3:.1f} | {t / tot:.3f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} |")
+    lines.append(f"| {k} | {nl} | {t / 1e3:.1f} | {t / tot:.3f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} |")
     base = k.split("<")[0]
     if base in stage_of:
-        traffic[stage_of[base]] = rd + wr
+        traffic[stage_of[base]] = (rd + wr) / nl  # per launch
 open(os.path.join(prof, f"{tag}_launches_c3.md"), "w").write("\n".join(lines) + "\n")
 tf = os.path.join(prof, "ncu_traffic.json")
 allt = json.load(open(tf)) if os.path.exists(tf) else {}
@@ -57,7 +61,11 @@ raw_keys = ["sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "dram__bytes_read.sum",
-            "dram__bytes_write.sum", "smsp__inst_executed.sum"]
+            "dram__bytes_write.sum", "smsp__inst_executed.sum",
+            "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed.avg.per_cycle_active",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active"]
 for f in sorted(os.listdir(ev)):
     if not f.endswith(".ncu-rep"):
         continue
@@ -88,5 +96,13 @@ for f in sorted(os.listdir(ev)):
     for x, k in sorted(stalls, reverse=True)[:10]:
         out.append(f"  {x / s:6.3f} {k}")
     name = f.replace(".ncu-rep", "")
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    tmp = os.path.join(ev, name + "_sass.csv")
+    open(tmp, "w").write(src)
+    hot = subprocess.run([sys.executable, os.path.join(root, "tools", "sass_hot.py"), tmp, "15"],
+                         capture_output=True, text=True).stdout
+    out.append("\nSASS opcode mix and hottest instructions (tools/sass_hot.py):")
+    out.append(hot)
     open(os.path.join(prof, f"{tag}_{name}.txt"), "w").write("\n".join(out) + "\n")
 print(open(os.path.join(prof, f"{tag}_launches_c3.md")).read())
