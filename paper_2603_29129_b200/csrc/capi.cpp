@@ -194,14 +194,15 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     delete pl;
     return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "m exceeds the primes' two-adicity");
   }
-  if (logm > 20) {
+  if (logm > 22) {
     delete pl;
-    return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "this build supports m <= 2^20 (n <= 2^19)");
+    return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "this build supports m <= 2^22 (n <= 2^21 padded, 2^22 cyclic)");
   }
-  // NTT decomposition: one pass up to m = 2^12, else rows of C = 2^11 (2^12 at m = 2^20) and
-  // columns of R = m / C <= 2^8.  (One-warp rows of C = 2^10 with 32 elements per thread,
-  // OZFFT_TUNE_LOGC=10, measured slower on B200: 122 vs 147 GFLOP/s at c3.)
-  pl->logC = logm <= 12 ? logm : std::max(11, logm - 8);
+  // NTT decomposition: one pass up to m = 2^12, else rows of C = 2^11 (2^12 from m = 2^20) and
+  // columns of R = m / C <= 2^8 (up to 2^10 at m = 2^21, 2^22, with 32 elements per thread).
+  // (One-warp rows of C = 2^10 with 32 elements per thread, OZFFT_TUNE_LOGC=10, measured
+  // slower on B200: 122 vs 147 GFLOP/s at c3.)
+  pl->logC = logm <= 12 ? logm : std::min(12, std::max(11, logm - 8));
   if (const char* t = std::getenv("OZFFT_TUNE_LOGC")) {  // tuning knob (tools/, not the hot path)
     const int v = std::atoi(t);
     if ((v == 10 || v == 11) && logm > 12 && logm - v <= 10) pl->logC = v;

@@ -83,8 +83,11 @@ def test_plan_create_validation(lib):
     # cyclic Bluestein: m = n for power-of-two n, same alpha as the padded plan
     st, info = create(n=1 << 18, batch=16, conv_mode=1)
     assert st == 0 and info.m == 1 << 18 and info.alpha == 20 and info.conv_mode == 1
-    st, info = create(n=1 << 20, conv_mode=1)     # m = 2^20 fits where the padded 2^21 does not
+    st, info = create(n=1 << 20, conv_mode=1)     # m = 2^20
     assert st == 0 and info.m == 1 << 20
-    assert create(n=1 << 20)[0] == 2
+    st, info = create(n=1 << 21)                  # m = 2^22 = 2^10 x 2^12, the largest
+    assert st == 0 and info.m == 1 << 22 and info.log2_rows == 10 and info.log2_cols == 12
+    assert create(n=(1 << 21) + 1)[0] == 2        # m = 2^23: beyond this build
+    assert create(n=1 << 22, conv_mode=1)[0] == 0
     assert create(n=100003, conv_mode=1)[0] == 2  # not a power of two
     assert create(n=1024, conv_mode=2)[0] == 1    # unknown mode

@@ -98,3 +98,16 @@ def test_decomposition_sizes(oz, n, B):
         for cv in range(4):
             ng = int(ot["sched"][cv, 0])
             assert np.array_equal(gt["crt"][b, cv, :ng].cpu().numpy(), ot["crt"][cv, :ng])
+
+
+@pytest.mark.parametrize("n,conv", [(600000, "padded"), (1 << 21, "padded"), (1 << 21, "cyclic")])
+def test_largest_sizes(oz, n, conv):
+    """The largest decompositions this build supports: m = 2^21 (R = 2^9, 32 elements per
+    thread in the column passes) and m = 2^22 = 2^10 x 2^12; cyclic m = n = 2^21.  One
+    transform, fp64 output bitwise equal to the oracle (whose integer stages are pinned)."""
+    x = workloads.draw("uniform", 21, 1, n)
+    plan = oz.Plan(n, 1, conv=conv)
+    y = plan.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert plan.stats()["nonfinite"] == 0
+    yo = O.Plan(n, cyclic=(conv == "cyclic")).execute(x[0])
+    assert np.array_equal(y[0], yo)
