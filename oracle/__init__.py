@@ -73,6 +73,9 @@ def lib():
                                    C.c_int, C.c_void_p]
         L.orc_plan_create.restype = C.c_void_p
         L.orc_plan_create.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint32, C.c_uint32]
+        L.orc_plan_create_ex.restype = C.c_void_p
+        L.orc_plan_create_ex.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint32, C.c_uint32,
+                                         C.c_int, C.c_int]
         L.orc_plan_create_conv.restype = C.c_void_p
         L.orc_plan_create_conv.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint32, C.c_uint32,
                                            C.c_int]
@@ -211,10 +214,11 @@ class Plan:
     """Oracle plan: chirp, omega~* split, and the cached W spectra."""
 
     def __init__(self, n: int, K: int = 3, L: int = 3, p0: int = P0, p1: int = P1,
-                 cyclic: bool = False):
-        """cyclic: m = n for power-of-two n instead of m >= 2n-1."""
-        self.n, self.K, self.L, self.p, self.cyclic = n, K, L, (p0, p1), cyclic
-        self._h = lib().orc_plan_create_conv(n, K, L, p0, p1, 1 if cyclic else 0)
+                 cyclic: bool = False, image: bool = False):
+        """cyclic: m = n for power-of-two n instead of m >= 2n-1.
+        image: complex-image accumulation (orc_execute_image)."""
+        self.n, self.K, self.L, self.p, self.cyclic, self.image = n, K, L, (p0, p1), cyclic, image
+        self._h = lib().orc_plan_create_ex(n, K, L, p0, p1, 1 if cyclic else 0, 1 if image else 0)
         if not self._h:
             raise ValueError("orc_plan_create failed")
         self.m = lib().orc_plan_m(self._h)

@@ -308,6 +308,43 @@ int orc_split(int64_t len, double* hi, double* lo, int alpha, int K, int32_t* di
   return k;
 }
 
+/* Image mode (beyond the paper): Alg.6 applied to the complex vector
+ * with ONE exponent per level shared by both parts -- mu = max_j max(|hi_re|, |hi_im|),
+ * then the same sigma and scale for both parts, each part stepping exactly as orc_split.
+ * digits is [2 parts][K][len]; returns the common level count (or -1, non-finite). */
+int orc_split_shared(int64_t len, double* hre, double* lre, double* him, double* lim, int alpha,
+                     int K, int32_t* digits, int32_t* E) {
+  const int rho = 53 - alpha;
+  int k;
+  for (k = 0; k < K; k++) {
+    double mu = 0.0;
+    for (int64_t j = 0; j < len; j++) {
+      double a = fabs(hre[j]), b = fabs(him[j]);
+      if (a > mu || a != a) mu = a;
+      if (b > mu || b != b) mu = b;
+    }
+    if (!isfinite(mu)) return -1;
+    if (mu == 0.0) break;
+    int Ek = ceil_log2_exact(mu);
+    double sigma = ldexp(1.0, Ek + rho);
+    double scale = ldexp(1.0, alpha - Ek);
+    E[k] = Ek;
+    for (int part = 0; part < 2; part++) {
+      double* hi = part ? him : hre;
+      double* lo = part ? lim : lre;
+      int32_t* D = digits + ((int64_t)part * K + k) * len;
+      for (int64_t j = 0; j < len; j++) {
+        double t = hi[j] + sigma;
+        double d = t - sigma;
+        D[j] = (int32_t)(d * scale);
+        double r = hi[j] - d;
+        fast_two_sum(r, lo[j], &hi[j], &lo[j]);
+      }
+    }
+  }
+  return k;
+}
+
 /* ------------------------------------------------------------------------- */
 /* O6. Alg.8 flush schedule (literally).  For one real convolution  */
 /* with kx slices of scale exponents sx[] and ky slices with sy[]:             */
@@ -369,8 +406,10 @@ typedef struct {
   int32_t* wdig;        /* omega~* digits [2 parts][K][m] */
   int32_t Ew[2][ORC_MAXK];
   int kw[2];
-  uint32_t* W;          /* [2 parts][K][2 primes][m], natural order */
+  uint32_t* W;          /* [2 parts][K][2 primes][m], natural order; image mode: [2 images] */
   int status;
+  int image;            /* 1: complex-image accumulation, see orc_execute_image */
+  uint32_t iota[2];     /* image mode: iota_q = g_q^((p_q - 1)/4), iota^2 = -1 mod p_q */
 } orc_plan;
 
 typedef struct {
@@ -408,9 +447,11 @@ void orc_plan_destroy(orc_plan* pl) {
  * unnecessary and the FFT length N can be kept equal to n".  The ZeroPad_pm
  * formula below then reduces to omega~*(j) = omega*(j), j < n (its two ranges coincide
  * because omega*(n - j) = omega*(j) for even n). */
-orc_plan* orc_plan_create_conv(int64_t n, int K, int L, uint32_t p0, uint32_t p1, int cyclic) {
+orc_plan* orc_plan_create_ex(int64_t n, int K, int L, uint32_t p0, uint32_t p1, int cyclic,
+                             int image) {
   if (n < 1 || K < 1 || K > ORC_MAXK || L < 1 || L > ORC_MAXL) return NULL;
   if (cyclic && (n & (n - 1))) return NULL;
+  if (image && ((p0 & 3u) != 1u || (p1 & 3u) != 1u)) return NULL; /* need iota, p = 1 mod 4 */
   orc_plan* pl = (orc_plan*)calloc(1, sizeof(orc_plan));
   pl->n = n;
   pl->m = cyclic ? n : pow2_ceil(2 * n - 1);
@@ -418,7 +459,13 @@ orc_plan* orc_plan_create_conv(int64_t n, int K, int L, uint32_t p0, uint32_t p1
   pl->L = L;
   pl->p[0] = p0;
   pl->p[1] = p1;
-  pl->alpha = orc_alpha(n, L, p0, p1); /* n = DFT length (ruling 2) */
+  pl->image = image;
+  /* n = DFT length (ruling 2).  Image mode: a real output of a group sums up to L n
+   * complex products, |Re(ab)| <= |ar br| + |ai bi| <= 2 4^alpha, so the bound is
+   * 2 L n 4^alpha < P/2, i.e. the real-mode alpha at 2n. */
+  pl->alpha = orc_alpha(image ? 2 * n : n, L, p0, p1);
+  if (image)
+    for (int q = 0; q < 2; q++) pl->iota[q] = orc_root_of_unity(pl->p[q], 4);
   int64_t m = pl->m;
   pl->C = (double*)malloc(sizeof(double) * n);
   pl->S = (double*)malloc(sizeof(double) * n);
@@ -439,9 +486,34 @@ orc_plan* orc_plan_create_conv(int64_t n, int K, int L, uint32_t p0, uint32_t p1
   }
   /* -S of +0.0 is -0.0: zeros compare equal and split identically */
   pl->wdig = (int32_t*)calloc((size_t)2 * K * m, sizeof(int32_t));
-  pl->kw[0] = orc_split(m, hre, lre, pl->alpha, K, pl->wdig, pl->Ew[0]);
-  pl->kw[1] = orc_split(m, him, lim, pl->alpha, K, pl->wdig + (size_t)K * m, pl->Ew[1]);
+  if (image) {
+    pl->kw[0] = pl->kw[1] = orc_split_shared(m, hre, lre, him, lim, pl->alpha, K, pl->wdig,
+                                             pl->Ew[0]);
+    for (int k = 0; k < K; k++) pl->Ew[1][k] = pl->Ew[0][k];
+  } else {
+    pl->kw[0] = orc_split(m, hre, lre, pl->alpha, K, pl->wdig, pl->Ew[0]);
+    pl->kw[1] = orc_split(m, him, lim, pl->alpha, K, pl->wdig + (size_t)K * m, pl->Ew[1]);
+  }
   free(hre); free(him); free(lre); free(lim);
+  if (image) { /* W images: NTT(Dre + iota Dim) (b = 0) and NTT(Dre - iota Dim) (b = 1) */
+    pl->W = (uint32_t*)calloc((size_t)2 * K * 2 * m, sizeof(uint32_t));
+    for (int b = 0; b < 2; b++)
+      for (int t = 0; t < pl->kw[0]; t++)
+        for (int q = 0; q < 2; q++) {
+          const uint32_t p = pl->p[q];
+          const uint32_t io = b ? p - pl->iota[q] : pl->iota[q];
+          uint32_t* dst = pl->W + (((size_t)b * K + t) * 2 + q) * m;
+          const int32_t* Dr = pl->wdig + (size_t)t * m;
+          const int32_t* Di = pl->wdig + ((size_t)K + t) * m;
+          for (int64_t j = 0; j < m; j++) {
+            uint32_t r = Dr[j] >= 0 ? (uint32_t)Dr[j] : (uint32_t)((int64_t)Dr[j] + p);
+            uint32_t i = Di[j] >= 0 ? (uint32_t)Di[j] : (uint32_t)((int64_t)Di[j] + p);
+            dst[j] = addmod(r, mulmod(io, i, p), p);
+          }
+          orc_ntt(dst, m, p, 0);
+        }
+    return pl;
+  }
   /* the 4K forward NTTs of the omega~* slices, computed once */
   pl->W = (uint32_t*)calloc((size_t)2 * K * 2 * m, sizeof(uint32_t));
   for (int b = 0; b < 2; b++)
@@ -456,8 +528,11 @@ orc_plan* orc_plan_create_conv(int64_t n, int K, int L, uint32_t p0, uint32_t p1
   return pl;
 }
 
+orc_plan* orc_plan_create_conv(int64_t n, int K, int L, uint32_t p0, uint32_t p1, int cyclic) {
+  return orc_plan_create_ex(n, K, L, p0, p1, cyclic, 0);
+}
 orc_plan* orc_plan_create(int64_t n, int K, int L, uint32_t p0, uint32_t p1) {
-  return orc_plan_create_conv(n, K, L, p0, p1, 0);
+  return orc_plan_create_ex(n, K, L, p0, p1, 0, 0);
 }
 
 int64_t orc_plan_m(const orc_plan* pl) { return pl->m; }
@@ -483,7 +558,168 @@ void orc_plan_copy(const orc_plan* pl, double* C, double* S, int32_t* wdig, uint
 /* (O10, ruling 16).                                                          */
 /* Returns 0, or 1 if the input was non-finite (output all NaN, ruling 18).   */
 /* ------------------------------------------------------------------------- */
+/* ------------------------------------------------------------------------- */
+/* Image mode (builds on P:916-938; beyond the  */
+/* paper).  The complex digit vectors D = Dre + i Dim (shared exponents, above)   */
+/* and Dw of omega~* are convolved as complex integers.  Since iota^2 = -1 mod p, */
+/* a -> a+ = ar + iota ai and a -> a- = ar - iota ai are ring homomorphisms of     */
+/* Z[i] -> Z_p, so (D (*) Dw)+- = D+- (*) Dw+-: two modular cyclic convolutions    */
+/* (images) replace the four real ones.  Per Alg.8 group and image:               */
+/*   Z+-_g = sum_(s,t) NTT(D+-_s) (.) W+-_t,  z+-_g = NTT^-1(Z+-_g)               */
+/* then per prime  re = (z+ + z-) / 2,  im = (z+ - z-) / (2 iota)  (mod p), Garner */
+/* on each across the primes, and the DD sums of re 2^-c and im 2^-c in flush     */
+/* order give y' directly.  Forward: 2 images x k slices x 2 primes; inverse:     */
+/* 2 images x groups x 2 primes (32 runtime NTTs at (K, L) = (3, 3) vs 52).       */
+/* Taps: digits / E / kv as the real mode (E and kv repeated per part); X[img];  */
+/* sched row 0 (rows 1-3 zero); Z[img], res[img]; crt row 0 = Re, row 1 = Im.    */
+/* ------------------------------------------------------------------------- */
+static int orc_execute_image(const orc_plan* pl, const double* x, double* y, int dir,
+                             orc_taps* tp) {
+  const int64_t n = pl->n, m = pl->m;
+  const int K = pl->K, L = pl->L, alpha = pl->alpha;
+  const int stride = orc_sched_stride(K, L);
+  const int G = K * K;
+  int flags = 0;
+  int64_t nfwd = 0, ninv = 0;
+  double* hr = (double*)malloc(sizeof(double) * n);
+  double* lr = (double*)malloc(sizeof(double) * n);
+  double* hi = (double*)malloc(sizeof(double) * n);
+  double* li = (double*)malloc(sizeof(double) * n);
+  orc_premul(n, x, pl->C, pl->S, dir > 0, hr, lr, hi, li);
+  if (tp && tp->xdd) {
+    memcpy(tp->xdd, hr, sizeof(double) * n);
+    memcpy(tp->xdd + n, lr, sizeof(double) * n);
+    memcpy(tp->xdd + 2 * n, hi, sizeof(double) * n);
+    memcpy(tp->xdd + 3 * n, li, sizeof(double) * n);
+  }
+  int32_t* dig = (int32_t*)calloc((size_t)2 * K * n, sizeof(int32_t));
+  int32_t Ex[ORC_MAXK] = {0};
+  const int kx = orc_split_shared(n, hr, lr, hi, li, alpha, K, dig, Ex);
+  free(hr); free(lr); free(hi); free(li);
+  if (kx < 0) {
+    flags |= 1;
+    for (int64_t j = 0; j < 2 * n; j++) y[j] = NAN;
+    if (tp && tp->flags) tp->flags[0] = flags;
+    free(dig);
+    return 1;
+  }
+  if (tp && tp->digits) memcpy(tp->digits, dig, sizeof(int32_t) * 2 * K * n);
+  if (tp && tp->E)
+    for (int a = 0; a < 2; a++)
+      for (int k = 0; k < K; k++) tp->E[a * K + k] = k < kx ? Ex[k] : 0;
+  if (tp && tp->kv) { tp->kv[0] = kx; tp->kv[1] = kx; }
+  /* forward NTTs of the digit images */
+  uint32_t* X = (uint32_t*)calloc((size_t)2 * K * 2 * m, sizeof(uint32_t));
+  for (int img = 0; img < 2; img++)
+    for (int s = 0; s < kx; s++)
+      for (int q = 0; q < 2; q++) {
+        const uint32_t p = pl->p[q];
+        const uint32_t io = img ? p - pl->iota[q] : pl->iota[q];
+        uint32_t* dst = X + (((size_t)img * K + s) * 2 + q) * m;
+        const int32_t* Dr = dig + (size_t)s * n;
+        const int32_t* Di = dig + ((size_t)K + s) * n;
+        for (int64_t j = 0; j < m; j++) {
+          int64_t vr = j < n ? Dr[j] : 0, vi = j < n ? Di[j] : 0;
+          uint32_t r = vr >= 0 ? (uint32_t)vr : (uint32_t)(vr + p);
+          uint32_t i = vi >= 0 ? (uint32_t)vi : (uint32_t)(vi + p);
+          dst[j] = addmod(r, mulmod(io, i, p), p);
+        }
+        orc_ntt(dst, m, p, 0);
+        nfwd++;
+      }
+  free(dig);
+  if (tp && tp->X) memcpy(tp->X, X, sizeof(uint32_t) * 2 * K * 2 * m);
+  int32_t sx[ORC_MAXK], sw[ORC_MAXK];
+  for (int k = 0; k < K; k++) {
+    sx[k] = alpha - Ex[k];
+    sw[k] = alpha - pl->Ew[0][k];
+  }
+  int32_t* sched = (int32_t*)malloc(sizeof(int32_t) * stride);
+  const int ng = orc_schedule(kx, sx, pl->kw[0], sw, K, L, sched);
+  if (tp && tp->sched) {
+    memset(tp->sched, 0, sizeof(int32_t) * 4 * stride);
+    memcpy(tp->sched, sched, sizeof(int32_t) * stride);
+  }
+  /* (2 iota)^-1 and 2^-1 per prime */
+  uint32_t inv2[2], inv2i[2];
+  for (int q = 0; q < 2; q++) {
+    inv2[q] = orc_invmod(2, pl->p[q]);
+    inv2i[q] = orc_invmod(mulmod(2, pl->iota[q], pl->p[q]), pl->p[q]);
+  }
+  double* acc = (double*)calloc((size_t)4 * n, sizeof(double)); /* DD re, DD im */
+  uint32_t* Zg = (uint32_t*)malloc(sizeof(uint32_t) * 4 * m);    /* [img][q][m] */
+  for (int g = 0; g < ng; g++) {
+    const int32_t* gr = sched + 1 + g * (2 + 2 * L);
+    const int32_t cexp = gr[0], np = gr[1];
+    for (int img = 0; img < 2; img++)
+      for (int q = 0; q < 2; q++) {
+        uint32_t* Zq = Zg + ((size_t)img * 2 + q) * m;
+        for (int64_t i = 0; i < m; i++) Zq[i] = 0;
+        for (int e = 0; e < np; e++) {
+          const int s = gr[2 + 2 * e], t = gr[3 + 2 * e];
+          const uint32_t* Xs = X + (((size_t)img * K + s) * 2 + q) * m;
+          const uint32_t* Wt = pl->W + (((size_t)img * K + t) * 2 + q) * m;
+          for (int64_t i = 0; i < m; i++)
+            Zq[i] = addmod(Zq[i], mulmod(Xs[i], Wt[i], pl->p[q]), pl->p[q]);
+        }
+        if (tp && tp->Z)
+          memcpy(tp->Z + (((size_t)img * G + g) * 2 + q) * m, Zq, sizeof(uint32_t) * m);
+        orc_ntt(Zq, m, pl->p[q], 1);
+        ninv++;
+        if (tp && tp->res)
+          memcpy(tp->res + (((size_t)img * G + g) * 2 + q) * n, Zq, sizeof(uint32_t) * n);
+      }
+    const double scale = ldexp(1.0, -cexp);
+    for (int64_t j = 0; j < n; j++) {
+      uint32_t zr[2], zi[2];
+      for (int q = 0; q < 2; q++) {
+        const uint32_t p = pl->p[q];
+        const uint32_t zp = Zg[((size_t)0 * 2 + q) * m + j], zm = Zg[((size_t)1 * 2 + q) * m + j];
+        zr[q] = mulmod(addmod(zp, zm, p), inv2[q], p);
+        zi[q] = mulmod(addmod(zp, p - zm, p), inv2i[q], p);
+      }
+      for (int part = 0; part < 2; part++) {
+        int fix = 0;
+        const int64_t Zj = part ? orc_garner2(zi[0], zi[1], pl->p[0], pl->p[1], &fix)
+                                : orc_garner2(zr[0], zr[1], pl->p[0], pl->p[1], &fix);
+        if (fix) flags |= 2;
+        if (tp && tp->crt) tp->crt[((size_t)part * G + g) * n + j] = Zj;
+        double h = (double)Zj;
+        double l = (double)(Zj - (int64_t)h);
+        dd_add(acc[(part * 2) * n + j], acc[(part * 2 + 1) * n + j], h * scale, l * scale,
+               &acc[(part * 2) * n + j], &acc[(part * 2 + 1) * n + j]);
+      }
+    }
+  }
+  free(Zg); free(sched); free(X);
+  for (int64_t j = 0; j < n; j++) {
+    const double yrh = acc[j], yrl = acc[n + j], yih = acc[2 * n + j], yil = acc[3 * n + j];
+    double a1h, a1l, a2h, a2l, o_re, o_im, tmp;
+    dd_mul_d(yrh, yrl, pl->C[j], &a1h, &a1l);
+    dd_mul_d(yih, yil, pl->S[j], &a2h, &a2l);
+    dd_add(a1h, a1l, -a2h, -a2l, &o_re, &tmp);
+    dd_mul_d(yrh, yrl, pl->S[j], &a1h, &a1l);
+    dd_mul_d(yih, yil, pl->C[j], &a2h, &a2l);
+    dd_add(a1h, a1l, a2h, a2l, &o_im, &tmp);
+    if (dir > 0) {
+      o_re = o_re / (double)n;
+      o_im = -o_im / (double)n;
+    }
+    y[2 * j] = o_re;
+    y[2 * j + 1] = o_im;
+  }
+  free(acc);
+  if (tp && tp->counts) {
+    tp->counts[0] = nfwd;
+    tp->counts[1] = ninv;
+    tp->counts[2] = 4 * (int64_t)pl->kw[0];
+  }
+  if (tp && tp->flags) tp->flags[0] = flags;
+  return 0;
+}
+
 int orc_execute(const orc_plan* pl, const double* x, double* y, int dir, orc_taps* tp) {
+  if (pl->image) return orc_execute_image(pl, x, y, dir, tp);
   const int64_t n = pl->n, m = pl->m;
   const int K = pl->K, L = pl->L, alpha = pl->alpha;
   const int stride = orc_sched_stride(K, L);
