@@ -200,7 +200,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     x_np = workloads.draw(cfg.dist, cfg.seed, world * B, n, rows=slice(rank * B, (rank + 1) * B)) \
         if world > 1 else workloads.config_input(cfg)
     x = torch.from_numpy(x_np).to(dev)
-    plan = oz.Plan(n, B, device=dev, conv=args.conv)
+    plan = oz.Plan(n, B, device=dev, conv=args.conv, accum=args.accum)
     out = torch.empty_like(x)
     back = torch.empty_like(x) if cfg.roundtrip else None
     stream = torch.cuda.current_stream(dev)
@@ -337,12 +337,14 @@ def run_ours(args, cfg, rank, world, local_rank):
                "kind": "oracle",
                "sample": f"{ntr} transforms of {cfg.name} ({'fwd+inv' if cfg.roundtrip else 'fwd'}), "
                          f"{ts[0]:.1f} s wall, OpenMP over transforms"}
-    # ---- the paper's own cyclic convention for power-of-two n:
-    # m = n, bitwise-identical output; timed with the same protocol, reported beside
-    # the headline (which follows the north star's m >= 2n-1)
-    cyc = None
-    if args.conv == "padded" and n > 1 and n & (n - 1) == 0 and not args.no_extra:
-        pc = oz.Plan(n, B, device=dev, conv="cyclic")
+    # ---- side measurements, same protocol, reported beside the headline (which follows the
+    # north star: m >= 2n-1, the paper's four real convolutions):
+    #   f1_cyclic: the paper's N = n cyclic Bluestein for power-of-two n, output
+    #              bitwise equal to the headline's (tests/test_gpu_cyclic.py);
+    #   f2_image:  complex-image accumulation (beyond the paper; own oracle mode,
+    #              tests/test_gpu_image.py), padded and, for power-of-two n, cyclic.
+    def side(conv, accum):
+        pc = oz.Plan(n, B, device=dev, conv=conv, accum=accum)
 
         def cstep():
             pc.forward(x, out=out)
@@ -367,12 +369,25 @@ def run_ours(args, cfg, rank, world, local_rank):
             t = torch.tensor([c_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             c_ms = float(t.item())
-        cyc = {"value": total_transforms * flops_per_transform(n) / (c_ms * 1e-3) / 1e9,
-               "unit": UNIT, "ms_per_step": c_ms / args.steps, "m": pc.m,
-               "ntt_split": f"m = 2^{pc.log2_rows} x 2^{pc.log2_cols}",
-               "note": "paper's N = n cyclic Bluestein (P:238-241); output bitwise equal to the "
-                       "headline's (tests/test_gpu_cyclic.py)"}
+        st = pc.stats()
+        r = {"value": total_transforms * flops_per_transform(n) / (c_ms * 1e-3) / 1e9,
+             "unit": UNIT, "ms_per_step": c_ms / args.steps, "m": pc.m, "alpha": pc.alpha,
+             "conv": conv, "accum": accum,
+             "ntt_split": f"m = 2^{pc.log2_rows} x 2^{pc.log2_cols}",
+             "ntts_per_transform": (st["fwd_ntts"] + st["inv_ntts"]) / B}
         del pc
+        return r
+
+    pow2 = n > 1 and n & (n - 1) == 0
+    cyc = img = imgc = None
+    if args.conv == "padded" and args.accum == "real" and not args.no_extra:
+        if pow2:
+            cyc = side("cyclic", "real")
+            cyc["note"] = "paper's N = n cyclic Bluestein (P:238-241); bitwise equal to the headline"
+        img = side("padded", "image")
+        img["note"] = "complex-image accumulation (SURVEY f2; beyond the paper; own oracle mode)"
+        if pow2:
+            imgc = side("cyclic", "image")
     clocks = sampler.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -383,7 +398,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "ntt_split": f"m = 2^{logR} x 2^{logC}", "parallelism": f"batch-sharded x{world}",
                    "directions": "fwd+inv" if cfg.roundtrip else "fwd",
                    "l2": "flushed between timed steps (512 MiB write outside the events)",
-                   "io_dtype": "complex128", "conv": args.conv},
+                   "io_dtype": "complex128", "conv": args.conv, "accum": args.accum},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
                 "d2h_bytes_per_step": io_bytes, "steps": e2e_steps},
         "gpu_launches": int(launches),
@@ -394,6 +409,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "ntt_counts_per_transform": {"fwd": stats["fwd_ntts"] / B, "inv": stats["inv_ntts"] / B,
                                      "cached": stats["cached_ntts"]},
         "f1_cyclic": cyc,
+        "f2_image": img,
+        "f1_f2_cyclic_image": imgc,
     }
     print(json.dumps(line), flush=True)
 
@@ -408,7 +425,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--conv", default="padded", choices=["padded", "cyclic"],
                     help="Bluestein length: m >= 2n-1 (north star) or m = n (P:238-241)")
-    ap.add_argument("--no-extra", action="store_true", help="skip the f1_cyclic side measurement")
+    ap.add_argument("--accum", default="real", choices=["real", "image"],
+                    help="four real convolutions (the paper) or complex images (SURVEY f2)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the f1_cyclic / f2_image side measurements")
     args = ap.parse_args()
     cfg = workloads.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -59,6 +59,8 @@ typedef struct {
   uint32_t p0, p1;            /* NTT primes, < 2^31, p-1 divisible by m            */
   int32_t device;             /* CUDA device ordinal, -1 = current                 */
   int32_t conv_mode;          /* OZFFT_CONV_PADDED (0) or OZFFT_CONV_CYCLIC (1), below */
+  int32_t accum_mode;         /* OZFFT_ACCUM_REAL (0) or OZFFT_ACCUM_IMAGE (1), below  */
+  int32_t reserved;           /* must be 0                                          */
   uint64_t max_workspace_bytes;
 } ozfft_plan_desc;
 
@@ -73,6 +75,24 @@ typedef struct {
 #define OZFFT_CONV_PADDED 0
 #define OZFFT_CONV_CYCLIC 1
 
+/* How the complex convolution is assembled from exact modular convolutions
+ * (desc.accum_mode).
+ *  OZFFT_ACCUM_REAL: the paper's method -- Re x' and Im x' (and Re, Im of omega~*) are
+ *    split separately and the complex convolution is four real ones, rr - ii and ir + ri
+ *    (P:1010-1021), each with its own Alg.8 schedule: 12 forward + 40 inverse NTTs per
+ *    transform at (K, L) = (3, 3).
+ *  OZFFT_ACCUM_IMAGE: complex-image accumulation (beyond the paper).
+ *    Both parts of each split level share one exponent (Alg.6 with mu = max over both
+ *    parts), and the complex digit vectors are convolved through the two ring maps
+ *    a + i b -> a +- iota b mod p (iota^2 = -1; both paper primes are 1 mod 4): two image
+ *    convolutions per Alg.8 group instead of four real ones, re = (z+ + z-)/2 and
+ *    im = (z+ - z-)/(2 iota) per prime, then Garner.  alpha uses the bound
+ *    2 L n 4^alpha < P/2.  12 forward + 20 inverse NTTs at (3, 3).  Results differ from
+ *    OZFFT_ACCUM_REAL (different digits); the oracle's image mode is the reference.
+ *    Not available with ozfft_shard_partial (OZFFT_ERR_SHARD). */
+#define OZFFT_ACCUM_REAL 0
+#define OZFFT_ACCUM_IMAGE 1
+
 typedef struct {
   int64_t n, m, batch, chunk;   /* m: Bluestein cyclic length; chunk: transforms per pass */
   int32_t K, L, alpha, rho;     /* alpha = floor((log2(p0p1/2) - log2(L n))/2), rho = 53-alpha */
@@ -81,6 +101,8 @@ typedef struct {
   uint64_t workspace_bytes;     /* caller allocates; 256-byte aligned              */
   int32_t cached_ntts;          /* forward NTTs of omega~* slices done at bind */
   int32_t conv_mode;            /* as in the descriptor                                */
+  int32_t accum_mode;           /* as in the descriptor                                */
+  int32_t reserved;
 } ozfft_plan_info;
 
 typedef struct {

@@ -186,6 +186,16 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     while (m < 2 * desc.n - 1) m <<= 1;  // Bluestein length, N >= 2n-1
   }
   pl->conv_mode = desc.conv_mode;
+  if ((desc.accum_mode != OZFFT_ACCUM_REAL && desc.accum_mode != OZFFT_ACCUM_IMAGE) ||
+      desc.reserved != 0) {
+    delete pl;
+    return fail(OZFFT_ERR_INVALID_ARGUMENT, "accum_mode must be OZFFT_ACCUM_REAL or _IMAGE");
+  }
+  pl->image = desc.accum_mode == OZFFT_ACCUM_IMAGE ? 1 : 0;
+  if (pl->image && ((p0 & 3u) != 1u || (p1 & 3u) != 1u)) {
+    delete pl;
+    return fail(OZFFT_ERR_BAD_PRIMES, "OZFFT_ACCUM_IMAGE needs primes = 1 mod 4");
+  }
   pl->m = m;
   int logm = 0;
   while ((1ll << logm) < m) ++logm;
@@ -208,7 +218,8 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     if ((v == 10 || v == 11) && logm > 12 && logm - v <= 10) pl->logC = v;
   }
   pl->logR = logm - pl->logC;
-  pl->alpha = compute_alpha(desc.n, desc.L, p0, p1);
+  // image mode: a real output sums L n complex products (|Re| <= 2 4^alpha each)
+  pl->alpha = compute_alpha(pl->image ? 2 * desc.n : desc.n, desc.L, p0, p1);
   if (pl->alpha < 1) {
     delete pl;
     return fail(OZFFT_ERR_ALPHA, "alpha < 1");
@@ -246,6 +257,7 @@ ozfft_status ozfft_plan_get_info(const ozfft_plan* pl, ozfft_plan_info* info) {
   info->workspace_bytes = pl->workspace_bytes;
   info->cached_ntts = pl->bound ? 2 * (pl->kw[0] + pl->kw[1]) : 4 * pl->K;
   info->conv_mode = pl->conv_mode;
+  info->accum_mode = pl->image;
   return OZFFT_OK;
 }
 
@@ -445,8 +457,10 @@ ozfft_status ozfft_last_stats(const ozfft_plan* pl, ozfft_exec_stats* out, void*
       out->flags |= 1u;
       continue;
     }
-    out->fwd_ntts += 2 * (r[0] + r[1]);
-    for (int cv = 0; cv < 4; ++cv) out->groups += hsched[(b * 4 + cv) * sched_stride(K, L)];
+    out->fwd_ntts += 2 * (r[0] + r[1]);  // image mode: 2 images x k slices (r[0] = r[1] = k)
+    // image mode: one schedule (row 0), its groups run once per image
+    for (int cv = 0; cv < 4; ++cv)
+      out->groups += (pl->image ? 2 : 1) * hsched[(b * 4 + cv) * sched_stride(K, L)];
   }
   out->inv_ntts = 2 * out->groups;
   return OZFFT_OK;
@@ -463,6 +477,7 @@ ozfft_status ozfft_shard_partial(const ozfft_plan* pl, int shard, int nshards, c
   if (s) return s;
   if (nshards < 1 || 8 % nshards != 0 || shard < 0 || shard >= nshards)
     return fail(OZFFT_ERR_SHARD, "nshards must divide 8 and 0 <= shard < nshards");
+  if (pl->image) return fail(OZFFT_ERR_SHARD, "sharding is not available for OZFFT_ACCUM_IMAGE");
   const int per = 8 / nshards;
   uint32_t mask = 0;
   for (int u = shard * per; u < (shard + 1) * per; ++u) mask |= 1u << u;
@@ -488,6 +503,7 @@ ozfft_status ozfft_shard_finish(const ozfft_plan* pl, const void* residues_all, 
                                 int direction, void* stream) {
   ozfft_status s = check_exec(pl, residues_all, out, direction);
   if (s) return s;
+  if (pl->image) return fail(OZFFT_ERR_SHARD, "sharding is not available for OZFFT_ACCUM_IMAGE");
   return launch_finish_from_residues(*pl, reinterpret_cast<const uint32_t*>(residues_all),
                                      reinterpret_cast<double*>(out), direction, stream);
 }

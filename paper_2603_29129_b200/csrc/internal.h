@@ -32,6 +32,8 @@ struct Plan {
   uint32_t p[2] = {0, 0};
   int logm = 0, logC = 0, logR = 0;  // m = R * C
   int conv_mode = 0;                 // OZFFT_CONV_PADDED (m >= 2n-1) or OZFFT_CONV_CYCLIC (m = n)
+  int image = 0;                     // OZFFT_ACCUM_IMAGE: complex-image accumulation (f2)
+  uint32_t iota[2] = {0, 0};         // image mode: iota_q = g^((p_q - 1)/4), iota^2 = -1
   int device = 0;
   uint64_t max_ws = 0;
   // host tables (built at create)

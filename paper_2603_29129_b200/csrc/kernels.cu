@@ -115,6 +115,7 @@ struct SplitParams {
   int32_t* sched;         // [nb][4][sched_stride] (nullptr: no schedule)
   const int32_t* wsplit;  // kw[2], Ew[2][K] of omega~* (for the schedule)
   int L;
+  int shared;             // image mode (f2): one exponent per level for both parts
 };
 
 __device__ __forceinline__ void load_xprime(const SplitParams& P, int64_t b, int64_t j, double& hr,
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(256) k_split_max(SplitParams P, int level) {
     m1 = warp_max_u64(m1);
     if (lane == 0) {
       unsigned long long* dst = P.mu + b * 2 * P.K;
+      if (P.shared) m0 = m1 = m0 > m1 ? m0 : m1;  // mu = max over both parts (f2)
       if (m0) atomicMax(&dst[0 * P.K + level], m0);
       if (m1) atomicMax(&dst[1 * P.K + level], m1);
     }
@@ -277,7 +279,8 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
       sx[k] = P.alpha - E[a][k];                 // c = (u sigma)^-1 = 2^(alpha - E) (l.785)
       sy[k] = P.alpha - P.wsplit[2 + bw * P.K + k];
     }
-    alg8_schedule(bad ? 0 : kv[a], sx, kw, sy, P.K, P.L,
+    // image mode: one complex schedule in row 0 (both parts share E), rows 1-3 empty
+    alg8_schedule(bad || (P.shared && cv > 0) ? 0 : kv[a], sx, kw, sy, P.K, P.L,
                   P.sched + (b * 4 + cv) * sched_stride(P.K, P.L));
   }
   if (bad) return;
@@ -619,7 +622,16 @@ struct ColParams {
   const int32_t* stats;   // [nb][stats_stride]
   const int32_t* sched;   // [nb][4][sched_stride]
   uint32_t unit_mask;
+  int image;              // f2: the forward vectors are the digit images D_re +- iota D_im
+  uint2 io[2][2];         // [q][image] Shoup pair of iota_q (image 0) or p_q - iota_q (1)
 };
+
+// Digit image a = 0: D_re + iota D_im, a = 1: D_re - iota D_im (mod p), canonical (f2).
+__device__ __forceinline__ uint32_t digit_image(int32_t dre, int32_t dim, uint2 io, uint32_t p) {
+  const uint32_t r = dre >= 0 ? (uint32_t)dre : (uint32_t)dre + p;
+  const uint32_t i = dim >= 0 ? (uint32_t)dim : (uint32_t)dim + p;
+  return add_mod(r, mul_shoup(i, io, p), p);
+}
 
 // Elements per thread per round (log2) of the row and column sub-transforms: 32 for the
 // one-warp rows of C = 2^10 (two-pass plans) and for columns of R >= 2^9, else 16.
@@ -664,7 +676,7 @@ __host__ __device__ constexpr int col_s1(int logR) {
 // Forward column pass: global DIF stages len = m .. 2C on columns of the R x C view.
 // One CTA per (transform, prime, part, column block) loops over the part's slices; the
 // next slice's column tile is loaded while the current one is transformed.
-template <int LOGR, int LOGC>
+template <int LOGR, int LOGC, bool IMG>
 __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(ColParams P) {
   extern __shared__ uint32_t smem[];
   constexpr int LOGCB = col_log_cb(LOGR, LOGC);
@@ -698,12 +710,23 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(C
   stage_col_tw0<S1, Cb>(tw0, T, C, cb << LOGCB);
   __syncthreads();
   uint32_t nxt[E];
+  [[maybe_unused]] const uint2 io = P.io[q][a];
   auto fetch = [&](int s) {
-    const int32_t* D = P.digits + ((b * 2 + a) * P.K + s) * P.in_len + col;
+    if constexpr (IMG) {  // image a of slice s from both parts' digits (f2; P.image)
+      const int32_t* Dr = P.digits + ((b * 2 + 0) * P.K + s) * P.in_len + col;
+      const int32_t* Di = P.digits + ((b * 2 + 1) * P.K + s) * P.in_len + col;
 #pragma unroll
-    for (int i = 0; i < CNT; ++i) {
-      const uint32_t e = round_elem<LOGR, false, 0, LOGE>(tv, i);
-      nxt[i] = e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u;
+      for (int i = 0; i < CNT; ++i) {
+        const uint32_t e = round_elem<LOGR, false, 0, LOGE>(tv, i);
+        nxt[i] = e * C < lim ? digit_image(__ldg(&Dr[e * C]), __ldg(&Di[e * C]), io, p) : 0u;
+      }
+    } else {
+      const int32_t* D = P.digits + ((b * 2 + a) * P.K + s) * P.in_len + col;
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) {
+        const uint32_t e = round_elem<LOGR, false, 0, LOGE>(tv, i);
+        nxt[i] = e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u;
+      }
     }
   };
   fetch(0);
@@ -793,6 +816,9 @@ struct RowParams {
   int fwd_only;           // 1: write the forward spectra (internal order) to Xout, stop
   uint32_t* Xout;         // fwd_only or tap: [nb][2 q][2 a][K][m]
   uint32_t* Zout;         // tap: [nb][2 q][4][K*K][m] (internal order, W m^{-1} scaled)
+  int image;              // f2: a = image index; one "conv" (the image) per CTA, schedule
+                          // row 0, W rows of image a; digits imaged on load (R == 1)
+  uint2 io[2][2];         // [q][image] Shoup pair of iota_q / p_q - iota_q
 };
 
 #ifndef OZ_ROW_DBUF
@@ -872,9 +898,10 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   const int32_t* st = P.stats + b * stats_stride(K);
   const int ka = st[a];
   // convolutions using part a: a = 0 -> rr (0), ri (3); a = 1 -> ii (1), ir (2)
-  const int cv0 = a == 0 ? 0 : 1, cv1 = a == 0 ? 3 : 2;
-  const bool want0 = (P.unit_mask >> (cv0 * 2 + q)) & 1u;
-  const bool want1 = (P.unit_mask >> (cv1 * 2 + q)) & 1u;
+  // (image mode: the CTA's one "conv" is its image a)
+  const int cv0 = P.image ? a : (a == 0 ? 0 : 1), cv1 = a == 0 ? 3 : 2;
+  const bool want0 = P.image || ((P.unit_mask >> (cv0 * 2 + q)) & 1u);
+  const bool want1 = !P.image && ((P.unit_mask >> (cv1 * 2 + q)) & 1u);
   if (!P.fwd_only && !want0 && !want1) return;
   if (ka == 0 && !P.fwd_only) return;  // no slices: the schedule has no groups here
   uint32_t* Xs = smem;               // [K][C] forward spectra rows (row_perm order)
@@ -890,7 +917,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   for (int ci = tv; ci < 2 && !P.fwd_only; ci += blockDim.x) {  // blockDim may be 1 (C < 32)
     const int cv = ci ? cv1 : cv0;
     const bool want = ci ? want1 : want0;
-    const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
+    const int32_t* srow = P.sched + (b * 4 + (P.image ? 0 : cv)) * sched_stride(K, L);
     const int ng = want ? srow[0] : 0;
     s_ng[ci] = ng;
     for (int g = 0; g < ng; ++g) {
@@ -923,10 +950,22 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
     } else {
       const int32_t* D = P.digits + ((b * 2 + a) * K + s) * P.in_len;
       const uint32_t in_len = (uint32_t)P.in_len;
-      sub_ntt<LOGC, false, 1, LOGE, true>(
-          tv, wk, 0u, 1u, Tf, p,
-          [&](int, uint32_t e) -> uint32_t { return e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
-          store_x);
+      if (P.image) {  // digit image a of slice s (f2)
+        const int32_t* Dr = P.digits + ((b * 2 + 0) * K + s) * P.in_len;
+        const int32_t* Di = P.digits + ((b * 2 + 1) * K + s) * P.in_len;
+        const uint2 io = P.io[q][a];
+        sub_ntt<LOGC, false, 1, LOGE, true>(
+            tv, wk, 0u, 1u, Tf, p,
+            [&](int, uint32_t e) -> uint32_t {
+              return e < in_len ? digit_image(__ldg(&Dr[e]), __ldg(&Di[e]), io, p) : 0u;
+            },
+            store_x);
+      } else {
+        sub_ntt<LOGC, false, 1, LOGE, true>(
+            tv, wk, 0u, 1u, Tf, p,
+            [&](int, uint32_t e) -> uint32_t { return e < in_len ? lift(__ldg(&D[e]), p) : 0u; },
+            store_x);
+      }
     }
   }
   if (P.fwd_only) return;
@@ -945,7 +984,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   // products X * W~ (W~ = W m^{-1} 2^32, sums < 3 p^2 < 2^64), one Montgomery reduction each
   auto pointwise = [&](int ci, int g, uint32_t (&z)[E]) {
     const int cv = ci ? cv1 : cv0;
-    const uint32_t* Wb = P.W + (size_t)(q * 2 + conv_b(cv)) * K * m + rowoff;
+    const uint32_t* Wb = P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff;
     const uint32_t* tg = tab + (ci * G + g) * tstride;
     const int np = (int)tg[0];
 #pragma unroll
@@ -1017,7 +1056,17 @@ struct FinishParams {
   double2* out;             // [nb][n]
   int direction;
   int64_t* crt_tap;         // [nb][4][K*K][n] or null
+  // image mode (f2): per prime q the Shoup pairs of 2^-1 and (2 iota_q)^-1 mod p_q
+  uint2 inv2[2], inv2i[2];
 };
+
+// f2: (re, im) residues of a complex integer from its two images z+ = re + iota im and
+// z- = re - iota im (mod p): re = (z+ + z-)/2, im = (z+ - z-)/(2 iota).
+__device__ __forceinline__ void image_pair(uint32_t zp, uint32_t zm, uint2 inv2, uint2 inv2i,
+                                           uint32_t p, uint32_t& re, uint32_t& im) {
+  re = mul_shoup(add_mod(zp, zm, p), inv2, p);
+  im = mul_shoup(sub_mod(zp, zm, p), inv2i, p);
+}
 
 // Garner, two primes (Alg.8 l.974): Z' = z0 + p0 ((z1 - z0) p0^{-1} mod p1)
 // in [0, p0 p1), then the symmetric representative in [-p0p1/2, p0p1/2) (
@@ -1099,6 +1148,67 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
   dd_add(a1h, a1l, -a2h, -a2l, ore, tmp);
   dd_mul_d(yrh, yrl, w.y, a1h, a1l);
   dd_mul_d(yih, yil, w.x, a2h, a2l);
+  dd_add(a1h, a1l, a2h, a2l, oim, tmp);
+  if (P.direction > 0) {
+    const double dn = (double)P.n;
+    ore = __ddiv_rn(ore, dn);
+    oim = __ddiv_rn(-oim, dn);
+  }
+  o.x = ore;
+  o.y = oim;
+  P.out[b * P.n + j] = o;
+}
+
+// f2, single-pass plans: the residues of both images of each group -> (re, im) per prime
+// -> Garner -> DD sums in flush order -> post-chirp (as k_crt_finish; res [nb][img][q][g][n]).
+__global__ void __launch_bounds__(256, 4) k_crt_finish_img(FinishParams P) {
+  const int64_t b = blockIdx.y;
+  const int K = P.K, L = P.L, G = K * K;
+  __shared__ int s_ng;
+  __shared__ double s_sc[kMaxK * kMaxK];
+  if (threadIdx.x == 0) {
+    const int32_t* srow = P.sched + (b * 4) * sched_stride(K, L);  // the complex schedule
+    s_ng = srow[0];
+    for (int g = 0; g < s_ng; ++g) s_sc[g] = scalbn(1.0, -srow[1 + g * (2 + 2 * L)]);
+  }
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.n) return;
+  double2 o;
+  if (P.stats[b * stats_stride(K) + 2 + 2 * K] & 1) {
+    o.x = __longlong_as_double(0x7FF8000000000000ll);
+    o.y = o.x;
+    P.out[b * P.n + j] = o;
+    return;
+  }
+  double sh[2] = {0.0, 0.0}, sl[2] = {0.0, 0.0};
+  const int ng = s_ng;
+  for (int g = 0; g < ng; ++g) {
+    uint32_t zr[2], zi[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t p = q ? P.p1 : P.p0;
+      const uint32_t zp = __ldcs(&P.res[(((b * 4 + 0) * 2 + q) * G + g) * P.n + j]);
+      const uint32_t zm = __ldcs(&P.res[(((b * 4 + 1) * 2 + q) * G + g) * P.n + j]);
+      image_pair(zp, zm, P.inv2[q], P.inv2i[q], p, zr[q], zi[q]);
+    }
+    const double sc = s_sc[g];
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const long long Z = part ? garner2(zi[0], zi[1], P) : garner2(zr[0], zr[1], P);
+      if (P.crt_tap) P.crt_tap[((b * 4 + part) * G + g) * P.n + j] = Z;
+      const double h = __ll2double_rn(Z);
+      const double l = __ll2double_rn(Z - __double2ll_rz(h));
+      dd_add(sh[part], sl[part], __dmul_rn(h, sc), __dmul_rn(l, sc), sh[part], sl[part]);
+    }
+  }
+  const double2 w = P.chirp[j];
+  double a1h, a1l, a2h, a2l, ore, oim, tmp;
+  dd_mul_d(sh[0], sl[0], w.x, a1h, a1l);
+  dd_mul_d(sh[1], sl[1], w.y, a2h, a2l);
+  dd_add(a1h, a1l, -a2h, -a2l, ore, tmp);
+  dd_mul_d(sh[0], sl[0], w.y, a1h, a1l);
+  dd_mul_d(sh[1], sl[1], w.x, a2h, a2l);
   dd_add(a1h, a1l, a2h, a2l, oim, tmp);
   if (P.direction > 0) {
     const double dn = (double)P.n;
@@ -1241,13 +1351,130 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   }
 }
 
+// f2 (image mode): the fused inverse column pass + CRT for the complex convolution.  CTA
+// = (transform, column block); per Alg.8 group the four tiles (image +, p0), (image -, p0),
+// (image +, p1), (image -, p1) are transformed in turn (next tile prefetched); each prime's
+// image pair gives (re, im) residues, the primes' pairs give Re and Im by Garner, and the
+// DD sums of Re 2^-c and Im 2^-c in flush order go to S[b][0] and S[b][1].
+template <int LOGR, int LOGC, bool PRUNE>
+__global__ void __launch_bounds__(256, 2) k_col_inv_crt_img(ColCrtParams P) {
+  extern __shared__ uint32_t smem[];
+  constexpr int LOGCB = col_log_cb(LOGR, LOGC);
+  constexpr int LOGE = col_loge(LOGR);
+  constexpr int E = 1 << LOGE;
+  constexpr int Cb = 1 << LOGCB;
+  constexpr uint32_t C = 1u << LOGC;
+  constexpr uint32_t m = 1u << (LOGR + LOGC);
+  constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
+  constexpr int CNT = RoundT<LOGR, true, 0, LOGE>::cnt;
+  constexpr int NR = RoundT<LOGR, true, 0, LOGE>::nr;
+  constexpr int SL = RoundT<LOGR, true, NR - 1, LOGE>::S;
+  constexpr int NH = RoundT<LOGR, true, NR - 1, LOGE>::cnt / (PRUNE ? 2 : 1);
+  auto needed = [](int i) { return !PRUNE || (i & ((1 << SL) - 1)) < (1 << (SL - 1)); };
+  auto hslot = [](int i) {
+    return PRUNE ? ((i >> SL) << (SL - 1)) + (i & ((1 << (SL - 1)) - 1)) : i;
+  };
+  constexpr int THREADS = RoundT<LOGR, true, 0, LOGE>::Tv << LOGCB;
+  constexpr int CNTL = RoundT<LOGR, true, NR - 1, LOGE>::cnt;
+  const int G = P.K * P.K;
+  const uint32_t cb = blockIdx.x % ncb;
+  const int64_t b = blockIdx.x / ncb;
+  const int tid = threadIdx.x;
+  const int c = tid & (Cb - 1);
+  const int tv = tid >> LOGCB;
+  const uint32_t col = (cb << LOGCB) + c;
+  __shared__ double s_sc[kMaxK * kMaxK];
+  const int32_t* srow = P.sched + (b * 4) * sched_stride(P.K, P.L);  // the complex schedule
+  const int ng = srow[0];
+  for (int g = tid; g < ng; g += blockDim.x) s_sc[g] = scalbn(1.0, -srow[1 + g * (2 + 2 * P.L)]);
+  constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;
+  double2* Sacc = reinterpret_cast<double2*>(smem + TILE + (TILE & 1));  // [2][NH][THREADS]
+#pragma unroll
+  for (int i = 0; i < 2 * NH; ++i) Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
+  const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
+  uint32_t nxt[E];
+  auto fetch = [&](int t) {  // tile t = 4 g + 2 q + image
+    const int g = t >> 2, q = (t >> 1) & 1, img = t & 1;
+    const uint32_t* in = P.G + (((b * 2 + q) * 4 + img) * G + g) * (int64_t)m + col;
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0, LOGE>(tv, i) * C]);
+  };
+  if (ng > 0) fetch(0);
+  __syncthreads();  // s_sc ready
+  uint32_t ra[NH], zr0[NH], zi0[NH];
+  for (int t = 0; t < 4 * ng; ++t) {
+    const int g = t >> 2, q = (t >> 1) & 1, img = t & 1;
+    uint32_t cur[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) cur[i] = nxt[i];
+    if (t + 1 < 4 * ng) fetch(t + 1);
+    if (t > 0) __syncthreads();  // smem tile free
+    const uint32_t p = q ? P.F.p1 : P.F.p0;
+    const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
+    uint32_t rr[NH];
+    sub_ntt<LOGR, true, Cb, LOGE>(tv, smem + c, col, C, T, p,
+                            [&](int i, uint32_t) -> uint32_t { return cur[i]; },
+                            [&](int i, uint32_t, uint32_t val) {
+                              if (needed(i)) rr[hslot(i)] = val;
+                            });
+    if (P.res_tap) {
+      uint32_t* rt = P.res_tap + (((b * 4 + img) * 2 + q) * G + g) * P.n + col;
+#pragma unroll
+      for (int i = 0; i < CNTL; ++i) {
+        if (!needed(i)) continue;
+        const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
+        if (e * C < lim) rt[e * C] = rr[hslot(i)];
+      }
+    }
+    if (img == 0) {
+#pragma unroll
+      for (int i = 0; i < NH; ++i) ra[i] = rr[i];
+    } else if (q == 0) {
+#pragma unroll
+      for (int i = 0; i < NH; ++i) image_pair(ra[i], rr[i], P.F.inv2[0], P.F.inv2i[0], p, zr0[i], zi0[i]);
+    } else {
+      const double sc = s_sc[g];
+#pragma unroll
+      for (int i = 0; i < CNTL; ++i) {
+        if (!needed(i)) continue;
+        const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
+        const int h = hslot(i);
+        if (e * C < lim) {
+          uint32_t zr1, zi1;
+          image_pair(ra[h], rr[h], P.F.inv2[1], P.F.inv2i[1], p, zr1, zi1);
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            const long long Z = part ? garner2(zi0[h], zi1, P.F) : garner2(zr0[h], zr1, P.F);
+            if (P.crt_tap) P.crt_tap[((b * 4 + part) * G + g) * P.n + col + e * C] = Z;
+            const double hi = __ll2double_rn(Z);
+            const double lo = __ll2double_rn(Z - __double2ll_rz(hi));
+            double2 a = Sacc[(part * NH + h) * THREADS + tid];
+            dd_add(a.x, a.y, __dmul_rn(hi, sc), __dmul_rn(lo, sc), a.x, a.y);
+            Sacc[(part * NH + h) * THREADS + tid] = a;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int part = 0; part < 2; ++part) {
+    double2* So = P.S + (b * 4 + part) * P.n + col;
+#pragma unroll
+    for (int i = 0; i < CNTL; ++i) {
+      if (!needed(i)) continue;
+      const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
+      if (e * C < lim) So[e * C] = Sacc[(part * NH + hslot(i)) * THREADS + tid];
+    }
+  }
+}
+
 // y' = (S_rr - S_ii) + i (S_ir + S_ri), post-chirp y = y' (.) omega
 // (Alg.4 l.480-484), fp64 output; inverse direction: conj and RN division by n (O10).
 __global__ void __launch_bounds__(256) k_finish_dd(const double2* __restrict__ S,
                                                    const int32_t* __restrict__ stats, int K,
                                                    const double2* __restrict__ chirp,
                                                    double2* __restrict__ out, int64_t n,
-                                                   int direction) {
+                                                   int direction, int image) {
   const int64_t b = blockIdx.y;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -1258,11 +1485,16 @@ __global__ void __launch_bounds__(256) k_finish_dd(const double2* __restrict__ S
     out[b * n + j] = o;
     return;
   }
-  const double2 rr = __ldcs(&S[(b * 4 + 0) * n + j]), ii = __ldcs(&S[(b * 4 + 1) * n + j]);
-  const double2 ir = __ldcs(&S[(b * 4 + 2) * n + j]), ri = __ldcs(&S[(b * 4 + 3) * n + j]);
   double yrh, yrl, yih, yil;
-  dd_add(rr.x, rr.y, -ii.x, -ii.y, yrh, yrl);
-  dd_add(ir.x, ir.y, ri.x, ri.y, yih, yil);
+  if (image) {  // f2: the DD sums are Re y' and Im y' themselves
+    const double2 re = __ldcs(&S[(b * 4 + 0) * n + j]), im = __ldcs(&S[(b * 4 + 1) * n + j]);
+    yrh = re.x; yrl = re.y; yih = im.x; yil = im.y;
+  } else {
+    const double2 rr = __ldcs(&S[(b * 4 + 0) * n + j]), ii = __ldcs(&S[(b * 4 + 1) * n + j]);
+    const double2 ir = __ldcs(&S[(b * 4 + 2) * n + j]), ri = __ldcs(&S[(b * 4 + 3) * n + j]);
+    dd_add(rr.x, rr.y, -ii.x, -ii.y, yrh, yrl);
+    dd_add(ir.x, ir.y, ri.x, ri.y, yih, yil);
+  }
   const double2 w = chirp[j];
   double a1h, a1l, a2h, a2l, ore, oim, tmp;
   dd_mul_d(yrh, yrl, w.x, a1h, a1l);
@@ -1288,6 +1520,23 @@ static void fill_crt_consts(const Plan& pl, FinishParams& FP) {
   FP.p0inv_sh = (uint32_t)(((uint64_t)pl.p0inv_mod_p1 << 32) / pl.p[1]);
   FP.P = (unsigned long long)pl.p[0] * pl.p[1];
   FP.halfP = (FP.P - 1) / 2;
+  for (int q = 0; q < 2; ++q) {  // f2: 2^-1 and (2 iota)^-1 = 2^-1 (-iota) (iota^-1 = -iota)
+    const uint64_t p = pl.p[q];
+    const uint64_t i2 = (p + 1) / 2;
+    const uint64_t i2i = pl.image ? i2 * (p - pl.iota[q]) % p : 0;
+    FP.inv2[q] = make_uint2((uint32_t)i2, (uint32_t)((i2 << 32) / p));
+    FP.inv2i[q] = make_uint2((uint32_t)i2i, (uint32_t)((i2i << 32) / p));
+  }
+}
+
+// f2: Shoup pairs of iota_q (image 0) and p_q - iota_q (image 1)
+static void fill_iota(const Plan& pl, uint2 (&io)[2][2]) {
+  for (int q = 0; q < 2; ++q)
+    for (int img = 0; img < 2; ++img) {
+      const uint64_t p = pl.p[q];
+      const uint64_t w = pl.image ? (img ? p - pl.iota[q] : pl.iota[q]) : 0;
+      io[q][img] = make_uint2((uint32_t)w, (uint32_t)((w << 32) / p));
+    }
 }
 
 // ============================================================== small utility kernels
@@ -1409,8 +1658,13 @@ template <int LOGR>
 static void launch_col_fwd_r(int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
                              const ColParams& CP) {
   dispatch_log<10, 12>(logC, [&](auto J) {
-    set_smem(k_col_fwd<LOGR, J.value>, c.col_fwd_smem);
-    k_col_fwd<LOGR, J.value><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
+    if (CP.image) {
+      set_smem(k_col_fwd<LOGR, J.value, true>, c.col_fwd_smem);
+      k_col_fwd<LOGR, J.value, true><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
+    } else {
+      set_smem(k_col_fwd<LOGR, J.value, false>, c.col_fwd_smem);
+      k_col_fwd<LOGR, J.value, false><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
+    }
   });
 }
 template <int LOGR>
@@ -1461,6 +1715,8 @@ static ozfft_status launch_forward_only(const Plan& pl, const int32_t* digits, i
     CP.nb = nb; CP.K = pl.K; CP.L = pl.L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
     CP.tw = tw; CP.digits = digits; CP.in_len = in_len; CP.Y = Y; CP.stats = stats;
     CP.unit_mask = 0xFF;
+    CP.image = pl.image;
+    fill_iota(pl, CP.io);
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
     launch_col_fwd(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
   }
@@ -1468,6 +1724,8 @@ static ozfft_status launch_forward_only(const Plan& pl, const int32_t* digits, i
   RP.logm = pl.logm; RP.logC = pl.logC; RP.logR = pl.logR; RP.nb = nb; RP.K = pl.K; RP.L = pl.L;
   RP.p[0] = pl.p[0]; RP.p[1] = pl.p[1]; RP.tw = tw; RP.digits = digits; RP.in_len = in_len;
   RP.Y = Y; RP.stats = stats; RP.unit_mask = 0xFF; RP.fwd_only = 1; RP.Xout = Xout;
+  RP.image = pl.image;
+  fill_iota(pl, RP.io);
   dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
   launch_row(pl.logC, pl.logR, grid, c, st, RP);
   return cuda_check("forward-only NTT");
@@ -1503,6 +1761,7 @@ ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
   SP.stats = stats;
   SP.sched = nullptr;
   SP.L = pl.L;
+  SP.shared = pl.image;
   ozfft_status s = launch_split(pl, SP, 1, st);
   if (!s) s = launch_forward_only(pl, digits, m, stats, Y, X, 1, st);
   int32_t hstats[4 + 2 * kMaxK];
@@ -1578,6 +1837,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   SP.sched = sched;
   SP.wsplit = wsplit;
   SP.L = L;
+  SP.shared = pl.image;
   ozfft_status s = launch_split(pl, SP, nb, st);
   if (s) return s;
   const NttLaunch c = ntt_launch_cfg(pl);
@@ -1595,6 +1855,8 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.nb = nb; CP.K = K; CP.L = L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
     CP.tw = tw; CP.digits = SP.digits; CP.in_len = n; CP.Y = Y; CP.stats = stats;
     CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n; CP.unit_mask = A.unit_mask;
+    CP.image = pl.image;
+    fill_iota(pl, CP.io);
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
     prof_mark(pl, OZFFT_STAGE_COL_FWD, true, st);
     launch_col_fwd(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
@@ -1608,6 +1870,8 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   RP.p[0] = pl.p[0]; RP.p[1] = pl.p[1]; RP.tw = tw; RP.digits = SP.digits; RP.in_len = n;
   RP.Y = Y; RP.W = W; RP.pinv[0] = pl.pinv[0]; RP.pinv[1] = pl.pinv[1]; RP.G = Gb; RP.res = res; RP.n = n; RP.stats = stats; RP.sched = sched;
   RP.unit_mask = A.unit_mask; RP.fwd_only = 0; RP.Xout = Xtap; RP.Zout = Ztap;
+  RP.image = pl.image;
+  fill_iota(pl, RP.io);
   {
     dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
     prof_mark(pl, OZFFT_STAGE_ROW_FUSED, true, st);
@@ -1631,12 +1895,18 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     const size_t tile = ((1ull << pl.logR) + ((1ull << pl.logR) >> cle) + 1) * (1ull << c.logCb);
     const bool prune = 2 * n <= m;  // padded plans; cyclic plans (m = n) need every row
     const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / (prune ? 2 : 1);
-    const size_t smem = (tile + (tile & 1)) * 4 + (size_t)nh * c.col_threads * 16;
-    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
+    const size_t smem = (tile + (tile & 1)) * 4 + (size_t)nh * c.col_threads * 16 * (pl.image ? 2 : 1);
+    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * (pl.image ? 1 : 4);
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
     dispatch_log<1, 10>(pl.logR, [&](auto I) {
       dispatch_log<10, 12>(pl.logC, [&](auto J) {
-        if (prune) {
+        if (pl.image && prune) {
+          set_smem(k_col_inv_crt_img<I.value, J.value, true>, smem);
+          k_col_inv_crt_img<I.value, J.value, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+        } else if (pl.image) {
+          set_smem(k_col_inv_crt_img<I.value, J.value, false>, smem);
+          k_col_inv_crt_img<I.value, J.value, false><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+        } else if (prune) {
           set_smem(k_col_inv_crt<I.value, J.value, true>, smem);
           k_col_inv_crt<I.value, J.value, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
         } else {
@@ -1652,7 +1922,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)nb);
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
     k_finish_dd<<<grid, 256, 0, st>>>(XP.S, stats, K, chirp, reinterpret_cast<double2*>(A.out), n,
-                                      A.direction);
+                                      A.direction, pl.image);
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
     count_launches(1);
     s = cuda_check("k_finish_dd");
@@ -1679,7 +1949,10 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     FP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)nb);
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
-    k_crt_finish<<<grid, 256, 0, st>>>(FP);
+    if (pl.image)
+      k_crt_finish_img<<<grid, 256, 0, st>>>(FP);
+    else
+      k_crt_finish<<<grid, 256, 0, st>>>(FP);
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
     count_launches(1);
     s = cuda_check("k_crt_finish");

@@ -106,6 +106,9 @@ ozfft_status build_plan_tables(Plan& pl) {
     }
   }
   pl.p0inv_mod_p1 = pow_mod(pl.p[0] % pl.p[1], pl.p[1] - 2, pl.p[1]);
+  // image mode (f2): iota = g^((p-1)/4), a square root of -1 mod p
+  if (pl.image)
+    for (int q = 0; q < 2; ++q) pl.iota[q] = pow_mod(generator(pl.p[q]), (pl.p[q] - 1) / 4, pl.p[q]);
   return OZFFT_OK;
 }
 
