@@ -269,3 +269,28 @@ class Plan:
         y = np.empty_like(x)
         used = lib().orc_execute_batch(self._h, B, _p(x), _p(y), 1 if inverse else -1, nthreads)
         return y, used
+
+
+# --------------------------------------------------------------------------- Fig. 1 alpha
+def alpha_formulas(n: int, u_log2_inv: int = 24, p0: int = P0, p1: int = P1) -> dict:
+    """The four split widths compared in the paper's Fig. 1, evaluated with
+    mpmath at 100 digits in the precision u = 2^-u_log2_inv (single precision: 24):
+      ozaki   eq:ozaki-scheme-alpha          floor((log2 u^-1 - log2 n) / 2)
+      fft     eq:ozaki-scheme-conv-fft-alpha floor(-(1 + log2 n + log2{(1+u)^3n
+              (1+u sqrt5)^(3n+1) (1+u/sqrt2)^3n - 1}) / 2)
+      ntt     eq:ozaki-scheme-conv-ntt-alpha floor((log2(p/2) - log2 n) / 2), p = p0
+      crt     eq:ozaki-scheme-conv-ntt-crt-alpha floor((log2(p0 p1/2) - log2 n) / 2)
+    (TEST INFRASTRUCTURE: tools/sweep.py and tests only.)"""
+    import mpmath
+    mpmath.mp.dps = 100
+    u = mpmath.mpf(2) ** -u_log2_inv
+    N = mpmath.mpf(n)
+    lg = lambda v: mpmath.log(v, 2)  # noqa: E731
+    growth = (1 + u) ** (3 * N) * (1 + u * mpmath.sqrt(5)) ** (3 * N + 1) * \
+        (1 + u / mpmath.sqrt(2)) ** (3 * N) - 1
+    return {
+        "ozaki": int(mpmath.floor((lg(1 / u) - lg(N)) / 2)),
+        "fft": int(mpmath.floor(-(1 + lg(N) + lg(growth)) / 2)),
+        "ntt": int(mpmath.floor((lg(mpmath.mpf(p0) / 2) - lg(N)) / 2)),
+        "crt": int(mpmath.floor((lg(mpmath.mpf(p0) * p1 / 2) - lg(N)) / 2)),
+    }

@@ -1,0 +1,55 @@
+"""NTT-count laws of the paper's (K, L) sweep on the GPU path.
+
+Per transform (Appendix B of SURVEY):
+  forward  = 2 (k_re + k_im)                     (slices of Re x', Im x' under 2 primes)
+  cached   = 2 (kw_re + kw_im)                   (omega~* slices, precomputed)
+  inverse  = 2 sum_conv groups;  L = 1: groups = k_a k_b per real conv (all pairs)
+Totals printed in the paper at phi = 0 and 1 for every n: 96 at (K, L) = (3, 1)
+and 64 = 24K - 8 at (3, 3).  Outputs are checked bit-exact against the oracle for
+the same (K, L) on one transform per point.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def oz():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_29129_b200 as oz
+    oz.load_library()
+    return oz
+
+
+@pytest.mark.parametrize("phi", [0.0, 1.0, 4.0])
+@pytest.mark.parametrize("n", [1024, 4096])
+@pytest.mark.parametrize("K,L", [(8, 1), (1, 1), (2, 1), (3, 1), (3, 3)])
+def test_count_laws(oz, phi, n, K, L):
+    B = 3
+    x = workloads.phi_input(n, phi, seed=n + int(phi), batch=B)
+    plan = oz.Plan(n, B, K=K, L=L)
+    xt = torch.from_numpy(x).cuda()
+    y, t = plan.execute_taps(xt)
+    st = plan.stats()
+    kv = t["kv"].cpu().numpy()
+    kw = st["k"][2:]
+    assert st["fwd_ntts"] == 2 * int(kv.sum())
+    assert st["cached_ntts"] == 2 * sum(kw)
+    groups = sum(int(t["sched"][b, cv, 0]) for b in range(B) for cv in range(4))
+    assert st["inv_ntts"] == 2 * groups
+    if L == 1:
+        pairs = sum(int(kv[b, a]) * kw[c] for b in range(B) for a, c in ((0, 0), (1, 1), (1, 0), (0, 1)))
+        assert groups == pairs
+    total = (st["fwd_ntts"] + st["inv_ntts"]) / B + st["cached_ntts"]
+    if phi < 2 and (K, L) == (3, 1):
+        assert total == 96
+    if phi < 2 and (K, L) == (3, 3):
+        assert total == 64  # P:1164, 24K - 8
+    yo = O.Plan(n, K, L).execute(x[0])
+    assert np.array_equal(y[0].cpu().numpy(), yo)
