@@ -1599,9 +1599,12 @@ static int col_threads(int logR, int logCb) {
   const int Tv = logR >= le ? (1 << (logR - le)) : 1;
   return Tv << logCb;
 }
+#ifndef OZ_SPLIT_EPT
+#define OZ_SPLIT_EPT 8  // elements per thread of the split kernels' grid-stride loops
+#endif
 static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cudaStream_t st) {
   const int threads = 256;
-  int64_t blocks_per = (SP.len + threads * 4 - 1) / (threads * 4);
+  int64_t blocks_per = (SP.len + threads * OZ_SPLIT_EPT - 1) / (threads * OZ_SPLIT_EPT);
   if (blocks_per < 1) blocks_per = 1;
   if (blocks_per > 65535) blocks_per = 65535;
   dim3 grid((unsigned)blocks_per, (unsigned)nb);
