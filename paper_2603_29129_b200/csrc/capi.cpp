@@ -215,7 +215,7 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
   pl->logC = logm <= 12 ? logm : std::min(12, std::max(11, logm - 8));
   if (const char* t = std::getenv("OZFFT_TUNE_LOGC")) {  // tuning knob (tools/, not the hot path)
     const int v = std::atoi(t);
-    if ((v == 10 || v == 11) && logm > 12 && logm - v <= 10) pl->logC = v;
+    if (v >= 10 && v <= 12 && logm > v && logm - v <= 10) pl->logC = v;
   }
   pl->logR = logm - pl->logC;
   // image mode: a real output sums L n complex products (|Re| <= 2 4^alpha each)
