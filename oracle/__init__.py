@@ -73,6 +73,22 @@ def lib():
                                    C.c_int, C.c_void_p]
         L.orc_plan_create.restype = C.c_void_p
         L.orc_plan_create.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint32, C.c_uint32]
+        L.orc_plan_create_ts.restype = C.c_void_p
+        L.orc_plan_create_ts.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint32, C.c_uint32,
+                                         C.c_int, C.c_int, C.c_int]
+        for fn in ("orc_ts_add", "orc_ts_mul"):
+            getattr(L, fn).restype = TS
+            getattr(L, fn).argtypes = [TS, TS]
+        L.orc_ts_neg.restype = TS
+        L.orc_ts_neg.argtypes = [TS]
+        L.orc_ts_from_double.restype = TS
+        L.orc_ts_from_double.argtypes = [C.c_double]
+        L.orc_ts_from_int64.restype = TS
+        L.orc_ts_from_int64.argtypes = [C.c_int64]
+        L.orc_ts_to_double.restype = C.c_double
+        L.orc_ts_to_double.argtypes = [TS]
+        L.orc_split_ts.restype = C.c_int
+        L.orc_split_ts.argtypes = [C.c_int64, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_plan_create_ex.restype = C.c_void_p
         L.orc_plan_create_ex.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint32, C.c_uint32,
                                          C.c_int, C.c_int]
@@ -100,6 +116,14 @@ def lib():
         L.orc_dft_f128.argtypes = [C.c_int64, C.c_void_p, C.c_int, C.c_void_p, C.c_int64,
                                    C.c_void_p]
     return _lib
+
+
+class TS(C.Structure):
+    """Triple-single number x0 + x1 + x2 (fp32 words), as orc_ts."""
+    _fields_ = [("x0", C.c_float), ("x1", C.c_float), ("x2", C.c_float)]
+
+    def words(self):
+        return (self.x0, self.x1, self.x2)
 
 
 class Taps(C.Structure):
@@ -214,11 +238,14 @@ class Plan:
     """Oracle plan: chirp, omega~* split, and the cached W spectra."""
 
     def __init__(self, n: int, K: int = 3, L: int = 3, p0: int = P0, p1: int = P1,
-                 cyclic: bool = False, image: bool = False):
+                 cyclic: bool = False, image: bool = False, ts: bool = False):
         """cyclic: m = n for power-of-two n instead of m >= 2n-1.
-        image: complex-image accumulation (orc_execute_image)."""
+        image: complex-image accumulation (orc_execute_image).
+        ts: triple-single working precision for a1, a2, a7."""
         self.n, self.K, self.L, self.p, self.cyclic, self.image = n, K, L, (p0, p1), cyclic, image
-        self._h = lib().orc_plan_create_ex(n, K, L, p0, p1, 1 if cyclic else 0, 1 if image else 0)
+        self.ts = ts
+        self._h = lib().orc_plan_create_ts(n, K, L, p0, p1, 1 if cyclic else 0, 1 if image else 0,
+                                           1 if ts else 0)
         if not self._h:
             raise ValueError("orc_plan_create failed")
         self.m = lib().orc_plan_m(self._h)
@@ -294,3 +321,34 @@ def alpha_formulas(n: int, u_log2_inv: int = 24, p0: int = P0, p1: int = P1) -> 
         "ntt": int(mpmath.floor((lg(mpmath.mpf(p0) / 2) - lg(N)) / 2)),
         "crt": int(mpmath.floor((lg(mpmath.mpf(p0) * p1 / 2) - lg(N)) / 2)),
     }
+
+
+# --------------------------------------------------------------------------- TS helpers
+def ts_from_double(d: float) -> TS:
+    return lib().orc_ts_from_double(d)
+
+
+def ts_from_int64(v: int) -> TS:
+    return lib().orc_ts_from_int64(v)
+
+
+def ts_to_double(t: TS) -> float:
+    return lib().orc_ts_to_double(t)
+
+
+def ts_add(a: TS, b: TS) -> TS:
+    return lib().orc_ts_add(a, b)
+
+
+def ts_mul(a: TS, b: TS) -> TS:
+    return lib().orc_ts_mul(a, b)
+
+
+def split_ts(r: np.ndarray, alpha_: int, K: int):
+    """orc_split_ts on a [3][len] float32 TS vector (modified in place). Returns (k, digits, E)."""
+    r = np.ascontiguousarray(r, dtype=np.float32)
+    n = r.shape[1]
+    dig = np.zeros((K, n), np.int32)
+    E = np.zeros(K, np.int32)
+    k = lib().orc_split_ts(n, _p(r), alpha_, K, _p(dig), _p(E))
+    return k, dig, E, r

@@ -308,6 +308,149 @@ int orc_split(int64_t len, double* hi, double* lo, int alpha, int K, int32_t* di
   return k;
 }
 
+/* ------------------------------------------------------------------------- */
+/* O-TS. Triple-single (TS) working precision.  */
+/* A TS number is x0 + x1 + x2 with fp32 words, |x_s| <= ulp(x_{s-1})/2.  The  */
+/* paper cites TS arithmetic (Fabiano et al.) without giving TSAdd / TSMul;     */
+/* the sequences below are this build's reading (DESIGN ruling 24): error-free */
+/* TwoSum / FastTwoSum / FMA TwoProd on fp32 words, a fixed rounded tail, then */
+/* Renorm3.  Their accuracy (relative error <= 2^-62) is pinned against exact  */
+/* rationals in tests/test_oracle_ts.py.  Every op is a single fp32 RN op; the */
+/* file is compiled with -ffp-contract=off.                                    */
+/* ------------------------------------------------------------------------- */
+typedef struct { float x0, x1, x2; } orc_ts;
+
+static void two_sum_f(float a, float b, float* s, float* e) {
+  *s = a + b;
+  float bb = *s - a;
+  *e = (a - (*s - bb)) + (b - bb);
+}
+static void fast_two_sum_f(float a, float b, float* s, float* e) {
+  *s = a + b;
+  *e = b - (*s - a);
+}
+static void two_prod_f(float a, float b, float* p, float* e) {
+  *p = a * b;
+  *e = fmaf(a, b, -*p);
+}
+/* Renorm3: (a, b, c) with a the leading term -> non-overlapping triple */
+static orc_ts ts_renorm3(float a, float b, float c) {
+  float s, t3, s0, t2, s1, s2;
+  two_sum_f(b, c, &s, &t3);
+  two_sum_f(a, s, &s0, &t2);
+  two_sum_f(t2, t3, &s1, &s2);
+  fast_two_sum_f(s0, s1, &s0, &s1);
+  fast_two_sum_f(s1, s2, &s1, &s2);
+  orc_ts r = {s0, s1, s2};
+  return r;
+}
+/* TS(d): exact for finite d inside the normal fp32 range (53 <= 72 bits) */
+orc_ts orc_ts_from_double(double d) {
+  orc_ts r;
+  r.x0 = (float)d;
+  double t = d - (double)r.x0;
+  r.x1 = (float)t;
+  t = t - (double)r.x1;
+  r.x2 = (float)t;
+  return r;
+}
+/* TS(v) for |v| < 2^62: exact (24 + 24 + 14 bits) */
+orc_ts orc_ts_from_int64(int64_t v) {
+  orc_ts r;
+  r.x0 = (float)v;
+  int64_t t = v - (int64_t)r.x0;
+  r.x1 = (float)t;
+  t = t - (int64_t)r.x1;
+  r.x2 = (float)t;
+  return r;
+}
+/* fl64(x0 + x1 + x2): x1 + x2 is exact in binary64, one rounding at the end */
+double orc_ts_to_double(orc_ts a) { return (double)a.x0 + ((double)a.x1 + (double)a.x2); }
+orc_ts orc_ts_add(orc_ts a, orc_ts b) {
+  float s0, e0, s1, e1, t1, f1;
+  two_sum_f(a.x0, b.x0, &s0, &e0);
+  two_sum_f(a.x1, b.x1, &s1, &e1);
+  const float s2 = a.x2 + b.x2;
+  two_sum_f(e0, s1, &t1, &f1);
+  const float t2 = (f1 + e1) + s2;
+  return ts_renorm3(s0, t1, t2);
+}
+orc_ts orc_ts_neg(orc_ts a) {
+  orc_ts r = {-a.x0, -a.x1, -a.x2};
+  return r;
+}
+orc_ts orc_ts_mul(orc_ts a, orc_ts b) {
+  float p0, q0, p1, q1, p2, q2, s1, r1, t1, r2;
+  two_prod_f(a.x0, b.x0, &p0, &q0);
+  two_prod_f(a.x0, b.x1, &p1, &q1);
+  two_prod_f(a.x1, b.x0, &p2, &q2);
+  const float c = ((((a.x0 * b.x2) + (a.x1 * b.x1)) + (a.x2 * b.x0)) + q1) + q2;
+  two_sum_f(p1, p2, &s1, &r1);
+  two_sum_f(q0, s1, &t1, &r2);
+  const float t2 = (r1 + r2) + c;
+  return ts_renorm3(p0, t1, t2);
+}
+/* exact scaling by 2^e (no overflow / underflow on this path's ranges) */
+static orc_ts ts_ldexp(orc_ts a, int e) {
+  orc_ts r = {ldexpf(a.x0, e), ldexpf(a.x1, e), ldexpf(a.x2, e)};
+  return r;
+}
+static int ts_finite(orc_ts a) { return isfinite(a.x0) && isfinite(a.x1) && isfinite(a.x2); }
+
+/* x' = x (.) omega in TS (Alg.4 TS form, P:473-474 with TS ops): TS(x) and
+ * TS(omega) from the binary64 values, TSSub / TSAdd of TSMul products. */
+void orc_premul_ts(int64_t n, const double* x, const double* C, const double* S, int conj,
+                   float* re /* [3][n] */, float* im /* [3][n] */) {
+  for (int64_t j = 0; j < n; j++) {
+    const orc_ts xr = orc_ts_from_double(x[2 * j]);
+    const orc_ts xi = orc_ts_from_double(conj ? -x[2 * j + 1] : x[2 * j + 1]);
+    const orc_ts c = orc_ts_from_double(C[j]), sn = orc_ts_from_double(S[j]);
+    const orc_ts r = orc_ts_add(orc_ts_mul(xr, c), orc_ts_neg(orc_ts_mul(xi, sn)));
+    const orc_ts i = orc_ts_add(orc_ts_mul(xr, sn), orc_ts_mul(xi, c));
+    re[j] = r.x0; re[n + j] = r.x1; re[2 * n + j] = r.x2;
+    im[j] = i.x0; im[n + j] = i.x1; im[2 * n + j] = i.x2;
+  }
+}
+
+/* TS split, Alg. SplitTSAndCalcNTT literally: rho = 24 - alpha (u32 = 2^-24),
+ * mu = ||r0||_inf, sigma = 2^(ceil(log2 mu) + rho), x = fl32(fl32(r0 + sigma) - sigma),
+ * (r0, r1) <- FastTwoSum(fl32(r0 - x), r1), then (r1, r2) <- FastTwoSum(r1, r2) with the
+ * r1 just produced (ruling 25), D = x c with c = (u32 sigma)^-1 = 2^(alpha - E).
+ * r is [3][len] (r0, r1, r2); digits [K][len]; returns levels, -1 if non-finite. */
+int orc_split_ts(int64_t len, float* r, int alpha, int K, int32_t* digits, int32_t* E) {
+  const int rho = 24 - alpha;
+  float* r0 = r;
+  float* r1 = r + len;
+  float* r2 = r + 2 * len;
+  int k;
+  for (k = 0; k < K; k++) {
+    double mu = 0.0;
+    for (int64_t j = 0; j < len; j++) {
+      double a = fabs((double)r0[j]);
+      if (a > mu || a != a) mu = a;
+    }
+    for (int64_t j = 0; j < len; j++)
+      if (!isfinite(r1[j]) || !isfinite(r2[j])) mu = NAN;
+    if (!isfinite(mu)) return -1;
+    if (mu == 0.0) break;
+    const int Ek = ceil_log2_exact(mu);
+    const float sigma = ldexpf(1.0f, Ek + rho);
+    const float scale = ldexpf(1.0f, alpha - Ek);
+    E[k] = Ek;
+    for (int64_t j = 0; j < len; j++) {
+      const float t = r0[j] + sigma;
+      const float x = t - sigma;
+      digits[(int64_t)k * len + j] = (int32_t)(x * scale);
+      const float d = r0[j] - x;
+      float a, b;
+      fast_two_sum_f(d, r1[j], &a, &b);
+      r0[j] = a;
+      fast_two_sum_f(b, r2[j], &r1[j], &r2[j]);
+    }
+  }
+  return k;
+}
+
 /* Image mode (beyond the paper): Alg.6 applied to the complex vector
  * with ONE exponent per level shared by both parts -- mu = max_j max(|hi_re|, |hi_im|),
  * then the same sigma and scale for both parts, each part stepping exactly as orc_split.
@@ -409,6 +552,7 @@ typedef struct {
   uint32_t* W;          /* [2 parts][K][2 primes][m], natural order; image mode: [2 images] */
   int status;
   int image;            /* 1: complex-image accumulation, see orc_execute_image */
+  int ts;               /* 1: triple-single working precision for a1, a2, a7 */
   uint32_t iota[2];     /* image mode: iota_q = g_q^((p_q - 1)/4), iota^2 = -1 mod p_q */
 } orc_plan;
 
@@ -447,9 +591,16 @@ void orc_plan_destroy(orc_plan* pl) {
  * unnecessary and the FFT length N can be kept equal to n".  The ZeroPad_pm
  * formula below then reduces to omega~*(j) = omega*(j), j < n (its two ranges coincide
  * because omega*(n - j) = omega*(j) for even n). */
+orc_plan* orc_plan_create_ts(int64_t n, int K, int L, uint32_t p0, uint32_t p1, int cyclic,
+                             int image, int ts);
 orc_plan* orc_plan_create_ex(int64_t n, int K, int L, uint32_t p0, uint32_t p1, int cyclic,
                              int image) {
+  return orc_plan_create_ts(n, K, L, p0, p1, cyclic, image, 0);
+}
+orc_plan* orc_plan_create_ts(int64_t n, int K, int L, uint32_t p0, uint32_t p1, int cyclic,
+                             int image, int ts) {
   if (n < 1 || K < 1 || K > ORC_MAXK || L < 1 || L > ORC_MAXL) return NULL;
+  if (ts && image) return NULL; /* TS precision is built for the paper's real mode only */
   if (cyclic && (n & (n - 1))) return NULL;
   if (image && ((p0 & 3u) != 1u || (p1 & 3u) != 1u)) return NULL; /* need iota, p = 1 mod 4 */
   orc_plan* pl = (orc_plan*)calloc(1, sizeof(orc_plan));
@@ -460,6 +611,7 @@ orc_plan* orc_plan_create_ex(int64_t n, int K, int L, uint32_t p0, uint32_t p1, 
   pl->p[0] = p0;
   pl->p[1] = p1;
   pl->image = image;
+  pl->ts = ts;
   /* n = DFT length (ruling 2).  Image mode: a real output of a group sums up to L n
    * complex products, |Re(ab)| <= |ar br| + |ai bi| <= 2 4^alpha, so the bound is
    * 2 L n 4^alpha < P/2, i.e. the real-mode alpha at 2n. */
@@ -490,6 +642,17 @@ orc_plan* orc_plan_create_ex(int64_t n, int K, int L, uint32_t p0, uint32_t p1, 
     pl->kw[0] = pl->kw[1] = orc_split_shared(m, hre, lre, him, lim, pl->alpha, K, pl->wdig,
                                              pl->Ew[0]);
     for (int k = 0; k < K; k++) pl->Ew[1][k] = pl->Ew[0][k];
+  } else if (ts) { /* TS(omega~*) from the binary64 table (Alg.4 TS form, step 1) */
+    float* r = (float*)malloc(sizeof(float) * 3 * m);
+    for (int part = 0; part < 2; part++) {
+      const double* h = part ? him : hre;
+      for (int64_t j = 0; j < m; j++) {
+        const orc_ts t = orc_ts_from_double(h[j]);
+        r[j] = t.x0; r[m + j] = t.x1; r[2 * m + j] = t.x2;
+      }
+      pl->kw[part] = orc_split_ts(m, r, pl->alpha, K, pl->wdig + (size_t)part * K * m, pl->Ew[part]);
+    }
+    free(r);
   } else {
     pl->kw[0] = orc_split(m, hre, lre, pl->alpha, K, pl->wdig, pl->Ew[0]);
     pl->kw[1] = orc_split(m, him, lim, pl->alpha, K, pl->wdig + (size_t)K * m, pl->Ew[1]);
@@ -727,25 +890,34 @@ int orc_execute(const orc_plan* pl, const double* x, double* y, int dir, orc_tap
   int flags = 0;
   int64_t nfwd = 0, ninv = 0;
 
-  double* hr = (double*)malloc(sizeof(double) * n);
-  double* lr = (double*)malloc(sizeof(double) * n);
-  double* hi = (double*)malloc(sizeof(double) * n);
-  double* li = (double*)malloc(sizeof(double) * n);
-  /* step 2 of Alg.4: x' = x (.) omega */
-  orc_premul(n, x, pl->C, pl->S, dir > 0, hr, lr, hi, li);
-  if (tp && tp->xdd) {
-    memcpy(tp->xdd, hr, sizeof(double) * n);
-    memcpy(tp->xdd + n, lr, sizeof(double) * n);
-    memcpy(tp->xdd + 2 * n, hi, sizeof(double) * n);
-    memcpy(tp->xdd + 3 * n, li, sizeof(double) * n);
-  }
   /* Alg.6 on Re x' and Im x' (split caching) */
   int32_t* dig = (int32_t*)calloc((size_t)2 * K * n, sizeof(int32_t));
   int32_t Ex[2][ORC_MAXK] = {{0}};
   int kx[2];
-  kx[0] = orc_split(n, hr, lr, alpha, K, dig, Ex[0]);
-  kx[1] = orc_split(n, hi, li, alpha, K, dig + (size_t)K * n, Ex[1]);
-  free(hr); free(lr); free(hi); free(li);
+  if (pl->ts) { /* TS working precision (f4): Alg.4 TS steps 1-2, TS split */
+    float* tre = (float*)malloc(sizeof(float) * 3 * n);
+    float* tim = (float*)malloc(sizeof(float) * 3 * n);
+    orc_premul_ts(n, x, pl->C, pl->S, dir > 0, tre, tim);
+    kx[0] = orc_split_ts(n, tre, alpha, K, dig, Ex[0]);
+    kx[1] = orc_split_ts(n, tim, alpha, K, dig + (size_t)K * n, Ex[1]);
+    free(tre); free(tim);
+  } else {
+    double* hr = (double*)malloc(sizeof(double) * n);
+    double* lr = (double*)malloc(sizeof(double) * n);
+    double* hi = (double*)malloc(sizeof(double) * n);
+    double* li = (double*)malloc(sizeof(double) * n);
+    /* step 2 of Alg.4: x' = x (.) omega */
+    orc_premul(n, x, pl->C, pl->S, dir > 0, hr, lr, hi, li);
+    if (tp && tp->xdd) {
+      memcpy(tp->xdd, hr, sizeof(double) * n);
+      memcpy(tp->xdd + n, lr, sizeof(double) * n);
+      memcpy(tp->xdd + 2 * n, hi, sizeof(double) * n);
+      memcpy(tp->xdd + 3 * n, li, sizeof(double) * n);
+    }
+    kx[0] = orc_split(n, hr, lr, alpha, K, dig, Ex[0]);
+    kx[1] = orc_split(n, hi, li, alpha, K, dig + (size_t)K * n, Ex[1]);
+    free(hr); free(lr); free(hi); free(li);
+  }
   if (kx[0] < 0 || kx[1] < 0) {
     flags |= 1;
     for (int64_t j = 0; j < 2 * n; j++) y[j] = NAN;
@@ -788,6 +960,7 @@ int orc_execute(const orc_plan* pl, const double* x, double* y, int dir, orc_tap
   static const int conv_a[4] = {0, 1, 1, 0};
   static const int conv_b[4] = {0, 1, 0, 1};
   double* acc = (double*)calloc((size_t)4 * 2 * n, sizeof(double)); /* DD per conv */
+  orc_ts* tacc = pl->ts ? (orc_ts*)calloc((size_t)4 * n, sizeof(orc_ts)) : NULL; /* TS per conv */
   int32_t* sched = (int32_t*)malloc(sizeof(int32_t) * stride);
   uint32_t* Zg = (uint32_t*)malloc(sizeof(uint32_t) * 2 * m);
   for (int cv = 0; cv < 4; cv++) {
@@ -823,6 +996,11 @@ int orc_execute(const orc_plan* pl, const double* x, double* y, int dir, orc_tap
         int64_t Zj = orc_garner2(Zg[j], Zg[m + j], pl->p[0], pl->p[1], &fix);
         if (fix) flags |= 2;
         if (tp && tp->crt) tp->crt[((size_t)cv * G + g) * n + j] = Zj;
+        if (pl->ts) { /* z / c in TS (exact), TSAdd in flush order (Alg.8 l.975-976) */
+          tacc[(size_t)cv * n + j] =
+              orc_ts_add(tacc[(size_t)cv * n + j], ts_ldexp(orc_ts_from_int64(Zj), -cexp));
+          continue;
+        }
         double h = (double)Zj;
         double l = (double)(Zj - (int64_t)h);
         dd_add(acc[(cv * 2) * n + j], acc[(cv * 2 + 1) * n + j], h * scale, l * scale,
@@ -832,6 +1010,24 @@ int orc_execute(const orc_plan* pl, const double* x, double* y, int dir, orc_tap
   }
   free(Zg); free(sched); free(X);
 
+  if (pl->ts) { /* TS: y' = (rr - ii) + i (ir + ri), y = y' (.) omega in TS, fl64 (Alg.4 TS 4-5) */
+    for (int64_t j = 0; j < n; j++) {
+      const orc_ts yr = orc_ts_add(tacc[0 * n + j], orc_ts_neg(tacc[1 * n + j]));
+      const orc_ts yi = orc_ts_add(tacc[2 * n + j], tacc[3 * n + j]);
+      const orc_ts c = orc_ts_from_double(pl->C[j]), sn = orc_ts_from_double(pl->S[j]);
+      const orc_ts orr = orc_ts_add(orc_ts_mul(yr, c), orc_ts_neg(orc_ts_mul(yi, sn)));
+      const orc_ts oii = orc_ts_add(orc_ts_mul(yr, sn), orc_ts_mul(yi, c));
+      double o_re = orc_ts_to_double(orr), o_im = orc_ts_to_double(oii);
+      if (!ts_finite(orr) || !ts_finite(oii)) flags |= 1;
+      if (dir > 0) {
+        o_re = o_re / (double)n;
+        o_im = -o_im / (double)n;
+      }
+      y[2 * j] = o_re;
+      y[2 * j + 1] = o_im;
+    }
+    free(tacc);
+  } else
   /* y' = (rr - ii) + i (ir + ri); Alg.4 step 4: y = y' (.) omega; step 5: round to fp64 */
   for (int64_t j = 0; j < n; j++) {
     double yrh, yrl, yih, yil;
