@@ -60,7 +60,7 @@ typedef struct {
   int32_t device;             /* CUDA device ordinal, -1 = current                 */
   int32_t conv_mode;          /* OZFFT_CONV_PADDED (0) or OZFFT_CONV_CYCLIC (1), below */
   int32_t accum_mode;         /* OZFFT_ACCUM_REAL (0) or OZFFT_ACCUM_IMAGE (1), below  */
-  int32_t reserved;           /* must be 0                                          */
+  int32_t precision;          /* OZFFT_PREC_DD (0) or OZFFT_PREC_TS (1), below          */
   uint64_t max_workspace_bytes;
 } ozfft_plan_desc;
 
@@ -93,6 +93,18 @@ typedef struct {
 #define OZFFT_ACCUM_REAL 0
 #define OZFFT_ACCUM_IMAGE 1
 
+/* Working precision of the O(n) steps a1 (premultiply), a2 (split) and a7 (recombination,
+ * post-chirp) (desc.precision).
+ *  OZFFT_PREC_DD: binary64 double-double (DESIGN ruling 1; the default).
+ *  OZFFT_PREC_TS: the paper's triple-single arithmetic (Alg.4 TS form, TS split
+ *    P:784-798): x, omega, omega~* converted to TS, x' = x (.) omega with
+ *    TSMul / TSAdd, the split on the TS words with rho = 24 - alpha, z / c accumulated with
+ *    TSAdd, post-chirp in TS, fl64 at the end.  TSAdd / TSMul are this build's reading
+ *    (the paper gives none; DESIGN ruling 24).  Inputs must stay inside the fp32 exponent
+ *    range (|x| <= ~2^100 and well above 2^-100); only with OZFFT_ACCUM_REAL. */
+#define OZFFT_PREC_DD 0
+#define OZFFT_PREC_TS 1
+
 typedef struct {
   int64_t n, m, batch, chunk;   /* m: Bluestein cyclic length; chunk: transforms per pass */
   int32_t K, L, alpha, rho;     /* alpha = floor((log2(p0p1/2) - log2(L n))/2), rho = 53-alpha */
@@ -102,7 +114,7 @@ typedef struct {
   int32_t cached_ntts;          /* forward NTTs of omega~* slices done at bind */
   int32_t conv_mode;            /* as in the descriptor                                */
   int32_t accum_mode;           /* as in the descriptor                                */
-  int32_t reserved;
+  int32_t precision;            /* as in the descriptor                                */
 } ozfft_plan_info;
 
 typedef struct {

@@ -41,7 +41,7 @@ class OzfftError(RuntimeError):
 class PlanDesc(C.Structure):
     _fields_ = [("n", C.c_int64), ("batch", C.c_int64), ("K", C.c_int32), ("L", C.c_int32),
                 ("p0", C.c_uint32), ("p1", C.c_uint32), ("device", C.c_int32),
-                ("conv_mode", C.c_int32), ("accum_mode", C.c_int32), ("reserved", C.c_int32),
+                ("conv_mode", C.c_int32), ("accum_mode", C.c_int32), ("precision", C.c_int32),
                 ("max_workspace_bytes", C.c_uint64)]
 
 
@@ -51,7 +51,7 @@ class PlanInfo(C.Structure):
                 ("log2_rows", C.c_int32), ("log2_cols", C.c_int32),
                 ("persistent_bytes", C.c_uint64), ("workspace_bytes", C.c_uint64),
                 ("cached_ntts", C.c_int32), ("conv_mode", C.c_int32), ("accum_mode", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("precision", C.c_int32)]
 
 
 class ExecStats(C.Structure):
@@ -145,14 +145,17 @@ class Plan:
     (m = n for power-of-two n; bitwise-identical results at half the NTT length).
     accum: "real" (the paper's four real convolutions) or "image" (complex-image
     accumulation: 32 instead of 52 runtime NTTs; different digits and bits).
+    precision: "dd" (double-double O(n) steps, the default) or "ts" (the paper's
+    triple-single arithmetic; accum="real" only).
     """
 
     CONV = {"padded": 0, "cyclic": 1}
     ACCUM = {"real": 0, "image": 1}
+    PREC = {"dd": 0, "ts": 1}
 
     def __init__(self, n: int, batch: int = 1, K: int = 3, L: int = 3, p0: int = 0, p1: int = 0,
                  device=None, max_workspace_bytes: int = 0, stream=None, conv: str = "padded",
-                 accum: str = "real"):
+                 accum: str = "real", precision: str = "dd"):
         if not torch.cuda.is_available():
             raise RuntimeError("ozfft needs a CUDA device (sm_100a); there is no CPU fallback")
         self._lib = load_library()
@@ -162,9 +165,11 @@ class Plan:
             raise ValueError(f"conv must be one of {sorted(self.CONV)}")
         if accum not in self.ACCUM:
             raise ValueError(f"accum must be one of {sorted(self.ACCUM)}")
+        if precision not in self.PREC:
+            raise ValueError(f"precision must be one of {sorted(self.PREC)}")
         d = PlanDesc(n=n, batch=batch, K=K, L=L, p0=p0, p1=p1, device=dev.index or 0,
-                     conv_mode=self.CONV[conv], accum_mode=self.ACCUM[accum], reserved=0,
-                     max_workspace_bytes=max_workspace_bytes)
+                     conv_mode=self.CONV[conv], accum_mode=self.ACCUM[accum],
+                     precision=self.PREC[precision], max_workspace_bytes=max_workspace_bytes)
         h = C.c_void_p()
         _check(self._lib.ozfft_plan_create(C.byref(d), C.byref(h)))
         self._h = h
@@ -173,7 +178,7 @@ class Plan:
         self.n, self.batch, self.K, self.L = n, batch, info.K, info.L
         self.m, self.alpha, self.rho, self.chunk = info.m, info.alpha, info.rho, info.chunk
         self.log2_rows, self.log2_cols = info.log2_rows, info.log2_cols
-        self.conv, self.accum = conv, accum
+        self.conv, self.accum, self.precision = conv, accum, precision
         with torch.cuda.device(dev):
             self.persistent = torch.empty(max(info.persistent_bytes, 256), dtype=torch.uint8, device=dev)
             self.workspace = torch.empty(max(info.workspace_bytes, 256), dtype=torch.uint8, device=dev)

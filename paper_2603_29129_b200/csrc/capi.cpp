@@ -186,12 +186,18 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     while (m < 2 * desc.n - 1) m <<= 1;  // Bluestein length, N >= 2n-1
   }
   pl->conv_mode = desc.conv_mode;
-  if ((desc.accum_mode != OZFFT_ACCUM_REAL && desc.accum_mode != OZFFT_ACCUM_IMAGE) ||
-      desc.reserved != 0) {
+  if (desc.accum_mode != OZFFT_ACCUM_REAL && desc.accum_mode != OZFFT_ACCUM_IMAGE) {
     delete pl;
     return fail(OZFFT_ERR_INVALID_ARGUMENT, "accum_mode must be OZFFT_ACCUM_REAL or _IMAGE");
   }
+  if ((desc.precision != OZFFT_PREC_DD && desc.precision != OZFFT_PREC_TS) ||
+      (desc.precision == OZFFT_PREC_TS && desc.accum_mode == OZFFT_ACCUM_IMAGE)) {
+    delete pl;
+    return fail(OZFFT_ERR_INVALID_ARGUMENT,
+                "precision must be OZFFT_PREC_DD or OZFFT_PREC_TS (TS with OZFFT_ACCUM_REAL only)");
+  }
   pl->image = desc.accum_mode == OZFFT_ACCUM_IMAGE ? 1 : 0;
+  pl->ts = desc.precision == OZFFT_PREC_TS ? 1 : 0;
   if (pl->image && ((p0 & 3u) != 1u || (p1 & 3u) != 1u)) {
     delete pl;
     return fail(OZFFT_ERR_BAD_PRIMES, "OZFFT_ACCUM_IMAGE needs primes = 1 mod 4");
@@ -210,12 +216,12 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
   }
   // NTT decomposition: one pass up to m = 2^12, else rows of C = 2^11 (2^12 from m = 2^20) and
   // columns of R = m / C <= 2^8 (up to 2^10 at m = 2^21, 2^22, with 32 elements per thread).
-  // (One-warp rows of C = 2^10 with 32 elements per thread, OZFFT_TUNE_LOGC=10, measured
-  // slower on B200: 122 vs 147 GFLOP/s at c3.)
+  // (Measured alternatives at c3: one-warp rows of C = 2^10, 122 vs 147 GFLOP/s; rows of
+  // C = 2^12, 141 vs 154 GFLOP/s -- OZFFT_TUNE_LOGC=12 still selects the latter.)
   pl->logC = logm <= 12 ? logm : std::min(12, std::max(11, logm - 8));
   if (const char* t = std::getenv("OZFFT_TUNE_LOGC")) {  // tuning knob (tools/, not the hot path)
     const int v = std::atoi(t);
-    if (v >= 10 && v <= 12 && logm > v && logm - v <= 10) pl->logC = v;
+    if (logm > 12 && decomposition_supported(logm - v, v)) pl->logC = v;
   }
   pl->logR = logm - pl->logC;
   // image mode: a real output sums L n complex products (|Re| <= 2 4^alpha each)
@@ -224,7 +230,7 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     delete pl;
     return fail(OZFFT_ERR_ALPHA, "alpha < 1");
   }
-  pl->rho = 53 - pl->alpha;
+  pl->rho = (pl->ts ? 24 : 53) - pl->alpha;  // u = 2^-24 (TS) or 2^-53 (DD, ruling 1)
   int dev = desc.device;
   if (dev < 0) {
     if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
@@ -258,6 +264,7 @@ ozfft_status ozfft_plan_get_info(const ozfft_plan* pl, ozfft_plan_info* info) {
   info->cached_ntts = pl->bound ? 2 * (pl->kw[0] + pl->kw[1]) : 4 * pl->K;
   info->conv_mode = pl->conv_mode;
   info->accum_mode = pl->image;
+  info->precision = pl->ts;
   return OZFFT_OK;
 }
 

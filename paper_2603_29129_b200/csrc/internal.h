@@ -33,6 +33,7 @@ struct Plan {
   int logm = 0, logC = 0, logR = 0;  // m = R * C
   int conv_mode = 0;                 // OZFFT_CONV_PADDED (m >= 2n-1) or OZFFT_CONV_CYCLIC (m = n)
   int image = 0;                     // OZFFT_ACCUM_IMAGE: complex-image accumulation (f2)
+  int ts = 0;                        // OZFFT_PREC_TS: triple-single a1 / a2 / a7 (f4)
   uint32_t iota[2] = {0, 0};         // image mode: iota_q = g^((p_q - 1)/4), iota^2 = -1
   int device = 0;
   uint64_t max_ws = 0;
@@ -79,6 +80,8 @@ struct Prof {
   std::vector<Rec> recs;
 };
 void prof_mark(const Plan& pl, int stage, bool begin, void* stream);
+// two-pass decompositions (log2 R, log2 C) instantiated in kernels.cu
+bool decomposition_supported(int logR, int logC);
 void count_launches(int n);
 
 // Schedule row length per (transform, conv): ngroups + K*K groups of (cexp, npairs, L pairs)

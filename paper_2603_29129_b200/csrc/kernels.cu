@@ -91,6 +91,101 @@ __device__ __forceinline__ void dd_mul_d(double ah, double al, double b, double&
   fast_two_sum(p, e, rh, rl);
 }
 
+// ============================================================== triple-single (TS, f4)
+// x0 + x1 + x2 in fp32 words.  The op sequences are this build's reading of
+// TSAdd / TSMul (DESIGN ruling 24) and must match oracle/ozfft_oracle.c op for op.
+struct TSv {
+  float x0, x1, x2;
+};
+__device__ __forceinline__ void two_sum_f(float a, float b, float& s, float& e) {
+  s = __fadd_rn(a, b);
+  const float bb = __fsub_rn(s, a);
+  e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
+}
+__device__ __forceinline__ void fast_two_sum_f(float a, float b, float& s, float& e) {
+  s = __fadd_rn(a, b);
+  e = __fsub_rn(b, __fsub_rn(s, a));
+}
+__device__ __forceinline__ void two_prod_f(float a, float b, float& p, float& e) {
+  p = __fmul_rn(a, b);
+  e = __fmaf_rn(a, b, -p);
+}
+__device__ __forceinline__ TSv ts_renorm3(float a, float b, float c) {
+  float s, t3, s0, t2, s1, s2;
+  two_sum_f(b, c, s, t3);
+  two_sum_f(a, s, s0, t2);
+  two_sum_f(t2, t3, s1, s2);
+  fast_two_sum_f(s0, s1, s0, s1);
+  fast_two_sum_f(s1, s2, s1, s2);
+  return TSv{s0, s1, s2};
+}
+__device__ __forceinline__ TSv ts_from_double(double d) {
+  TSv r;
+  r.x0 = __double2float_rn(d);
+  double t = __dsub_rn(d, (double)r.x0);
+  r.x1 = __double2float_rn(t);
+  t = __dsub_rn(t, (double)r.x1);
+  r.x2 = __double2float_rn(t);
+  return r;
+}
+__device__ __forceinline__ TSv ts_from_int64(long long v) {
+  TSv r;
+  r.x0 = __ll2float_rn(v);
+  long long t = v - __float2ll_rz(r.x0);
+  r.x1 = __ll2float_rn(t);
+  t = t - __float2ll_rz(r.x1);
+  r.x2 = __ll2float_rn(t);
+  return r;
+}
+__device__ __forceinline__ double ts_to_double(TSv a) {
+  return __dadd_rn((double)a.x0, __dadd_rn((double)a.x1, (double)a.x2));
+}
+__device__ __forceinline__ TSv ts_add(TSv a, TSv b) {
+  float s0, e0, s1, e1, t1, f1;
+  two_sum_f(a.x0, b.x0, s0, e0);
+  two_sum_f(a.x1, b.x1, s1, e1);
+  const float s2 = __fadd_rn(a.x2, b.x2);
+  two_sum_f(e0, s1, t1, f1);
+  const float t2 = __fadd_rn(__fadd_rn(f1, e1), s2);
+  return ts_renorm3(s0, t1, t2);
+}
+__device__ __forceinline__ TSv ts_neg(TSv a) { return TSv{-a.x0, -a.x1, -a.x2}; }
+__device__ __forceinline__ TSv ts_mul(TSv a, TSv b) {
+  float p0, q0, p1, q1, p2, q2, s1, r1, t1, r2;
+  two_prod_f(a.x0, b.x0, p0, q0);
+  two_prod_f(a.x0, b.x1, p1, q1);
+  two_prod_f(a.x1, b.x0, p2, q2);
+  const float c = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(a.x0, b.x2), __fmul_rn(a.x1, b.x1)),
+                                                __fmul_rn(a.x2, b.x0)), q1), q2);
+  two_sum_f(p1, p2, s1, r1);
+  two_sum_f(q0, s1, t1, r2);
+  const float t2 = __fadd_rn(__fadd_rn(r1, r2), c);
+  return ts_renorm3(p0, t1, t2);
+}
+__device__ __forceinline__ TSv ts_ldexp(TSv a, int e) {
+  return TSv{ldexpf(a.x0, e), ldexpf(a.x1, e), ldexpf(a.x2, e)};
+}
+// TS split step (ruling 25): x = fl32(fl32(r0 + sigma) - sigma), digit x 2^(alpha-E),
+// (r0, t) = FastTwoSum(fl32(r0 - x), r1), (r1, r2) = FastTwoSum(t, r2).
+__device__ __forceinline__ int32_t split_step_ts(TSv& r, int E, int alpha, int rho) {
+  const float sigma = ldexpf(1.0f, E + rho);
+  const float t = __fadd_rn(r.x0, sigma);
+  const float x = __fsub_rn(t, sigma);
+  const int32_t D = __float2int_rz(__fmul_rn(x, ldexpf(1.0f, alpha - E)));
+  const float d = __fsub_rn(r.x0, x);
+  float a, b;
+  fast_two_sum_f(d, r.x1, a, b);
+  r.x0 = a;
+  fast_two_sum_f(b, r.x2, r.x1, r.x2);
+  return D;
+}
+// x' in TS (Alg.4 TS form): TS(x), TS(omega); mode 1: TS(omega~*).  Also the max-key of
+// |r0| (a NaN key when r1 or r2 is not finite, as the oracle's mu).
+__device__ __forceinline__ unsigned long long ts_key(const TSv& r) {
+  if (!isfinite(r.x1) || !isfinite(r.x2)) return 0x7FF8000000000000ull;
+  return (unsigned long long)__double_as_longlong(fabs((double)r.x0));
+}
+
 // ceil(log2(mu)) exactly from the bits of a positive finite double (ruling 8)
 __device__ __forceinline__ int ceil_log2_bits(unsigned long long u) {
   const int eb = (int)(u >> 52);
@@ -140,6 +235,23 @@ __device__ __forceinline__ void load_xprime(const SplitParams& P, int64_t b, int
   }
 }
 
+// x' in TS (Alg.4 TS form, steps 1-2): TS(x), TS(omega); mode 1: TS(omega~*) (f4).
+__device__ __forceinline__ void load_xprime_ts(const SplitParams& P, int64_t b, int64_t j, TSv& re,
+                                               TSv& im) {
+  if (P.mode == 0) {
+    const double2 xv = P.x[b * P.len + j];
+    const double2 w = P.chirp[j];
+    const TSv xr = ts_from_double(xv.x), xi = ts_from_double(P.conj ? -xv.y : xv.y);
+    const TSv c = ts_from_double(w.x), sn = ts_from_double(w.y);
+    re = ts_add(ts_mul(xr, c), ts_neg(ts_mul(xi, sn)));
+    im = ts_add(ts_mul(xr, sn), ts_mul(xi, c));
+  } else {
+    const double2 wv = P.x[j];
+    re = ts_from_double(wv.x);
+    im = ts_from_double(wv.y);
+  }
+}
+
 // One Ozaki extraction step on (h, l) with level exponent E (Alg.6 l.781-783).
 __device__ __forceinline__ int32_t split_step(double& h, double& l, int E, int alpha, int rho) {
   const double sigma = scalbn(1.0, E + rho);
@@ -161,6 +273,7 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 }
 
 // Max |hi| over the transform at split level `level` (levels < level applied first).
+template <bool TS>
 __global__ void __launch_bounds__(256) k_split_max(SplitParams P, int level) {
   const int64_t b = blockIdx.y;
   const unsigned long long* mub = P.mu + b * 2 * P.K;
@@ -178,13 +291,24 @@ __global__ void __launch_bounds__(256) k_split_max(SplitParams P, int level) {
   unsigned long long m0 = 0, m1 = 0;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P.len;
        j += (int64_t)gridDim.x * blockDim.x) {
-    double h[2], l[2];
-    load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
+    unsigned long long a0, a1;
+    if constexpr (TS) {  // f4: TS words, mu over r0
+      TSv r[2];
+      load_xprime_ts(P, b, j, r[0], r[1]);
 #pragma unroll
-    for (int v = 0; v < 2; ++v)  // a level with mu == 0 ended this part's split (Alg.6 l.780)
-      for (int k = 0; k < lv[v]; ++k) (void)split_step(h[v], l[v], E[v][k], P.alpha, P.rho);
-    const unsigned long long a0 = (unsigned long long)__double_as_longlong(fabs(h[0]));
-    const unsigned long long a1 = (unsigned long long)__double_as_longlong(fabs(h[1]));
+      for (int v = 0; v < 2; ++v)
+        for (int k = 0; k < lv[v]; ++k) (void)split_step_ts(r[v], E[v][k], P.alpha, P.rho);
+      a0 = ts_key(r[0]);
+      a1 = ts_key(r[1]);
+    } else {
+      double h[2], l[2];
+      load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
+#pragma unroll
+      for (int v = 0; v < 2; ++v)  // a level with mu == 0 ended this part's split (Alg.6 l.780)
+        for (int k = 0; k < lv[v]; ++k) (void)split_step(h[v], l[v], E[v][k], P.alpha, P.rho);
+      a0 = (unsigned long long)__double_as_longlong(fabs(h[0]));
+      a1 = (unsigned long long)__double_as_longlong(fabs(h[1]));
+    }
     m0 = a0 > m0 ? a0 : m0;  // NaN bits exceed +Inf bits: a NaN sticks
     m1 = a1 > m1 ? a1 : m1;
   }
@@ -243,6 +367,7 @@ __device__ void alg8_schedule(int kx, const int* sx, int ky, const int* sy, int 
 }
 
 // Digits for every level, per-transform stats and (block 0) the schedules.
+template <bool TS>
 __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
   const int64_t b = blockIdx.y;
   const unsigned long long* mub = P.mu + b * 2 * P.K;
@@ -286,15 +411,29 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
   if (bad) return;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P.len;
        j += (int64_t)gridDim.x * blockDim.x) {
-    double h[2], l[2];
-    load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
+    if constexpr (TS) {
+      TSv r[2];
+      load_xprime_ts(P, b, j, r[0], r[1]);
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j;
-      for (int k = 0; k < P.K; ++k) {
-        int32_t D = 0;
-        if (k < kv[v]) D = split_step(h[v], l[v], E[v][k], P.alpha, P.rho);
-        dv[k * P.len] = D;
+      for (int v = 0; v < 2; ++v) {
+        int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j;
+        for (int k = 0; k < P.K; ++k) {
+          int32_t D = 0;
+          if (k < kv[v]) D = split_step_ts(r[v], E[v][k], P.alpha, P.rho);
+          dv[k * P.len] = D;
+        }
+      }
+    } else {
+      double h[2], l[2];
+      load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j;
+        for (int k = 0; k < P.K; ++k) {
+          int32_t D = 0;
+          if (k < kv[v]) D = split_step(h[v], l[v], E[v][k], P.alpha, P.rho);
+          dv[k * P.len] = D;
+        }
       }
     }
   }
@@ -1058,7 +1197,28 @@ struct FinishParams {
   int64_t* crt_tap;         // [nb][4][K*K][n] or null
   // image mode (f2): per prime q the Shoup pairs of 2^-1 and (2 iota_q)^-1 mod p_q
   uint2 inv2[2], inv2i[2];
+  int ts;                   // f4: TS accumulation (sums stored as float4 (x0, x1, x2, 0))
 };
+
+// f4: accumulate z 2^-cexp into a TS sum kept in a 16-byte slot (Alg.8 l.975-976 with TSAdd)
+__device__ __forceinline__ double2 ts_accum(double2 slot, long long Z, int cexp) {
+  const float4 a = *reinterpret_cast<const float4*>(&slot);
+  const TSv r = ts_add(TSv{a.x, a.y, a.z}, ts_ldexp(ts_from_int64(Z), -cexp));
+  const float4 o = make_float4(r.x0, r.x1, r.x2, 0.0f);
+  return *reinterpret_cast<const double2*>(&o);
+}
+__device__ __forceinline__ TSv ts_of_slot(double2 slot) {
+  const float4 a = *reinterpret_cast<const float4*>(&slot);
+  return TSv{a.x, a.y, a.z};
+}
+// f4: y' = (rr - ii) + i (ir + ri), y = y' (.) omega in TS, fl64 (Alg.4 TS steps 4-5)
+__device__ __forceinline__ double2 ts_finish(TSv rr, TSv ii, TSv ir, TSv ri, double2 w) {
+  const TSv yr = ts_add(rr, ts_neg(ii)), yi = ts_add(ir, ri);
+  const TSv c = ts_from_double(w.x), sn = ts_from_double(w.y);
+  const TSv orr = ts_add(ts_mul(yr, c), ts_neg(ts_mul(yi, sn)));
+  const TSv oii = ts_add(ts_mul(yr, sn), ts_mul(yi, c));
+  return make_double2(ts_to_double(orr), ts_to_double(oii));
+}
 
 // f2: (re, im) residues of a complex integer from its two images z+ = re + iota im and
 // z- = re - iota im (mod p): re = (z+ + z-)/2, im = (z+ - z-)/(2 iota).
@@ -1159,6 +1319,52 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
   P.out[b * P.n + j] = o;
 }
 
+// f4, single-pass plans: Garner per group, z 2^-cexp accumulated with TSAdd in flush order
+// per real conv, TS combine + post-chirp, fl64 (as k_crt_finish, in TS).
+__global__ void __launch_bounds__(256, 4) k_crt_finish_ts(FinishParams P) {
+  const int64_t b = blockIdx.y;
+  const int K = P.K, L = P.L, G = K * K;
+  __shared__ int s_ng[4];
+  __shared__ int s_ce[4][kMaxK * kMaxK];
+  if (threadIdx.x < 4) {
+    const int cv = threadIdx.x;
+    const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
+    const int ng = srow[0];
+    s_ng[cv] = ng;
+    for (int g = 0; g < ng; ++g) s_ce[cv][g] = srow[1 + g * (2 + 2 * L)];
+  }
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.n) return;
+  double2 o;
+  if (P.stats[b * stats_stride(K) + 2 + 2 * K] & 1) {
+    o.x = __longlong_as_double(0x7FF8000000000000ll);
+    o.y = o.x;
+    P.out[b * P.n + j] = o;
+    return;
+  }
+  TSv S[4];
+#pragma unroll
+  for (int cv = 0; cv < 4; ++cv) {
+    TSv acc{0.0f, 0.0f, 0.0f};
+    const uint32_t* r0 = P.res + (((b * 4 + cv) * 2 + 0) * G) * P.n + j;
+    const uint32_t* r1 = P.res + (((b * 4 + cv) * 2 + 1) * G) * P.n + j;
+    for (int g = 0; g < s_ng[cv]; ++g) {
+      const long long Z = garner2(__ldcs(&r0[(int64_t)g * P.n]), __ldcs(&r1[(int64_t)g * P.n]), P);
+      if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + j] = Z;
+      acc = ts_add(acc, ts_ldexp(ts_from_int64(Z), -s_ce[cv][g]));
+    }
+    S[cv] = acc;
+  }
+  o = ts_finish(S[0], S[1], S[2], S[3], P.chirp[j]);
+  if (P.direction > 0) {
+    const double dn = (double)P.n;
+    o.x = __ddiv_rn(o.x, dn);
+    o.y = __ddiv_rn(-o.y, dn);
+  }
+  P.out[b * P.n + j] = o;
+}
+
 // f2, single-pass plans: the residues of both images of each group -> (re, im) per prime
 // -> Garner -> DD sums in flush order -> post-chirp (as k_crt_finish; res [nb][img][q][g][n]).
 __global__ void __launch_bounds__(256, 4) k_crt_finish_img(FinishParams P) {
@@ -1239,7 +1445,7 @@ struct ColCrtParams {
   int64_t* crt_tap;        // null, or [nb][4][K*K][n]
 };
 
-template <int LOGR, int LOGC, bool PRUNE>
+template <int LOGR, int LOGC, bool PRUNE, bool TS>
 __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_inv_crt(ColCrtParams P) {
   extern __shared__ uint32_t smem[];
   constexpr int LOGCB = col_log_cb(LOGR, LOGC);
@@ -1271,9 +1477,13 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   const int tv = tid >> LOGCB;
   const uint32_t col = (cb << LOGCB) + c;
   __shared__ double s_sc[kMaxK * kMaxK];
+  __shared__ int s_ce[kMaxK * kMaxK];
   const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(P.K, P.L);
   const int ng = srow[0];
-  for (int g = tid; g < ng; g += blockDim.x) s_sc[g] = scalbn(1.0, -srow[1 + g * (2 + 2 * P.L)]);
+  for (int g = tid; g < ng; g += blockDim.x) {
+    s_ce[g] = srow[1 + g * (2 + 2 * P.L)];
+    s_sc[g] = scalbn(1.0, -s_ce[g]);
+  }
   constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;
   double2* Sacc = reinterpret_cast<double2*>(smem + TILE + (TILE & 1));  // [NH][THREADS]
   // (staging the step-1 round twiddles in shared memory, as k_col_fwd does, measured slower
@@ -1333,6 +1543,10 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
         if (e * C < lim) {
           const long long Z = garner2(r0[h], rr[h], P.F);  // l.974
           if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + col + e * C] = Z;
+          if constexpr (TS) {  // f4: TSAdd of z 2^-cexp (slot holds the TS words)
+            Sacc[h * THREADS + tid] = ts_accum(Sacc[h * THREADS + tid], Z, s_ce[g]);
+            continue;
+          }
           const double hi = __ll2double_rn(Z);
           const double lo = __ll2double_rn(Z - __double2ll_rz(hi));
           double2 a = Sacc[h * THREADS + tid];
@@ -1474,7 +1688,7 @@ __global__ void __launch_bounds__(256) k_finish_dd(const double2* __restrict__ S
                                                    const int32_t* __restrict__ stats, int K,
                                                    const double2* __restrict__ chirp,
                                                    double2* __restrict__ out, int64_t n,
-                                                   int direction, int image) {
+                                                   int direction, int image, int ts) {
   const int64_t b = blockIdx.y;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
@@ -1482,6 +1696,18 @@ __global__ void __launch_bounds__(256) k_finish_dd(const double2* __restrict__ S
   if (stats[b * stats_stride(K) + 2 + 2 * K] & 1) {
     o.x = __longlong_as_double(0x7FF8000000000000ll);
     o.y = o.x;
+    out[b * n + j] = o;
+    return;
+  }
+  if (ts) {  // f4: the four sums are TS words
+    o = ts_finish(ts_of_slot(__ldcs(&S[(b * 4 + 0) * n + j])), ts_of_slot(__ldcs(&S[(b * 4 + 1) * n + j])),
+                  ts_of_slot(__ldcs(&S[(b * 4 + 2) * n + j])), ts_of_slot(__ldcs(&S[(b * 4 + 3) * n + j])),
+                  chirp[j]);
+    if (direction > 0) {
+      const double dn = (double)n;
+      o.x = __ddiv_rn(o.x, dn);
+      o.y = __ddiv_rn(-o.y, dn);
+    }
     out[b * n + j] = o;
     return;
   }
@@ -1527,6 +1753,7 @@ static void fill_crt_consts(const Plan& pl, FinishParams& FP) {
     FP.inv2[q] = make_uint2((uint32_t)i2, (uint32_t)((i2 << 32) / p));
     FP.inv2i[q] = make_uint2((uint32_t)i2i, (uint32_t)((i2i << 32) / p));
   }
+  FP.ts = pl.ts;
 }
 
 // f2: Shoup pairs of iota_q (image 0) and p_q - iota_q (image 1)
@@ -1609,10 +1836,18 @@ static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cud
   if (blocks_per > 65535) blocks_per = 65535;
   dim3 grid((unsigned)blocks_per, (unsigned)nb);
   prof_mark(pl, OZFFT_STAGE_SPLIT_MAX, true, st);
-  for (int level = 0; level < SP.K; ++level) k_split_max<<<grid, threads, 0, st>>>(SP, level);
+  for (int level = 0; level < SP.K; ++level) {
+    if (pl.ts)
+      k_split_max<true><<<grid, threads, 0, st>>>(SP, level);
+    else
+      k_split_max<false><<<grid, threads, 0, st>>>(SP, level);
+  }
   prof_mark(pl, OZFFT_STAGE_SPLIT_MAX, false, st);
   prof_mark(pl, OZFFT_STAGE_SPLIT_DIGITS, true, st);
-  k_split_digits<<<grid, threads, 0, st>>>(SP);
+  if (pl.ts)
+    k_split_digits<true><<<grid, threads, 0, st>>>(SP);
+  else
+    k_split_digits<false><<<grid, threads, 0, st>>>(SP);
   prof_mark(pl, OZFFT_STAGE_SPLIT_DIGITS, false, st);
   count_launches(SP.K + 1);
   return cuda_check("split kernels");
@@ -1651,45 +1886,58 @@ static void dispatch_log(int v, F&& f) {
   }
 }
 
+// Compile-time dispatch of the two-pass decompositions this build instantiates (capi.cpp
+// picks them): C = 2^11 with R = 2^2 .. 2^8 (m = 2^13 .. 2^19) and C = 2^12 with R = 2^7 ..
+// 2^10 (m = 2^19 tuning knob, 2^20 .. 2^22).  f(R, C) receives integral constants.
+template <int R, int C, class F>
+static void dispatch_rc_(int logR, int logC, F& f) {
+  if constexpr (C == 11 && R <= 8) {
+    if (logR == R && logC == C) return f(std::integral_constant<int, R>{}, std::integral_constant<int, C>{});
+    return dispatch_rc_<R + 1, C>(logR, logC, f);
+  } else if constexpr (C == 11) {
+    return dispatch_rc_<7, 12>(logR, logC, f);
+  } else if constexpr (R <= 10) {
+    if (logR == R && logC == C) return f(std::integral_constant<int, R>{}, std::integral_constant<int, C>{});
+    return dispatch_rc_<R + 1, C>(logR, logC, f);
+  }
+}
+template <class F>
+static void dispatch_rc(int logR, int logC, F&& f) {
+  dispatch_rc_<2, 11>(logR, logC, f);
+}
+bool decomposition_supported(int logR, int logC) {
+  return (logC == 11 && logR >= 2 && logR <= 8) || (logC == 12 && logR >= 7 && logR <= 10);
+}
+
 template <class K>
 static void set_smem(K kern, size_t bytes) {
   if (bytes > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int LOGR>
-static void launch_col_fwd_r(int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
-                             const ColParams& CP) {
-  dispatch_log<10, 12>(logC, [&](auto J) {
+static void launch_col_fwd(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
+                           const ColParams& CP) {
+  dispatch_rc(logR, logC, [&](auto I, auto J) {
     if (CP.image) {
-      set_smem(k_col_fwd<LOGR, J.value, true>, c.col_fwd_smem);
-      k_col_fwd<LOGR, J.value, true><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
+      set_smem(k_col_fwd<I.value, J.value, true>, c.col_fwd_smem);
+      k_col_fwd<I.value, J.value, true><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
     } else {
-      set_smem(k_col_fwd<LOGR, J.value, false>, c.col_fwd_smem);
-      k_col_fwd<LOGR, J.value, false><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
+      set_smem(k_col_fwd<I.value, J.value, false>, c.col_fwd_smem);
+      k_col_fwd<I.value, J.value, false><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
     }
   });
 }
-template <int LOGR>
-static void launch_col_inv_r(int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
-                             const ColParams& CP) {
-  dispatch_log<10, 12>(logC, [&](auto J) {
-    set_smem(k_col_inv<LOGR, J.value>, c.col_smem);
-    k_col_inv<LOGR, J.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
-  });
-}
-static void launch_col_fwd(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
-                           const ColParams& CP) {
-  dispatch_log<1, 10>(logR, [&](auto I) { launch_col_fwd_r<I.value>(logC, nblk, c, st, CP); });
-}
 static void launch_col_inv(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
                            const ColParams& CP) {
-  dispatch_log<1, 10>(logR, [&](auto I) { launch_col_inv_r<I.value>(logC, nblk, c, st, CP); });
+  dispatch_rc(logR, logC, [&](auto I, auto J) {
+    set_smem(k_col_inv<I.value, J.value>, c.col_smem);
+    k_col_inv<I.value, J.value><<<nblk, c.col_threads, c.col_smem, st>>>(CP);
+  });
 }
 static void launch_row(int logC, int logR, dim3 grid, const NttLaunch& c, cudaStream_t st,
                        const RowParams& RP) {
   if (logR > 0) {
-    dispatch_log<10, 12>(logC, [&](auto I) {
+    dispatch_log<11, 12>(logC, [&](auto I) {
       set_smem(k_row_fused<I.value, true>, c.row_smem);
       k_row_fused<I.value, true><<<grid, c.row_threads, c.row_smem, st>>>(RP);
     });
@@ -1901,22 +2149,28 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     const size_t smem = (tile + (tile & 1)) * 4 + (size_t)nh * c.col_threads * 16 * (pl.image ? 2 : 1);
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * (pl.image ? 1 : 4);
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
-    dispatch_log<1, 10>(pl.logR, [&](auto I) {
-      dispatch_log<10, 12>(pl.logC, [&](auto J) {
+    dispatch_rc(pl.logR, pl.logC, [&](auto I, auto J) {
+      {
         if (pl.image && prune) {
           set_smem(k_col_inv_crt_img<I.value, J.value, true>, smem);
           k_col_inv_crt_img<I.value, J.value, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
         } else if (pl.image) {
           set_smem(k_col_inv_crt_img<I.value, J.value, false>, smem);
           k_col_inv_crt_img<I.value, J.value, false><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+        } else if (prune && pl.ts) {
+          set_smem(k_col_inv_crt<I.value, J.value, true, true>, smem);
+          k_col_inv_crt<I.value, J.value, true, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+        } else if (pl.ts) {
+          set_smem(k_col_inv_crt<I.value, J.value, false, true>, smem);
+          k_col_inv_crt<I.value, J.value, false, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
         } else if (prune) {
-          set_smem(k_col_inv_crt<I.value, J.value, true>, smem);
-          k_col_inv_crt<I.value, J.value, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+          set_smem(k_col_inv_crt<I.value, J.value, true, false>, smem);
+          k_col_inv_crt<I.value, J.value, true, false><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
         } else {
-          set_smem(k_col_inv_crt<I.value, J.value, false>, smem);
-          k_col_inv_crt<I.value, J.value, false><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+          set_smem(k_col_inv_crt<I.value, J.value, false, false>, smem);
+          k_col_inv_crt<I.value, J.value, false, false><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
         }
-      });
+      }
     });
     prof_mark(pl, OZFFT_STAGE_COL_INV, false, st);
     count_launches(1);
@@ -1925,7 +2179,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)nb);
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
     k_finish_dd<<<grid, 256, 0, st>>>(XP.S, stats, K, chirp, reinterpret_cast<double2*>(A.out), n,
-                                      A.direction, pl.image);
+                                      A.direction, pl.image, pl.ts);
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
     count_launches(1);
     s = cuda_check("k_finish_dd");
@@ -1954,6 +2208,8 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
     if (pl.image)
       k_crt_finish_img<<<grid, 256, 0, st>>>(FP);
+    else if (pl.ts)
+      k_crt_finish_ts<<<grid, 256, 0, st>>>(FP);
     else
       k_crt_finish<<<grid, 256, 0, st>>>(FP);
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
@@ -2079,7 +2335,10 @@ ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, do
   FP.direction = direction;
   dim3 grid((unsigned)((pl.n + 255) / 256), 1);
   prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
-  k_crt_finish<<<grid, 256, 0, st>>>(FP);
+  if (pl.ts)
+    k_crt_finish_ts<<<grid, 256, 0, st>>>(FP);
+  else
+    k_crt_finish<<<grid, 256, 0, st>>>(FP);
   prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
   count_launches(1);
   return cuda_check("k_crt_finish (shard)");

@@ -55,7 +55,7 @@ def test_plan_create_validation(lib):
 
     def create(**kw):
         d = oz.PlanDesc(**{"n": 1024, "batch": 1, "K": 3, "L": 3, "p0": 0, "p1": 0,
-                           "device": 0, "conv_mode": 0, "accum_mode": 0, "reserved": 0,
+                           "device": 0, "conv_mode": 0, "accum_mode": 0, "precision": 0,
                            "max_workspace_bytes": 0, **kw})
         h = ctypes.c_void_p()
         st = L.ozfft_plan_create(ctypes.byref(d), ctypes.byref(h))
@@ -98,6 +98,9 @@ def test_plan_create_validation(lib):
     st, info = create(n=1 << 17, accum_mode=1)
     assert st == 0 and info.alpha == 20           # the real-mode value at 2n
     assert create(n=1024, accum_mode=2)[0] == 1
-    assert create(n=1024, reserved=1)[0] == 1
+    assert create(n=1024, precision=2)[0] == 1
+    st, info = create(n=1024, precision=1)
+    assert st == 0 and info.precision == 1 and info.alpha == 24
+    assert create(n=1024, precision=1, accum_mode=1)[0] == 1  # TS with the real mode only
     assert create(n=1024, accum_mode=1, p0=2130706433, p1=2013265921)[0] == 0  # 15*2^27+1
     assert create(n=1024, accum_mode=1, p0=2130706433, p1=2147483647)[0] == 3  # 2^31-1 = 3 mod 4
