@@ -187,6 +187,62 @@ def run_reference(args, cfg, rank, world):
 
 
 # ---------------------------------------------------------------------------- GPU arm
+def run_single(args, cfg, rank, world, local_rank):
+    """--mode single: ONE transform (row 0 of the config) sharded over the ranks by
+    (prime, real convolution) units, one NCCL all_gather_into_tensor of the inverse-NTT
+    residues, then CRT + recombination on every rank.
+    Strong scaling; device time per step = max over ranks (CUDA events on the stream)."""
+    import torch
+    import paper_2603_29129_b200 as oz
+    from paper_2603_29129_b200 import dist as ozd
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    n = cfg.n
+    x = torch.from_numpy(workloads.draw(cfg.dist, cfg.seed, cfg.batch, n, rows=slice(0, 1))).to(dev)
+    plan = oz.Plan(n, 1, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return ozd.gpu_sharded_forward(plan, x, rank, world)
+
+    for _ in range(max(args.warmup, 3)):
+        y = step()
+    torch.cuda.synchronize(dev)
+    ref = plan.forward(x)
+    assert torch.equal(y.view(1, n), ref), "sharded transform differs from the one-GPU execute"
+    if dist:
+        dist.barrier()
+    launches0 = oz.kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if dist:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    if rank == 0:
+        line = {"metric": METRIC, "value": args.steps * flops_per_transform(n) / (t_ms * 1e-3) / 1e9,
+                "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+                "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": {"workload": f"single-transform variant of {cfg.name}: transform 0, n={n}, "
+                                       f"units (prime, conv) split over {world} rank(s), one NCCL "
+                                       "all-gather of the residues before CRT",
+                           "n": n, "m": plan.m, "parallelism": f"unit-sharded x{world}",
+                           "residue_bytes_gathered": plan.shard_residue_bytes()},
+                "gpu_launches": int(oz.kernel_launches() - launches0)}
+        print(json.dumps(line), flush=True)
+
+
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
     import paper_2603_29129_b200 as oz
@@ -425,6 +481,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--conv", default="padded", choices=["padded", "cyclic"],
                     help="Bluestein length: m >= 2n-1 (north star) or m = n (P:238-241)")
+    ap.add_argument("--mode", default="batch", choices=["batch", "single"],
+                    help="batch: weak-scaled batches (the headline); single: one transform "
+                         "sharded over the ranks with an NCCL all-gather (SURVEY 8(e))")
     ap.add_argument("--accum", default="real", choices=["real", "image"],
                     help="four real convolutions (the paper) or complex images (SURVEY f2)")
     ap.add_argument("--no-extra", action="store_true",
@@ -443,7 +502,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, cfg, rank, world, local_rank)
+        if args.mode == "single":
+            run_single(args, cfg, rank, world, local_rank)
+        else:
+            run_ours(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
