@@ -333,41 +333,50 @@ ozfft_status ozfft_execute(const ozfft_plan* pl, const void* in, void* out, int 
   return OZFFT_OK;
 }
 
+// Concurrent host pipeline (the whole batch fits one workspace chunk): sub-batches use
+// disjoint workspace and staging slots, so they need no slot-reuse waits and alternate
+// between two compute streams -- the small first / last sub-batches (short pipeline fill
+// and drain) overlap the large ones on the GPU instead of running it half-empty.
+// Host-buffer pipeline: the batch runs as sub-batches (small first and last ones shorten
+// the fill -- the first H2D -- and the drain -- the last D2H); sub-batch j uses staging and
+// workspace slot j mod nslots and alternates between two compute streams, so H2D, D2H and
+// the kernels of neighbouring sub-batches overlap, and the small edge sub-batches share the
+// GPU with large ones instead of running it half-empty.  Slot reuse waits for the previous
+// occupant's kernels (input consumed) and D2H (output and workspace free).
 ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* out, int direction,
                                 void* stream) {
   ozfft_status s = check_exec(pl, in, out, direction);
   if (s) return s;
   ozfft_plan* mp = const_cast<ozfft_plan*>(pl);
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t n = pl->n;
-  // sub-batch schedule: small first/last sub-batches shorten the pipeline fill (first H2D)
-  // and drain (last D2H); the middle ones are large enough to keep the GPU busy.  Staging
-  // slots (a ring of nslots x sb transforms) live in the io_in / io_out areas.
-  const int64_t sb = std::max<int64_t>(1, std::min<int64_t>(pl->chunk, (pl->batch + 3) / 4));
+  const int64_t n = pl->n, B = pl->batch;
   std::vector<int64_t> sizes;
   {
-    const bool ramp = pl->batch >= 2 * sb + 4 && sb > 2;
-    int64_t rem = pl->batch - (ramp ? 4 : 0);
-    if (ramp) { sizes.push_back(1); sizes.push_back(2); }
+    const int64_t big = std::max<int64_t>(1, std::min<int64_t>((B + 3) / 4, std::max<int64_t>(1, pl->chunk / 3)));
+    const int64_t edge = std::max<int64_t>(1, big / 4);
+    int64_t rem = B;
+    const bool edges = big > 1 && B >= 2 * edge + 1;
+    if (edges) { sizes.push_back(edge); rem -= 2 * edge; }
     while (rem > 0) {
-      const int64_t take = std::min(sb, rem);
+      const int64_t take = std::min(big, rem);
       sizes.push_back(take);
       rem -= take;
     }
-    if (ramp) sizes.push_back(1);
+    if (edges) sizes.push_back(edge);
   }
   const int64_t nsub = (int64_t)sizes.size();
-  const int64_t nslots = std::max<int64_t>(1, std::min<int64_t>(4, pl->chunk / sb));
-  if (!mp->pipe) {
-    mp->pipe = new HostPipe();
-    cudaStream_t a, b;
-    if (cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking) != cudaSuccess)
-      return check_cuda(cudaGetLastError(), "copy stream create");
-    mp->pipe->h2d = (void*)a;
-    mp->pipe->d2h = (void*)b;
-  }
+  const int64_t sb = *std::max_element(sizes.begin(), sizes.end());
+  const int64_t nslots = std::max<int64_t>(1, std::min<int64_t>(nsub, pl->chunk / sb));
+  if (!mp->pipe) mp->pipe = new HostPipe();
   HostPipe& hp = *mp->pipe;
+  void** streams[4] = {&hp.h2d, &hp.d2h, &hp.cs[0], &hp.cs[1]};
+  for (void** sp : streams)
+    if (!*sp) {
+      cudaStream_t cs;
+      if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+        return check_cuda(cudaGetLastError(), "pipeline stream create");
+      *sp = (void*)cs;
+    }
   while ((int64_t)hp.ev.size() < 3 * nsub + 1) {
     cudaEvent_t e;
     s = check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
@@ -376,34 +385,37 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
   }
   cudaStream_t h2d = (cudaStream_t)hp.h2d, d2h = (cudaStream_t)hp.d2h;
   auto ev = [&](int64_t k) { return (cudaEvent_t)hp.ev[k]; };
-  // copies start after everything already queued on the caller's stream
-  cudaEventRecord(ev(3 * nsub), st);
+  cudaEventRecord(ev(3 * nsub), st);  // everything already queued on the caller's stream
   cudaStreamWaitEvent(h2d, ev(3 * nsub), 0);
+  for (int c = 0; c < 2; ++c) cudaStreamWaitEvent((cudaStream_t)hp.cs[c], ev(3 * nsub), 0);
   double* din0 = reinterpret_cast<double*>(pl->ws + pl->woff.io_in);
   double* dout0 = reinterpret_cast<double*>(pl->ws + pl->woff.io_out);
   int64_t b0 = 0;
   for (int64_t j = 0; j < nsub; b0 += sizes[j], ++j) {
     const int64_t nb = sizes[j];
     const size_t bytes = (size_t)nb * n * 16;
-    double* din = din0 + 2 * (j % nslots) * sb * n;
-    double* dout = dout0 + 2 * (j % nslots) * sb * n;
-    if (j >= nslots) cudaStreamWaitEvent(h2d, ev(3 * (j - nslots) + 1), 0);  // in-slot consumed
+    const int64_t slot = (j % nslots) * sb;
+    double* din = din0 + 2 * slot * n;
+    double* dout = dout0 + 2 * slot * n;
+    cudaStream_t cs = (cudaStream_t)hp.cs[j & 1];
+    if (j >= nslots) cudaStreamWaitEvent(h2d, ev(3 * (j - nslots) + 1), 0);  // input consumed
     s = check_cuda(cudaMemcpyAsync(din, in + 2 * b0 * n, bytes, cudaMemcpyHostToDevice, h2d), "H2D");
     if (s) return s;
     cudaEventRecord(ev(3 * j + 0), h2d);
-    cudaStreamWaitEvent(st, ev(3 * j + 0), 0);
-    if (j >= nslots) cudaStreamWaitEvent(st, ev(3 * (j - nslots) + 2), 0);  // out-slot drained
+    cudaStreamWaitEvent(cs, ev(3 * j + 0), 0);
+    if (j >= nslots) cudaStreamWaitEvent(cs, ev(3 * (j - nslots) + 2), 0);  // slot drained
     ExecArgs a{};
     a.nb = nb;
     a.in = din;
     a.out = dout;
     a.b0 = b0;
+    a.ws0 = slot;
     a.direction = direction;
     a.unit_mask = 0xFF;
     a.finish = true;
-    s = launch_execute(*pl, a, stream);
+    s = launch_execute(*pl, a, (void*)cs);
     if (s) return s;
-    cudaEventRecord(ev(3 * j + 1), st);
+    cudaEventRecord(ev(3 * j + 1), cs);
     cudaStreamWaitEvent(d2h, ev(3 * j + 1), 0);
     s = check_cuda(cudaMemcpyAsync(out + 2 * b0 * n, dout, bytes, cudaMemcpyDeviceToHost, d2h), "D2H");
     if (s) return s;

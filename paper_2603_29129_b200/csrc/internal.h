@@ -68,6 +68,7 @@ struct Plan {
 struct HostPipe {
   void* h2d = nullptr;
   void* d2h = nullptr;
+  void* cs[2] = {nullptr, nullptr};  // compute streams of the concurrent schedule
   std::vector<void*> ev;  // cudaEvent_t, 3 per sub-batch
 };
 
@@ -106,6 +107,8 @@ struct ExecArgs {
   uint32_t unit_mask;  // bit (cv*2 + q): which (conv, prime) units to compute (0xFF = all)
   bool finish;         // run CRT/recombine/post-chirp
   const ozfft_taps* taps;
+  int64_t ws0 = 0;     // first transform slot of the chunked workspace regions used
+                       // (ws0 + nb <= chunk); disjoint slots may run on concurrent streams
 };
 ozfft_status launch_plan_precompute(Plan& pl, void* stream);
 ozfft_status launch_execute(const Plan& pl, const ExecArgs& a, void* stream);

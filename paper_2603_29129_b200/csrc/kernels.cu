@@ -2061,11 +2061,14 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   // per-batch stats and schedules live at the transform's global index
   int32_t* stats = reinterpret_cast<int32_t*>(ws + pl.woff.stats) + A.b0 * stats_stride(K);
   int32_t* sched = reinterpret_cast<int32_t*>(ws + pl.woff.sched) + A.b0 * 4 * sched_stride(K, L);
-  unsigned long long* mu = reinterpret_cast<unsigned long long*>(ws + pl.woff.mu);
-  int32_t* digits = reinterpret_cast<int32_t*>(ws + pl.woff.digits);
-  uint32_t* Y = reinterpret_cast<uint32_t*>(ws + pl.woff.Y);
-  uint32_t* Gb = reinterpret_cast<uint32_t*>(ws + pl.woff.G);
-  uint32_t* res = reinterpret_cast<uint32_t*>(ws + pl.woff.res);
+  // chunked per-transform regions, from workspace slot A.ws0
+  const int64_t w0 = A.ws0;
+  unsigned long long* mu = reinterpret_cast<unsigned long long*>(ws + pl.woff.mu) + w0 * 2 * K;
+  int32_t* digits = reinterpret_cast<int32_t*>(ws + pl.woff.digits) + w0 * 2 * K * n;
+  uint32_t* Y = reinterpret_cast<uint32_t*>(ws + pl.woff.Y) + w0 * 4 * K * m;
+  uint32_t* Gb = reinterpret_cast<uint32_t*>(ws + pl.woff.G) + w0 * 8 * G * m;
+  uint32_t* res = reinterpret_cast<uint32_t*>(ws + pl.woff.res) + w0 * 8 * G * n;
+  double2* Sdd = reinterpret_cast<double2*>(ws + pl.woff.S) + w0 * 4 * n;
   const uint2* tw = reinterpret_cast<const uint2*>(pl.pers + pl.poff.tw);
   const uint32_t* W = reinterpret_cast<const uint32_t*>(pl.pers + pl.poff.W);
   const double2* chirp = reinterpret_cast<const double2*>(pl.pers + pl.poff.chirp);
@@ -2139,7 +2142,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     XP.logm = pl.logm; XP.K = K; XP.L = L; XP.n = n; XP.nb = nb;
     fill_crt_consts(pl, XP.F);
     XP.tw = tw; XP.G = Gb; XP.sched = sched;
-    XP.S = reinterpret_cast<double2*>(ws + pl.woff.S);
+    XP.S = Sdd;
     XP.res_tap = taps && taps->res ? res : nullptr;
     XP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
     const int cle = col_loge(pl.logR);

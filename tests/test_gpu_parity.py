@@ -153,6 +153,22 @@ def test_host_entry_point(oz):
     assert torch.equal(yh, yd)
 
 
+@pytest.mark.parametrize("n,B,ws", [(4096, 16, 0), (5000, 13, 3 << 20), (1000, 40, 0)])
+def test_host_pipeline_schedules(oz, n, B, ws):
+    """execute_host over sub-batches on two compute streams (edge sub-batches, disjoint
+    workspace slots, slot reuse when the workspace chunk is smaller than the batch) gives
+    the same bits as the device-buffer execute."""
+    x = workloads.draw("signexp", B, B, n)
+    plan = oz.Plan(n, B, max_workspace_bytes=ws)
+    xh = torch.from_numpy(x).pin_memory()
+    for _ in range(2):  # the second call reuses the pipeline's streams and events
+        yh = plan.execute_host(xh)
+    yd = plan.forward(torch.from_numpy(x).cuda()).cpu()
+    assert torch.equal(yh, yd)
+    xr = plan.execute_host(yh.pin_memory(), direction=+1)
+    assert torch.equal(xr, plan.inverse(yd.cuda()).cpu())
+
+
 def test_chunked_batch(oz):
     """A workspace budget forcing several chunks gives the same bits as one chunk."""
     n, B = 5000, 7
