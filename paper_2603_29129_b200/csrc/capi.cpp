@@ -356,13 +356,29 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
     const int64_t edge = std::max<int64_t>(1, big / 4);
     int64_t rem = B;
     const bool edges = big > 1 && B >= 2 * edge + 1;
+    const int64_t ramp = big - 1;  // second / second-to-last: slightly below big (measured)
+    const bool ramps = edges && ramp > edge && B - 2 * edge >= 2 * ramp + big;
     if (edges) { sizes.push_back(edge); rem -= 2 * edge; }
+    if (ramps) { sizes.push_back(ramp); rem -= 2 * ramp; }
     while (rem > 0) {
       const int64_t take = std::min(big, rem);
       sizes.push_back(take);
       rem -= take;
     }
+    if (ramps) sizes.push_back(ramp);
     if (edges) sizes.push_back(edge);
+    if (const char* t = std::getenv("OZFFT_HOST_SUBS")) {  // tuning knob (tools/), "1,4,4,..."
+      std::vector<int64_t> v;
+      int64_t tot = 0;
+      for (const char* c = t; *c;) {
+        const int64_t k = std::strtoll(c, const_cast<char**>(&c), 10);
+        if (k <= 0) break;
+        v.push_back(k);
+        tot += k;
+        if (*c == ',') ++c;
+      }
+      if (tot == B && *std::max_element(v.begin(), v.end()) <= pl->chunk) sizes = v;
+    }
   }
   const int64_t nsub = (int64_t)sizes.size();
   const int64_t sb = *std::max_element(sizes.begin(), sizes.end());
