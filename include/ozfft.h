@@ -24,6 +24,10 @@
  *     its workspace.  execute never allocates, never synchronizes the host, and
  *     never falls back to the CPU.
  *   - A plan is immutable after bind; one execute at a time per bound workspace.
+ *   - Plan options (descriptor): conv_mode (padded m >= 2n-1 / the paper's cyclic m = n),
+ *     accum_mode (the paper's four real convolutions / complex images), precision
+ *     (double-double / the paper's triple-single) -- see the OZFFT_CONV_*, OZFFT_ACCUM_*
+ *     and OZFFT_PREC_* blocks below; the defaults are the north star's path.
  */
 #ifndef OZFFT_H
 #define OZFFT_H
@@ -178,10 +182,14 @@ ozfft_status ozfft_plan_bind(ozfft_plan* plan, void* persistent, size_t persiste
 ozfft_status ozfft_execute(const ozfft_plan* plan, const void* in, void* out, int direction,
                            void* stream);
 
-/* Same as ozfft_execute but `in`/`out` are HOST buffers (ideally pinned): the
- * host->device copy of the inputs and the device->host copy of the outputs are
- * issued on `stream` around the device pipeline; returns after the D2H copy has
- * completed (synchronizes `stream`).  Uses the workspace's staging area. */
+/* Same as ozfft_execute but `in`/`out` are HOST buffers (pinned for overlap): the batch
+ * runs as sub-batches (small first and last ones) in disjoint staging + workspace slots;
+ * host->device copies, the device pipeline (alternating between two internal compute
+ * streams) and device->host copies of neighbouring sub-batches overlap.  Ordered after
+ * the work already queued on `stream`; returns after the last D2H copy has completed
+ * (synchronizes `stream`).  Uses the workspace's staging area.  Env OZFFT_HOST_SUBS
+ * ("1,3,4,...", summing to the batch) overrides the sub-batch sizes (tuning only).
+ * Errors: NOT_BOUND, INVALID_ARGUMENT, CUDA. */
 ozfft_status ozfft_execute_host(const ozfft_plan* plan, const double* in, double* out,
                                 int direction, void* stream);
 
