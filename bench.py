@@ -172,6 +172,7 @@ def run_reference(args, cfg, rank, world):
         ts.append(t[0])
     tot = sum(ts)
     value = units * args.steps * flops_per_transform(cfg.n) / tot / 1e9
+    t1, _, _ = time_oracle(cfg, 1, nthreads=1)  # single-thread time of one transform
     sample = (f"{ntrans} of the {cfg.batch} transforms of {cfg.name} per step "
               f"({'fwd+inv' if cfg.roundtrip else 'fwd'}), OpenMP over transforms")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
@@ -181,7 +182,8 @@ def run_reference(args, cfg, rank, world):
             "config": {"workload": workload_desc(cfg), "n": cfg.n, "batch": cfg.batch, "K": 3,
                        "L": 3, "impl": "CPU oracle (oracle/ozfft_oracle.c)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample,
+                             "single_thread_s_per_transform": t1[0] / (2 if cfg.roundtrip else 1)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -205,8 +207,24 @@ def run_single(args, cfg, rank, world, local_rank):
     plan = oz.Plan(n, 1, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        return ozd.gpu_sharded_forward(plan, x, rank, world)
+    nwords = plan.shard_residue_bytes() // 4
+    residues = torch.empty(nwords, dtype=torch.int32, device=dev)
+    out = torch.empty(n, dtype=torch.complex128, device=dev)
+    ag = []  # (start, end) events around the all-gather of each timed step
+
+    def step(record=False):
+        plan.shard_partial(x, rank, world, residues)
+        if world > 1:
+            per = nwords // world
+            mine = residues[rank * per:(rank + 1) * per].clone()
+            if record:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            dist.all_gather_into_tensor(residues, mine)
+            if record:
+                e1.record(stream)
+                ag.append((e0, e1))
+        return plan.shard_finish(residues, out)
 
     for _ in range(max(args.warmup, 3)):
         y = step()
@@ -221,15 +239,22 @@ def run_single(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     for i in range(args.steps):
         ev[i][0].record(stream)
-        step()
+        step(record=True)
         ev[i][1].record(stream)
     torch.cuda.synchronize(dev)
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    ag_ms = sum(a.elapsed_time(b) for a, b in ag)
     if dist:
-        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([t_ms, ag_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
+        t_ms, ag_ms = float(t[0].item()), float(t[1].item())
     if rank == 0:
+        nbytes = plan.shard_residue_bytes()
+        ag_per = ag_ms / args.steps
+        allgather = {"ms_per_step": ag_per, "bytes": nbytes,
+                     "busbw_GBs": (nbytes * (world - 1) / world) / (ag_per * 1e-3) / 1e9 if ag_per > 0 else None,
+                     "note": "NCCL all_gather_into_tensor of the inverse-NTT residues, CUDA events "
+                             "on the stream, max over ranks; busBW = bytes (N-1)/N / time"}
         line = {"metric": METRIC, "value": args.steps * flops_per_transform(n) / (t_ms * 1e-3) / 1e9,
                 "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
                 "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
@@ -239,7 +264,8 @@ def run_single(args, cfg, rank, world, local_rank):
                                        "all-gather of the residues before CRT",
                            "n": n, "m": plan.m, "parallelism": f"unit-sharded x{world}",
                            "residue_bytes_gathered": plan.shard_residue_bytes()},
-                "gpu_launches": int(oz.kernel_launches() - launches0)}
+                "gpu_launches": int(oz.kernel_launches() - launches0),
+                "allgather": allgather if world > 1 else None}
         print(json.dumps(line), flush=True)
 
 
@@ -286,6 +312,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             ev[i][1].record(stream)
         torch.cuda.synchronize(dev)
     launches = oz.kernel_launches() - launches0
+    per_step = sorted(a.elapsed_time(b) for a, b in ev)
+    step_ms = {"median": statistics.median(per_step), "min": per_step[0], "max": per_step[-1],
+               "note": "rank-local CUDA-event time of each timed step (rank 0)"}
     prof = plan.profile_read()
     plan.profile(False)
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
@@ -447,7 +476,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     clocks = sampler.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "step_ms": step_ms,
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": workload_desc(cfg), "n": n, "m": m, "batch_per_gpu": B,
                    "global_batch": world * B, "K": plan.K, "L": plan.L, "alpha": plan.alpha,
