@@ -170,7 +170,8 @@ ozfft_status ozfft_plan_get_info(const ozfft_plan* plan, ozfft_plan_info* info);
 /* Bind caller-owned device memory (persistent >= info.persistent_bytes, workspace >=
  * info.workspace_bytes, both 256-byte aligned) and precompute on `stream`: uploads
  * tables, splits omega~* (Alg.6) and runs its 4K forward NTTs into the
- * cached W spectra.  Synchronizes `stream` once (plan time, not on the hot path).
+ * cached W spectra, using the workspace as scratch (no device allocation).
+ * Synchronizes `stream` (plan time, not on the hot path).
  * Errors: INVALID_ARGUMENT, MISALIGNED, BUFFER_TOO_SMALL, CUDA. */
 ozfft_status ozfft_plan_bind(ozfft_plan* plan, void* persistent, size_t persistent_bytes,
                              void* workspace, size_t workspace_bytes, void* stream);

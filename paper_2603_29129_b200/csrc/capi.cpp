@@ -110,7 +110,12 @@ static void layout(Plan& pl) {
   pl.woff.io_in = o;  o = align256(o + (uint64_t)chunk * n * 16);
   pl.woff.io_out = o; o = align256(o + (uint64_t)chunk * n * 16);
   pl.woff.end = o;
-  pl.workspace_bytes = o;
+  // bind-time scratch (launch_plan_precompute: mu, digits, stats, Y, X of omega~*) reuses
+  // the workspace before the first execute
+  const uint64_t bind_scratch = align256((uint64_t)2 * K * 8) + align256((uint64_t)2 * K * m * 4) +
+                                align256((uint64_t)stats_stride(K) * 4) +
+                                2 * align256((uint64_t)4 * K * m * 4);
+  pl.workspace_bytes = std::max<uint64_t>(o, bind_scratch);
 }
 
 static ozfft_status check_cuda(cudaError_t e, const char* what) {
@@ -294,8 +299,9 @@ ozfft_status ozfft_plan_bind(ozfft_plan* pl, void* persistent, size_t pbytes, vo
     s = check_cuda(cudaMemcpyAsync(pl->pers + pl->poff.W, pl->wstar.data(), (size_t)m * 16,
                                    cudaMemcpyHostToDevice, st),
                    "upload omega~*");
+  if (!s) s = launch_plan_precompute(*pl, stream);  // uses the workspace as scratch
   if (!s) s = check_cuda(cudaMemsetAsync(pl->ws, 0, pl->woff.mu, st), "clear stats");
-  if (!s) s = launch_plan_precompute(*pl, stream);
+  if (!s) s = check_cuda(cudaStreamSynchronize(st), "bind sync");
   if (s) return s;
   pl->bound = true;
   return OZFFT_OK;

@@ -1986,17 +1986,19 @@ ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t m = pl.m;
   const int K = pl.K;
-  // scratch (plan time only)
-  unsigned long long* mu = nullptr;
-  int32_t *digits = nullptr, *stats = nullptr;
-  uint32_t *Y = nullptr, *X = nullptr;
-  if (cudaMalloc(&mu, sizeof(unsigned long long) * 2 * K) ||
-      cudaMalloc(&digits, sizeof(int32_t) * 2 * K * m) ||
-      cudaMalloc(&stats, sizeof(int32_t) * stats_stride(K)) ||
-      cudaMalloc(&Y, sizeof(uint32_t) * 4 * K * m) || cudaMalloc(&X, sizeof(uint32_t) * 4 * K * m)) {
-    set_error("cudaMalloc failed in plan precompute");
-    return OZFFT_ERR_CUDA;
-  }
+  // scratch (plan time only): carved from the caller's workspace, which is free before the
+  // first execute and sized for it (capi.cpp layout(): bind_scratch_bytes)
+  uint8_t* sc = pl.ws;
+  auto carve = [&](size_t bytes) {
+    uint8_t* p = sc;
+    sc += (bytes + 255) & ~(size_t)255;
+    return p;
+  };
+  unsigned long long* mu = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * 2 * K));
+  int32_t* digits = reinterpret_cast<int32_t*>(carve(sizeof(int32_t) * 2 * K * m));
+  int32_t* stats = reinterpret_cast<int32_t*>(carve(sizeof(int32_t) * stats_stride(K)));
+  uint32_t* Y = reinterpret_cast<uint32_t*>(carve(sizeof(uint32_t) * 4 * K * m));
+  uint32_t* X = reinterpret_cast<uint32_t*>(carve(sizeof(uint32_t) * 4 * K * m));
   cudaMemsetAsync(mu, 0, sizeof(unsigned long long) * 2 * K, st);
   cudaMemsetAsync(X, 0, sizeof(uint32_t) * 4 * K * m, st);
   SplitParams SP{};
@@ -2045,11 +2047,6 @@ ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
     s = cuda_check("W finalize");
     if (!s && cudaStreamSynchronize(st) != cudaSuccess) s = cuda_check("plan precompute sync");
   }
-  cudaFree(mu);
-  cudaFree(digits);
-  cudaFree(stats);
-  cudaFree(Y);
-  cudaFree(X);
   return s;
 }
 
