@@ -584,6 +584,8 @@ ozfft_status ozfft_plan_destroy(ozfft_plan* pl) {
     for (void* e : pl->pipe->ev) cudaEventDestroy((cudaEvent_t)e);
     if (pl->pipe->h2d) cudaStreamDestroy((cudaStream_t)pl->pipe->h2d);
     if (pl->pipe->d2h) cudaStreamDestroy((cudaStream_t)pl->pipe->d2h);
+    for (void* cs : pl->pipe->cs)
+      if (cs) cudaStreamDestroy((cudaStream_t)cs);
     delete pl->pipe;
   }
   if (pl && pl->prof) {
