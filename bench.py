@@ -282,7 +282,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     x_np = workloads.draw(cfg.dist, cfg.seed, world * B, n, rows=slice(rank * B, (rank + 1) * B)) \
         if world > 1 else workloads.config_input(cfg)
     x = torch.from_numpy(x_np).to(dev)
-    plan = oz.Plan(n, B, device=dev, conv=args.conv, accum=args.accum)
+    plan = oz.Plan(n, B, device=dev, conv=args.conv, accum=args.accum, precision=args.precision)
     out = torch.empty_like(x)
     back = torch.empty_like(x) if cfg.roundtrip else None
     stream = torch.cuda.current_stream(dev)
@@ -372,9 +372,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         "col_inv": (inv_vec * 4 * (m + n), inv_vec * (m // 2) * logR),
         "crt_finish": (inv_vec * 4 * n + 32 * n * B, 0),
     }
+    nsums = 2 if args.accum == "image" else 4  # DD sums per transform: Re, Im (f2) or rr, ii, ir, ri
     if logR > 0:  # fused inverse column pass + CRT + DD accumulation; finish reads the DD sums
-        per_exec["col_inv"] = (inv_vec * 4 * m + 64 * n * B, inv_vec * (m // 2) * logR)
-        per_exec["crt_finish"] = (80 * n * B + 16 * n, 0)  # S (4 DD) + out per transform, chirp once
+        per_exec["col_inv"] = (inv_vec * 4 * m + 16 * nsums * n * B, inv_vec * (m // 2) * logR)
+        per_exec["crt_finish"] = ((16 * nsums + 16) * n * B + 16 * n, 0)  # sums + out, chirp once
     hbm, hbm_kind = hbm_peak()
     stages = {}
     for s, (ms, cnt) in prof.items():
@@ -465,7 +466,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     pow2 = n > 1 and n & (n - 1) == 0
     cyc = img = imgc = None
-    if args.conv == "padded" and args.accum == "real" and not args.no_extra:
+    if args.conv == "padded" and args.accum == "real" and args.precision == "dd" and not args.no_extra:
         if pow2:
             cyc = side("cyclic", "real")
             cyc["note"] = "paper's N = n cyclic Bluestein (P:238-241); bitwise equal to the headline"
@@ -484,7 +485,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "ntt_split": f"m = 2^{logR} x 2^{logC}", "parallelism": f"batch-sharded x{world}",
                    "directions": "fwd+inv" if cfg.roundtrip else "fwd",
                    "l2": "flushed between timed steps (512 MiB write outside the events)",
-                   "io_dtype": "complex128", "conv": args.conv, "accum": args.accum},
+                   "io_dtype": "complex128", "conv": args.conv, "accum": args.accum,
+                   "precision": args.precision},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
                 "d2h_bytes_per_step": io_bytes, "steps": e2e_steps},
         "gpu_launches": int(launches),
@@ -514,6 +516,8 @@ def main():
     ap.add_argument("--mode", default="batch", choices=["batch", "single"],
                     help="batch: weak-scaled batches (the headline); single: one transform "
                          "sharded over the ranks with an NCCL all-gather (SURVEY 8(e))")
+    ap.add_argument("--precision", default="dd", choices=["dd", "ts"],
+                    help="double-double O(n) steps (default) or the paper's triple-single (f4)")
     ap.add_argument("--accum", default="real", choices=["real", "image"],
                     help="four real convolutions (the paper) or complex images (SURVEY f2)")
     ap.add_argument("--no-extra", action="store_true",

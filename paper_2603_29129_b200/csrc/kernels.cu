@@ -785,6 +785,9 @@ __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32
 #ifndef OZ_CI_PF
 #define OZ_CI_PF 0
 #endif
+#ifndef OZ_IMG_CB_SHIFT
+#define OZ_IMG_CB_SHIFT 1
+#endif
 #ifndef OZ_CI_MINB
 #define OZ_CI_MINB 3
 #endif
@@ -1570,10 +1573,18 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
 // (image +, p1), (image -, p1) are transformed in turn (next tile prefetched); each prime's
 // image pair gives (re, im) residues, the primes' pairs give Re and Im by Garner, and the
 // DD sums of Re 2^-c and Im 2^-c in flush order go to S[b][0] and S[b][1].
+// Column block of the image kernel: half the real-mode width (>= 8 columns, one 32-byte
+// sector per row segment) -- its accumulators are twice as many (Re and Im sums), so the
+// narrower block keeps more CTAs resident.
+__host__ __device__ constexpr int col_log_cb_img(int logR, int logC) {
+  return col_log_cb(logR, logC) - OZ_IMG_CB_SHIFT >= 3 ? col_log_cb(logR, logC) - OZ_IMG_CB_SHIFT
+                                                        : (col_log_cb(logR, logC) < 3 ? col_log_cb(logR, logC) : 3);
+}
+
 template <int LOGR, int LOGC, bool PRUNE>
 __global__ void __launch_bounds__(256, 2) k_col_inv_crt_img(ColCrtParams P) {
   extern __shared__ uint32_t smem[];
-  constexpr int LOGCB = col_log_cb(LOGR, LOGC);
+  constexpr int LOGCB = col_log_cb_img(LOGR, LOGC);
   constexpr int LOGE = col_loge(LOGR);
   constexpr int E = 1 << LOGE;
   constexpr int Cb = 1 << LOGCB;
@@ -2143,20 +2154,22 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     XP.res_tap = taps && taps->res ? res : nullptr;
     XP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
     const int cle = col_loge(pl.logR);
-    const size_t tile = ((1ull << pl.logR) + ((1ull << pl.logR) >> cle) + 1) * (1ull << c.logCb);
+    const int lcb = pl.image ? col_log_cb_img(pl.logR, pl.logC) : c.logCb;
+    const int threads = col_threads(pl.logR, lcb);
+    const size_t tile = ((1ull << pl.logR) + ((1ull << pl.logR) >> cle) + 1) * (1ull << lcb);
     const bool prune = 2 * n <= m;  // padded plans; cyclic plans (m = n) need every row
     const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / (prune ? 2 : 1);
-    const size_t smem = (tile + (tile & 1)) * 4 + (size_t)nh * c.col_threads * 16 * (pl.image ? 2 : 1);
-    const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * (pl.image ? 1 : 4);
+    const size_t smem = (tile + (tile & 1)) * 4 + (size_t)nh * threads * 16 * (pl.image ? 2 : 1);
+    const int64_t nblk = (1ll << (pl.logC - lcb)) * nb * (pl.image ? 1 : 4);
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
     dispatch_rc(pl.logR, pl.logC, [&](auto I, auto J) {
       {
         if (pl.image && prune) {
           set_smem(k_col_inv_crt_img<I.value, J.value, true>, smem);
-          k_col_inv_crt_img<I.value, J.value, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+          k_col_inv_crt_img<I.value, J.value, true><<<(unsigned)nblk, threads, smem, st>>>(XP);
         } else if (pl.image) {
           set_smem(k_col_inv_crt_img<I.value, J.value, false>, smem);
-          k_col_inv_crt_img<I.value, J.value, false><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+          k_col_inv_crt_img<I.value, J.value, false><<<(unsigned)nblk, threads, smem, st>>>(XP);
         } else if (prune && pl.ts) {
           set_smem(k_col_inv_crt<I.value, J.value, true, true>, smem);
           k_col_inv_crt<I.value, J.value, true, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
