@@ -429,8 +429,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     #              bitwise equal to the headline's (tests/test_gpu_cyclic.py);
     #   f2_image:  complex-image accumulation (beyond the paper; own oracle mode,
     #              tests/test_gpu_image.py), padded and, for power-of-two n, cyclic.
-    def side(conv, accum):
-        pc = oz.Plan(n, B, device=dev, conv=conv, accum=accum)
+    def side(conv, accum, precision="dd"):
+        pc = oz.Plan(n, B, device=dev, conv=conv, accum=accum, precision=precision)
 
         def cstep():
             pc.forward(x, out=out)
@@ -458,14 +458,14 @@ def run_ours(args, cfg, rank, world, local_rank):
         st = pc.stats()
         r = {"value": total_transforms * flops_per_transform(n) / (c_ms * 1e-3) / 1e9,
              "unit": UNIT, "ms_per_step": c_ms / args.steps, "m": pc.m, "alpha": pc.alpha,
-             "conv": conv, "accum": accum,
+             "conv": conv, "accum": accum, "precision": precision,
              "ntt_split": f"m = 2^{pc.log2_rows} x 2^{pc.log2_cols}",
              "ntts_per_transform": (st["fwd_ntts"] + st["inv_ntts"]) / B}
         del pc
         return r
 
     pow2 = n > 1 and n & (n - 1) == 0
-    cyc = img = imgc = None
+    cyc = img = imgc = tsl = None
     if args.conv == "padded" and args.accum == "real" and args.precision == "dd" and not args.no_extra:
         if pow2:
             cyc = side("cyclic", "real")
@@ -474,6 +474,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         img["note"] = "complex-image accumulation (SURVEY f2; beyond the paper; own oracle mode)"
         if pow2:
             imgc = side("cyclic", "image")
+        tsl = side("padded", "real", "ts")
+        tsl["note"] = "the paper's triple-single working precision (SURVEY f4)"
     clocks = sampler.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -499,6 +501,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "f1_cyclic": cyc,
         "f2_image": img,
         "f1_f2_cyclic_image": imgc,
+        "f4_ts": tsl,
     }
     print(json.dumps(line), flush=True)
 
