@@ -785,6 +785,12 @@ __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32
 #ifndef OZ_CI_PF
 #define OZ_CI_PF 0
 #endif
+#ifndef OZ_CI_CB_SHIFT
+#define OZ_CI_CB_SHIFT 0
+#endif
+#ifndef OZ_CI_CB_SHIFT_FULL
+#define OZ_CI_CB_SHIFT_FULL 0
+#endif
 #ifndef OZ_IMG_CB_SHIFT
 #define OZ_IMG_CB_SHIFT 1
 #endif
@@ -1448,10 +1454,19 @@ struct ColCrtParams {
   int64_t* crt_tap;        // null, or [nb][4][K*K][n]
 };
 
+// Column block of the fused inverse column kernel (real mode): the real-mode column width,
+// narrowed by OZ_CI_CB_SHIFT (pruned plans) / OZ_CI_CB_SHIFT_FULL (unpruned, twice the
+// accumulators) down to >= 8 columns.
+__host__ __device__ constexpr int col_log_cb_ci(int logR, int logC, bool prune) {
+  return col_log_cb(logR, logC) - (prune ? OZ_CI_CB_SHIFT : OZ_CI_CB_SHIFT_FULL) >= 3
+             ? col_log_cb(logR, logC) - (prune ? OZ_CI_CB_SHIFT : OZ_CI_CB_SHIFT_FULL)
+             : (col_log_cb(logR, logC) < 3 ? col_log_cb(logR, logC) : 3);
+}
+
 template <int LOGR, int LOGC, bool PRUNE, bool TS>
 __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_inv_crt(ColCrtParams P) {
   extern __shared__ uint32_t smem[];
-  constexpr int LOGCB = col_log_cb(LOGR, LOGC);
+  constexpr int LOGCB = col_log_cb_ci(LOGR, LOGC, PRUNE);
   constexpr int LOGE = col_loge(LOGR);
   constexpr int E = 1 << LOGE;
   constexpr int Cb = 1 << LOGCB;
@@ -2154,7 +2169,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     XP.res_tap = taps && taps->res ? res : nullptr;
     XP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
     const int cle = col_loge(pl.logR);
-    const int lcb = pl.image ? col_log_cb_img(pl.logR, pl.logC) : c.logCb;
+    const int lcb = pl.image ? col_log_cb_img(pl.logR, pl.logC) : col_log_cb_ci(pl.logR, pl.logC, 2 * n <= m);
     const int threads = col_threads(pl.logR, lcb);
     const size_t tile = ((1ull << pl.logR) + ((1ull << pl.logR) >> cle) + 1) * (1ull << lcb);
     const bool prune = 2 * n <= m;  // padded plans; cyclic plans (m = n) need every row
@@ -2172,16 +2187,16 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
           k_col_inv_crt_img<I.value, J.value, false><<<(unsigned)nblk, threads, smem, st>>>(XP);
         } else if (prune && pl.ts) {
           set_smem(k_col_inv_crt<I.value, J.value, true, true>, smem);
-          k_col_inv_crt<I.value, J.value, true, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+          k_col_inv_crt<I.value, J.value, true, true><<<(unsigned)nblk, threads, smem, st>>>(XP);
         } else if (pl.ts) {
           set_smem(k_col_inv_crt<I.value, J.value, false, true>, smem);
-          k_col_inv_crt<I.value, J.value, false, true><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+          k_col_inv_crt<I.value, J.value, false, true><<<(unsigned)nblk, threads, smem, st>>>(XP);
         } else if (prune) {
           set_smem(k_col_inv_crt<I.value, J.value, true, false>, smem);
-          k_col_inv_crt<I.value, J.value, true, false><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+          k_col_inv_crt<I.value, J.value, true, false><<<(unsigned)nblk, threads, smem, st>>>(XP);
         } else {
           set_smem(k_col_inv_crt<I.value, J.value, false, false>, smem);
-          k_col_inv_crt<I.value, J.value, false, false><<<(unsigned)nblk, c.col_threads, smem, st>>>(XP);
+          k_col_inv_crt<I.value, J.value, false, false><<<(unsigned)nblk, threads, smem, st>>>(XP);
         }
       }
     });
