@@ -189,3 +189,21 @@ def test_error_vs_float128(oz):
         eo = np.max(np.abs((yo - hi) - lo)) / np.max(np.abs(hi))
         eg = np.max(np.abs((y - hi) - lo)) / np.max(np.abs(hi))
         assert eg <= 2 * eo + 1e-300 and eg <= 1e-15, (n, eg, eo)
+
+
+@pytest.mark.parametrize("conv,accum,precision", [("padded", "image", "dd"), ("cyclic", "image", "dd"),
+                                                  ("padded", "real", "ts"), ("cyclic", "real", "ts")])
+def test_modes_chunked_and_host(oz, conv, accum, precision):
+    """Every plan mode through the chunked workspace and the host pipeline gives the bits of
+    a one-chunk device execute."""
+    n, B = 4096, 9
+    x = workloads.draw("normal", 31, B, n)
+    kw = dict(conv=conv, accum=accum, precision=precision)
+    full = oz.Plan(n, B, **kw)
+    small = oz.Plan(n, B, max_workspace_bytes=8 << 20, **kw)
+    assert small.chunk < B
+    xd = torch.from_numpy(x).cuda()
+    ref = full.forward(xd)
+    assert torch.equal(small.forward(xd), ref)
+    assert torch.equal(small.execute_host(torch.from_numpy(x).pin_memory()), ref.cpu())
+    assert torch.equal(full.execute_host(torch.from_numpy(x).pin_memory()), ref.cpu())
