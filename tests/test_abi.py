@@ -104,3 +104,31 @@ def test_plan_create_validation(lib):
     assert create(n=1024, precision=1, accum_mode=1)[0] == 1  # TS with the real mode only
     assert create(n=1024, accum_mode=1, p0=2130706433, p1=2013265921)[0] == 0  # 15*2^27+1
     assert create(n=1024, accum_mode=1, p0=2130706433, p1=2147483647)[0] == 3  # 2^31-1 = 3 mod 4
+
+
+def test_entry_point_errors_without_device(lib):
+    """Synchronous argument errors of the execute / bind / shard / stats entry points (no
+    device memory is touched before these checks)."""
+    import paper_2603_29129_b200 as oz
+    L = oz.load_library()
+    d = oz.PlanDesc(n=1000, batch=2, K=3, L=3, p0=0, p1=0, device=0, conv_mode=0, accum_mode=0,
+                    precision=0, max_workspace_bytes=0)
+    h = ctypes.c_void_p()
+    assert L.ozfft_plan_create(ctypes.byref(d), ctypes.byref(h)) == 0
+    buf = ctypes.c_void_p(1 << 20)  # never dereferenced: the checks fail first
+    assert L.ozfft_execute(h, buf, buf, -1, None) == 5          # NOT_BOUND
+    assert L.ozfft_execute_host(h, buf, buf, -1, None) == 5
+    assert L.ozfft_shard_partial(h, 0, 2, buf, -1, buf, None) == 5
+    st = oz.ExecStats()
+    assert L.ozfft_last_stats(h, ctypes.byref(st), None) == 5
+    assert L.ozfft_plan_bind(h, None, 0, None, 0, None) == 1    # null buffers
+    assert L.ozfft_plan_bind(h, ctypes.c_void_p(257), 1 << 30, ctypes.c_void_p(512), 1 << 30, None) == 6
+    info = oz.PlanInfo()
+    assert L.ozfft_plan_get_info(h, ctypes.byref(info)) == 0
+    assert L.ozfft_plan_bind(h, ctypes.c_void_p(256), info.persistent_bytes - 1, ctypes.c_void_p(512),
+                             info.workspace_bytes, None) == 9   # BUFFER_TOO_SMALL
+    assert L.ozfft_execute(None, buf, buf, -1, None) == 1
+    assert b"null plan" in L.ozfft_last_error_string()
+    assert L.ozfft_status_string(9) == b"OZFFT_ERR_BUFFER_TOO_SMALL"
+    assert L.ozfft_plan_destroy(h) == 0
+    assert L.ozfft_plan_destroy(None) == 0
