@@ -1241,7 +1241,9 @@ __device__ __forceinline__ void image_pair(uint32_t zp, uint32_t zm, uint2 inv2,
 // in [0, p0 p1), then the symmetric representative in [-p0p1/2, p0p1/2) (
 // it is unique, so this equals the symmetric-Garner form of the oracle).
 __device__ __forceinline__ long long garner2(uint32_t z0, uint32_t z1, const FinishParams& P) {
-  const uint32_t z0r = z0 >= P.p1 ? z0 - P.p1 : z0;  // z0 mod p1 (z0 < p0 < 2 p1)
+  // z0 mod p1: one conditional subtraction when p0 < 2 p1 (the paper's primes), else a
+  // remainder (custom prime pairs)
+  const uint32_t z0r = P.p0 < 2ull * P.p1 ? (z0 >= P.p1 ? z0 - P.p1 : z0) : z0 % P.p1;
   const uint32_t d = sub_mod(z1, z0r, P.p1);
   const uint32_t t = mul_shoup(d, make_uint2(P.p0inv, P.p0inv_sh), P.p1);
   const unsigned long long Zp = (unsigned long long)z0 + (unsigned long long)P.p0 * t;

@@ -207,3 +207,20 @@ def test_modes_chunked_and_host(oz, conv, accum, precision):
     assert torch.equal(small.forward(xd), ref)
     assert torch.equal(small.execute_host(torch.from_numpy(x).pin_memory()), ref.cpu())
     assert torch.equal(full.execute_host(torch.from_numpy(x).pin_memory()), ref.cpu())
+
+
+@pytest.mark.parametrize("p0,p1", [(2013265921, 1811939329), (2130706433, 998244353),
+                                   (998244353, 2113929217)])
+def test_custom_primes(oz, p0, p1):
+    """User-chosen NTT primes (desc.p0 / p1): bit-exact against the oracle with
+    the same primes, including p0 > 2 p1 (Garner's z0 mod p1 is a full remainder there)."""
+    n, B = 1000, 2
+    x = workloads.draw("normal", 17, B, n)
+    plan = oz.Plan(n, B, p0=p0, p1=p1)
+    op = O.Plan(n, p0=p0, p1=p1)
+    assert plan.alpha == op.alpha
+    y, gt = plan.execute_taps(torch.from_numpy(x).cuda())
+    for b in range(B):
+        yo, ot = op.execute(x[b], taps=True)
+        check_taps(gt, ot, n, 3, b)
+        assert np.array_equal(y[b].cpu().numpy(), yo)
