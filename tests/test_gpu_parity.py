@@ -224,3 +224,20 @@ def test_custom_primes(oz, p0, p1):
         yo, ot = op.execute(x[b], taps=True)
         check_taps(gt, ot, n, 3, b)
         assert np.array_equal(y[b].cpu().numpy(), yo)
+
+
+@pytest.mark.parametrize("mode", [dict(accum="image"), dict(precision="ts")])
+@pytest.mark.parametrize("K,L", [(1, 1), (2, 1), (4, 3), (8, 8)])
+def test_modes_other_K_L(oz, mode, K, L):
+    """The f2 / f4 plan modes with other split caps and accumulation bounds, wide-range
+    inputs (phi = 4): taps and output bit-exact against the oracle's mode."""
+    n, B = 700, 2
+    x = workloads.phi_input(n, 4.0, seed=K * 10 + L, batch=B)
+    plan = oz.Plan(n, B, K=K, L=L, **mode)
+    op = O.Plan(n, K, L, image=mode.get("accum") == "image", ts=mode.get("precision") == "ts")
+    y, gt = plan.execute_taps(torch.from_numpy(x).cuda())
+    for b in range(B):
+        yo, ot = op.execute(x[b], taps=True)
+        assert np.array_equal(gt["crt"][b].cpu().numpy(), ot["crt"])
+        assert np.array_equal(gt["sched"][b].cpu().numpy(), ot["sched"])
+        assert np.array_equal(y[b].cpu().numpy(), yo)
