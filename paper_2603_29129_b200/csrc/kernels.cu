@@ -1,27 +1,29 @@
 // kernels.cu -- sm_100a kernels of the ozfft hot path (arXiv 2603.29129).
 //
-//   k_split_max      a1+a2  chirp premultiply in DD (Alg.4 l.473-474) + per-level
-//                           max |hi| for the Ozaki split (Alg.6 l.778/786, eq:ts-split-mu)
-//   k_split_digits   a2     int32 digits D = fl(fl(hi+sigma)-sigma) 2^(alpha-E)
-//                           (Alg.6 l.781-785) + Alg.8 flush schedule per real conv
-//   k_col_fwd        a3     residue lift + first log2(R) DIF stages of the length-m
-//                           forward NTT (eq:ntt P:248) on column tiles (stride C)
-//   k_row_fused      a3-a5  last log2(C) DIF stages of the 2K slice NTTs of one row,
-//                           pointwise products + NTT-domain accumulation of each
-//                           Alg.8 group (l.981-982), first log2(C) DIT stages of
-//                           its inverse NTT (l.973)
-//   k_col_inv        a5     last log2(R) DIT stages of the inverse NTT, natural
-//                           order, only indices j < n written
-//   k_crt_finish     a6+a7  Garner CRT (l.974), exact power-of-two scaling, DD
-//                           accumulation in flush order (l.975-976), complex combine
-//                           (P:1012-1019), post-chirp (Alg.4 l.480-484), fp64 output
+// Default path, per execute of a batch:
+//   k_split_max<TS>       a1+a2  chirp premultiply (DD, or TS for f4) + per-level max |hi|
+//                                 of the Ozaki split (Alg.6 l.778/786), one launch per level
+//   k_split_digits<TS>    a2     int32 digits D = fl(fl(hi+sigma)-sigma) 2^(alpha-E)
+//                                 (Alg.6 l.781-785) + the Alg.8 flush schedules
+//   k_col_fwd<R,C,IMG>    a3     residue lift (or digit images, f2) + the first log2 R DIF
+//                                 stages of the length-m forward NTT on column tiles
+//   k_row_fused<C,2PASS>  a3-a5  last log2 C DIF stages of the slices of one row, pointwise
+//                                 products + NTT-domain accumulation per Alg.8 group, first
+//                                 log2 C DIT stages of each group's inverse NTT
+//   k_col_inv_crt<R,C,PRUNE,TS>  a5-a7  last log2 R DIT stages, Garner CRT, exact 2^-c
+//                                 scaling and the DD (TS) sum in flush order per real conv
+//   k_finish_dd           a7     rr - ii, ir + ri, post-chirp, fp64 (inverse: conj, 1/n)
+// Variants: k_col_inv_crt_img / k_crt_finish_img (complex images, f2), k_crt_finish(_ts)
+// (one-pass plans, m <= 4096), k_col_inv + k_crt_finish (unit-sharded single transform,
+// SURVEY 8(e)), k_w_finalize (plan time), k_tap_permute (test taps).
 //
 // NTT arithmetic: canonical residues in [0,p), Shoup multiplication by precomputed
 // twiddles, branch-free conditional subtraction via unsigned min
 // (one VIADDMNMX on sm_100a).  The forward NTT is decimation-in-frequency from
 // natural order to bit-reversed order; the inverse is decimation-in-time from
 // bit-reversed to natural order, so the pointwise stage needs no permutation.
-// m^{-1} of eq:intt is folded into the cached W spectra.
+// m^{-1} of eq:intt is folded into the cached W spectra.  Compile-time tuning knobs
+// (OZ_*) default to the measured best (DESIGN.md section 6 lists the rejected ones).
 #include <cuda_runtime.h>
 
 #include <cstdio>
