@@ -658,29 +658,6 @@ __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int
   }
 }
 
-// L1 prefetch of every twiddle a thread reads in the sub-transform (same addressing as
-// dif_group / dit_group), so that the loads of a later sub-transform hit L1 instead of L2.
-template <int LOGN, bool INV, int LOGE, int R = 0>
-__device__ __forceinline__ void prefetch_sub_ntt_tw(int tv, uint32_t gb_mod, uint32_t gs,
-                                                    const uint2* __restrict__ T) {
-  if constexpr (LOGN > 0 && R < RoundT<LOGN, INV, 0, LOGE>::nr) {
-    using RT = RoundT<LOGN, INV, R, LOGE>;
-    constexpr uint32_t step = 1u << RT::logstep;
-#pragma unroll
-    for (int u = 0; u < (RT::cnt >> RT::S); ++u) {
-      const uint32_t g = (uint32_t)(tv + u * RT::Tv);
-      const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
-      const uint32_t gstep = step * gs;
-#pragma unroll
-      for (int st = 0; st < RT::S; ++st)
-#pragma unroll
-        for (int j = 0; j < (1 << st); ++j)
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(&T[(gstep << st) + rmod + (uint32_t)j * gstep]));
-    }
-    prefetch_sub_ntt_tw<LOGN, INV, LOGE, R + 1>(tv, gb_mod, gs, T);
-  }
-}
-
 // Length-2^LOGN sub-transforms of NV vectors at the same positions, executed cooperatively
 // by 2^max(LOGN-LOGE,0) threads (index tv), 2^LOGE elements per thread and vector per round
 // in rounds of <= LOGE radix-2 stages; twiddles are loaded once for the NV vectors, and
@@ -784,9 +761,6 @@ __host__ __device__ constexpr int row_loge(int logC, bool two_pass) {
 #endif
 __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32_MIN_LOGR ? 5 : 4; }
 
-#ifndef OZ_CI_PF
-#define OZ_CI_PF 0
-#endif
 #ifndef OZ_CI_CB_SHIFT
 #define OZ_CI_CB_SHIFT 0
 #endif
@@ -971,9 +945,6 @@ struct RowParams {
   uint2 io[2][2];         // [q][image] Shoup pair of iota_q / p_q - iota_q
 };
 
-#ifndef OZ_ROW_DBUF
-#define OZ_ROW_DBUF 0
-#endif
 #ifndef OZ_ROW_QMAJOR
 #define OZ_ROW_QMAJOR 1
 #endif
@@ -1055,14 +1026,11 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   if (!P.fwd_only && !want0 && !want1) return;
   if (ka == 0 && !P.fwd_only) return;  // no slices: the schedule has no groups here
   uint32_t* Xs = smem;               // [K][C] forward spectra rows (row_perm order)
-  // [2][padC]: inter-round exchange buffers, alternating between consecutive sub-transforms
-  // so that a sub-transform's first writes never race the previous one's last reads (the
-  // sub-transform before that one ended before the CTA barrier of the previous one)
+  // [padC]: inter-round exchange buffer; a CTA barrier before each sub-transform frees it
+  // (double buffering, which would drop that barrier, measured slower: more registers)
   uint32_t* work = smem + K * C;
-  int nsub = 0;  // sub-transforms issued so far (buffer = nsub & 1)
-  constexpr uint32_t dbuf = OZ_ROW_DBUF ? padC : 0u;  // 0: one buffer, CTA barrier per sub-transform
   // group table for 2 convs x K*K groups: npairs, then (X row offset, W row offset) x L
-  uint32_t* tab = work + padC + dbuf;
+  uint32_t* tab = work + padC;
   const int tstride = 1 + 2 * L;
   for (int ci = tv; ci < 2 && !P.fwd_only; ci += blockDim.x) {  // blockDim may be 1 (C < 32)
     const int cv = ci ? cv1 : cv0;
@@ -1087,8 +1055,8 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   for (int s = 0; s < ka; ++s) {
     uint32_t* xs = Xs + s * C;
     uint32_t* outX = P.Xout ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff : nullptr;
-    uint32_t* wk = work + (nsub++ & 1) * dbuf;
-    if (!OZ_ROW_DBUF && s > 0) __syncthreads();  // `work` free (previous last reads done)
+    uint32_t* wk = work;
+    if (s > 0) __syncthreads();  // `work` free (previous last reads done)
     auto store_x = [&](int i, uint32_t e, uint32_t v) {
       xs[row_slot<LOGC, TWO_PASS>(tv, i)] = v;  // == row_perm(e)
       if (outX) outX[e] = v;
@@ -1173,8 +1141,8 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   // (processing two items at once with sub_ntt_multi<..., 2> shares twiddles and barriers
   // but measured slower on B200 -- fewer resident CTAs -- so items run one at a time)
   for (int it = 0; it < nitems; ++it) {
-    uint32_t* wk = work + (nsub++ & 1) * dbuf;
-    if (!OZ_ROW_DBUF && it > 0) __syncthreads();  // exchange buffer free
+    uint32_t* wk = work;
+    if (it > 0) __syncthreads();  // exchange buffer free
     int ci0, g0;
     item(it, ci0, g0);
     uint32_t z[E];
@@ -1198,6 +1166,7 @@ struct FinishParams {
   int64_t n, nb;
   int K, L;
   uint32_t p0, p1, p0inv, p0inv_sh;  // p0^{-1} mod p1 and its Shoup companion
+  uint32_t p1_barrett;               // floor(2^32 / p1)
   unsigned long long P, halfP;       // p0 p1 and (p0 p1 - 1) / 2
   const uint32_t* res;      // [nb][4][2][K*K][n]
   const int32_t* stats;
@@ -1243,9 +1212,11 @@ __device__ __forceinline__ void image_pair(uint32_t zp, uint32_t zm, uint2 inv2,
 // in [0, p0 p1), then the symmetric representative in [-p0p1/2, p0p1/2) (
 // it is unique, so this equals the symmetric-Garner form of the oracle).
 __device__ __forceinline__ long long garner2(uint32_t z0, uint32_t z1, const FinishParams& P) {
-  // z0 mod p1: one conditional subtraction when p0 < 2 p1 (the paper's primes), else a
-  // remainder (custom prime pairs)
-  const uint32_t z0r = P.p0 < 2ull * P.p1 ? (z0 >= P.p1 ? z0 - P.p1 : z0) : z0 % P.p1;
+  // z0 mod p1 for any prime pair: Barrett with c = floor(2^32 / p1) leaves r < 2 p1, one
+  // conditional subtraction finishes (for the paper's primes c = 2 and z0 < 2^31, so q = 0)
+  const uint32_t q0 = __umulhi(z0, P.p1_barrett);
+  uint32_t z0r = z0 - q0 * P.p1;
+  z0r = min(z0r, z0r - P.p1);
   const uint32_t d = sub_mod(z1, z0r, P.p1);
   const uint32_t t = mul_shoup(d, make_uint2(P.p0inv, P.p0inv_sh), P.p1);
   const unsigned long long Zp = (unsigned long long)z0 + (unsigned long long)P.p0 * t;
@@ -1528,12 +1499,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
     uint32_t cur[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) cur[i] = nxt[i];
-    if (t + 1 < 2 * ng) {
-      fetch(t + 1);
-#if OZ_CI_PF
-      prefetch_sub_ntt_tw<LOGR, true, LOGE>(tv, col, C, P.tw + (size_t)(((t + 1) & 1) * 2 + 1) * m);
-#endif
-    }
+    if (t + 1 < 2 * ng) fetch(t + 1);
     if (t > 0) __syncthreads();  // smem tile free
     const uint32_t p = q ? P.F.p1 : P.F.p0;
     const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
@@ -1774,6 +1740,7 @@ static void fill_crt_consts(const Plan& pl, FinishParams& FP) {
   FP.p1 = pl.p[1];
   FP.p0inv = pl.p0inv_mod_p1;
   FP.p0inv_sh = (uint32_t)(((uint64_t)pl.p0inv_mod_p1 << 32) / pl.p[1]);
+  FP.p1_barrett = (uint32_t)((1ull << 32) / pl.p[1]);
   FP.P = (unsigned long long)pl.p[0] * pl.p[1];
   FP.halfP = (FP.P - 1) / 2;
   for (int q = 0; q < 2; ++q) {  // f2: 2^-1 and (2 iota)^-1 = 2^-1 (-iota) (iota^-1 = -iota)
@@ -1900,7 +1867,7 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   const size_t C = 1ull << pl.logC;
   const int rle = row_loge(pl.logC, pl.logR > 0);
   const size_t padC = C + (C >> rle) + 1;
-  c.row_smem = ((size_t)pl.K * C + (OZ_ROW_DBUF ? 2 : 1) * padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
+  c.row_smem = ((size_t)pl.K * C + padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
   c.row_threads = pl.logC >= rle ? (1 << (pl.logC - rle)) : 1;  // exactly Tv: every thread active
   return c;
 }
