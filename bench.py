@@ -410,7 +410,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "peak_kind": "derived: 16 Shoup butterflies/clk/SM (64-lane ALU + 64-lane FMA "
                              "pipes, 8 lane-slots per butterfly) x 148 SMs x sm_max clock; "
                              "in-register radix-16 measured 13.1/clk/SM (tools/microbench_bfly.cu)",
-                "kernel": dom, "hbm_GB_s": d["GB_s"], "hbm_frac": d["frac_hbm"]}
+                "kernel": dom, "hbm_GB_s": d["GB_s"], "hbm_frac": d["frac_hbm"],
+                "hbm_frac_of_8TBs_spec": d["GB_s"] / 8000.0}
     else:
         roof = {"bound": "hbm", "achieved": d["GB_s"], "peak": hbm, "unit": "GB/s",
                 "frac": d["frac_hbm"], "traffic": traffic, "peak_kind": hbm_kind + " (MEASURED_PEAKS.json)",
