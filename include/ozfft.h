@@ -179,7 +179,10 @@ ozfft_status ozfft_plan_bind(ozfft_plan* plan, void* persistent, size_t persiste
 /* y = DFT(x) (direction -1) or x = DFT^-1(y) (direction +1, P:158-160,
  * computed as conj(DFT(conj(y)))/n with RN division, ruling 16), for the plan's
  * batch.  `in` and `out` are device complex128 [batch][n]; in == out is allowed.
- * Asynchronous on `stream`.  Errors: NOT_BOUND, INVALID_ARGUMENT, MISALIGNED, CUDA. */
+ * Asynchronous on `stream`.  Small plans (batch * m <= 2^22, env OZFFT_GRAPH_MAX_WORK)
+ * capture the launch sequence once per (in, out, direction) as a CUDA graph and replay
+ * it (up to 8 cached per plan); not while the stage profiler is on.
+ * Errors: NOT_BOUND, INVALID_ARGUMENT, MISALIGNED, CUDA. */
 ozfft_status ozfft_execute(const ozfft_plan* plan, const void* in, void* out, int direction,
                            void* stream);
 

@@ -59,6 +59,7 @@ static int compute_alpha(int64_t n, int64_t L, uint32_t p0, uint32_t p1) {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+uint64_t launches_so_far() { return g_launches.load(std::memory_order_relaxed); }
 
 void prof_mark(const Plan& pl, int stage, bool begin, void* stream) {
   Prof* pr = pl.prof;
@@ -117,6 +118,10 @@ static void layout(Plan& pl) {
                                 2 * align256((uint64_t)4 * K * m * 4);
   pl.workspace_bytes = std::max<uint64_t>(o, bind_scratch);
 }
+
+#ifndef OZFFT_GRAPH_MAX_WORK_DEFAULT
+#define OZFFT_GRAPH_MAX_WORK_DEFAULT (1ll << 22)  // batch * m up to which execute is a graph
+#endif
 
 static ozfft_status check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) return fail(OZFFT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -317,11 +322,74 @@ static ozfft_status check_exec(const ozfft_plan* pl, const void* in, const void*
   return OZFFT_OK;
 }
 
+// Replay (or capture, then replay) the whole execute as one CUDA graph on `stream`.
+static ozfft_status execute_graph(ozfft_plan* pl, const void* in, void* out, int direction,
+                                  cudaStream_t st) {
+  if (!pl->graphs) pl->graphs = new GraphCache();
+  GraphCache& gc = *pl->graphs;
+  for (const GraphCache::Entry& e : gc.entries)
+    if (e.in == in && e.out == out && e.direction == direction) {
+      count_launches(e.launches);
+      return check_cuda(cudaGraphLaunch((cudaGraphExec_t)e.exec, st), "graph launch");
+    }
+  if (!gc.capture) {
+    cudaStream_t cs;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+      return check_cuda(cudaGetLastError(), "capture stream create");
+    gc.capture = (void*)cs;
+  }
+  cudaStream_t cs = (cudaStream_t)gc.capture;
+  ozfft_status s = check_cuda(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+  if (s) return s;
+  const uint64_t l0 = launches_so_far();
+  ExecArgs a{};
+  a.nb = pl->batch;
+  a.in = reinterpret_cast<const double*>(in);
+  a.out = reinterpret_cast<double*>(out);
+  a.b0 = 0;
+  a.direction = direction;
+  a.unit_mask = 0xFF;
+  a.finish = true;
+  const ozfft_status ls = launch_execute(*pl, a, (void*)cs);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+  if (ls) {
+    if (g) cudaGraphDestroy(g);
+    return ls;
+  }
+  s = check_cuda(ce, "end capture");
+  if (s) return s;
+  cudaGraphExec_t ge = nullptr;
+  s = check_cuda(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+  cudaGraphDestroy(g);
+  if (s) return s;
+  GraphCache::Entry e{in, out, direction, (void*)ge, (int)(launches_so_far() - l0)};
+  if (gc.entries.size() < GraphCache::kMax) {
+    gc.entries.push_back(e);
+  } else {  // replace the oldest
+    cudaGraphExecDestroy((cudaGraphExec_t)gc.entries[gc.next].exec);
+    gc.entries[gc.next] = e;
+    gc.next = (gc.next + 1) % GraphCache::kMax;
+  }
+  return check_cuda(cudaGraphLaunch(ge, st), "graph launch");  // (captured launches counted)
+}
+
 ozfft_status ozfft_execute(const ozfft_plan* pl, const void* in, void* out, int direction,
                            void* stream) {
   ozfft_status s = check_exec(pl, in, out, direction);
   if (s) return s;
   const int64_t n = pl->n;
+  // small plans: one CUDA graph per (in, out, direction) instead of ~8 launches
+  static const int64_t graph_max_work = [] {
+    const char* t = std::getenv("OZFFT_GRAPH_MAX_WORK");  // batch * m; 0 disables
+    return t ? std::atoll(t) : (int64_t)OZFFT_GRAPH_MAX_WORK_DEFAULT;
+  }();
+  if (pl->chunk == pl->batch && pl->batch * pl->m <= graph_max_work && !(pl->prof && pl->prof->on)) {
+    s = execute_graph(const_cast<ozfft_plan*>(pl), in, out, direction, (cudaStream_t)stream);
+    if (s) return s;
+    const_cast<ozfft_plan*>(pl)->last_batch = pl->batch;
+    return OZFFT_OK;
+  }
   for (int64_t b0 = 0; b0 < pl->batch; b0 += pl->chunk) {
     ExecArgs a{};
     a.nb = std::min<int64_t>(pl->chunk, pl->batch - b0);
@@ -593,6 +661,11 @@ ozfft_status ozfft_plan_destroy(ozfft_plan* pl) {
     for (void* cs : pl->pipe->cs)
       if (cs) cudaStreamDestroy((cudaStream_t)cs);
     delete pl->pipe;
+  }
+  if (pl && pl->graphs) {
+    for (const GraphCache::Entry& e : pl->graphs->entries) cudaGraphExecDestroy((cudaGraphExec_t)e.exec);
+    if (pl->graphs->capture) cudaStreamDestroy((cudaStream_t)pl->graphs->capture);
+    delete pl->graphs;
   }
   if (pl && pl->prof) {
     for (void* e : pl->prof->pool) cudaEventDestroy((cudaEvent_t)e);

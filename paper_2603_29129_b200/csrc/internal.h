@@ -61,6 +61,23 @@ struct Plan {
   int64_t last_batch = 0;  // transforms covered by the per-batch stats arrays
   struct Prof* prof = nullptr;  // profiling state (mutable through the pointer)
   struct HostPipe* pipe = nullptr;  // copy streams/events of ozfft_execute_host (lazy)
+  struct GraphCache* graphs = nullptr;  // captured executes (ozfft_execute, small plans)
+};
+
+// CUDA graphs of ozfft_execute keyed by (in, out, direction): the launch sequence of a
+// small plan is latency-bound, so it is captured once and replayed (small-n).
+struct GraphCache {
+  struct Entry {
+    const void* in;
+    void* out;
+    int direction;
+    void* exec;       // cudaGraphExec_t
+    int launches;     // kernels in the graph (added to the launch counter per replay)
+  };
+  std::vector<Entry> entries;  // at most kMax, oldest replaced first
+  size_t next = 0;
+  void* capture = nullptr;     // cudaStream_t used for capture
+  static constexpr size_t kMax = 8;
 };
 
 // Copy/compute pipelining of ozfft_execute_host: H2D and D2H run on their own streams,
@@ -84,6 +101,7 @@ void prof_mark(const Plan& pl, int stage, bool begin, void* stream);
 // two-pass decompositions (log2 R, log2 C) instantiated in kernels.cu
 bool decomposition_supported(int logR, int logC);
 void count_launches(int n);
+uint64_t launches_so_far();
 
 // Schedule row length per (transform, conv): ngroups + K*K groups of (cexp, npairs, L pairs)
 OZ_HD inline int sched_stride(int K, int L) { return 1 + K * K * (2 + 2 * L); }
