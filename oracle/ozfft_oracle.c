@@ -34,6 +34,15 @@
  *   final fp64 bits    the DD op sequence is this build's contract; the
  *                      paper fixes only the [1e-16,1e-15] error band ->
  *                      "parity unpinned" at the bit level, pinned in error band.
+ *   cyclic plans (f1)  pinned: brute-force integer cyclic convolution of length n, and
+ *                      bitwise equality with the padded plans
+ *   orc_split_shared,  pinned: brute-force complex integer convolution, the iota ring
+ *   orc_execute_image  homomorphism, the alpha bound, counts 12+20, float128 (f2)
+ *   orc_ts_*           pinned: exact rationals -- conversions exact, TSAdd/TSMul relative
+ *                      error <= 2^-62 (f4; the algorithms are this build's reading,
+ *                      DESIGN ruling 24, so their exact bits are unpinned by the paper)
+ *   orc_split_ts       pinned: |D| <= 2^alpha, reconstruction within the last unit
+ *   orc_execute (TS)   pinned: float128 error band, 64 NTTs at phi = 0
  */
 #include <stdint.h>
 #include <stdlib.h>
