@@ -98,6 +98,7 @@ static void layout(Plan& pl) {
                        (uint64_t)32 * G * n + (uint64_t)32 * n + (two ? (uint64_t)64 * n : 0);
   int64_t chunk = (int64_t)std::max<uint64_t>(1, pl.max_ws / std::max<uint64_t>(per, 1));
   chunk = std::min<int64_t>(chunk, pl.batch);
+  chunk = std::min<int64_t>(chunk, 65535);  // per-transform kernels index transforms by gridDim.y
   pl.chunk = chunk;
   o = 0;
   pl.woff.stats = o;  o = align256(o + (uint64_t)pl.batch * stats_stride(K) * 4);

@@ -241,3 +241,15 @@ def test_modes_other_K_L(oz, mode, K, L):
         assert np.array_equal(gt["crt"][b].cpu().numpy(), ot["crt"])
         assert np.array_equal(gt["sched"][b].cpu().numpy(), ot["sched"])
         assert np.array_equal(y[b].cpu().numpy(), yo)
+
+
+def test_huge_batch_tiny_n(oz):
+    """batch > 65535 (the gridDim.y limit of the per-transform kernels) runs in chunks."""
+    n, B = 5, 70000
+    x = workloads.draw("uniform", 5, B, n)
+    plan = oz.Plan(n, B)
+    assert plan.chunk <= 65535
+    y = plan.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    op = O.Plan(n)
+    for b in (0, 1, 65534, 65535, 65536, B - 1):
+        assert np.array_equal(y[b], op.execute(x[b])), b
