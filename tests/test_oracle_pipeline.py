@@ -174,3 +174,45 @@ def test_batch_matches_single():
     assert used >= 1
     for b in range(6):
         assert np.array_equal(yb[b], pl.execute(x[b]))
+
+
+@pytest.mark.parametrize("n,signs", [(4, "plus"), (64, "plus"), (64, "random"), (1000, "plus"),
+                                     (1000, "random")])
+def test_integer_core_adversarial_bound(n, signs):
+    """digits all at +-2^alpha and groups of L = 3 pairs -- the largest sums the
+    alpha condition allows (L n 4^alpha < P/2) -- are still recovered exactly by
+    the oracle's NTT-domain accumulation, inverse NTT and Garner."""
+    L = 3
+    a = O.alpha(n, L)
+    m = 1
+    while m < 2 * n - 1:
+        m <<= 1
+    rng = np.random.default_rng(n)
+    big = 2 ** a
+
+    def vec(length):
+        v = np.full(length, big, dtype=np.int64)
+        if signs == "random":
+            v *= rng.choice([-1, 1], length)
+        return v
+
+    xs = [np.concatenate([vec(n), np.zeros(m - n, np.int64)]) for _ in range(L)]
+    ws = [vec(m) for _ in range(L)]
+    for w in ws:
+        w[n:m - n + 1] = 0  # omega~* support: j < n and j > m - n (ZeroPad_pm, P:196-214)
+    exact = np.zeros(n, dtype=object)
+    for x, w in zip(xs, ws):
+        xo, wo = x.astype(object), w.astype(object)
+        for j in range(n):
+            exact[j] += sum(xo[i] * wo[(j - i) % m] for i in range(n))
+    assert max(abs(int(v)) for v in exact) <= L * n * big * big < O.P0 * O.P1 // 2
+    res = []
+    for p in (O.P0, O.P1):
+        acc = np.zeros(m, dtype=np.uint64)
+        for x, w in zip(xs, ws):
+            X = O.ntt(np.mod(x, p).astype(np.uint32), p).astype(np.uint64)
+            W = O.ntt(np.mod(w, p).astype(np.uint32), p).astype(np.uint64)
+            acc = (acc + X * W % p) % p
+        res.append(O.ntt(acc.astype(np.uint32), p, inverse=True))
+    got = [O.garner2(int(res[0][j]), int(res[1][j]))[0] for j in range(n)]
+    assert got == [int(v) for v in exact]
