@@ -253,3 +253,21 @@ def test_huge_batch_tiny_n(oz):
     op = O.Plan(n)
     for b in (0, 1, 65534, 65535, 65536, B - 1):
         assert np.array_equal(y[b], op.execute(x[b])), b
+
+
+@pytest.mark.parametrize("n", [1000, 4096, 1 << 13])
+def test_max_digit_input(oz, n):
+    """x(j) = conj(omega(j)) makes x' = x (.) omega = |omega|^2 ~ 1 everywhere, so the level-0
+    digits of Re x' all sit at the top of the digit range and the group sums approach the
+    CRT range bound: bit-exact against the oracle."""
+    j = np.arange(n, dtype=np.float64)
+    x = np.exp(1j * np.pi * (j * j % (2 * n)) / n)[None, :].astype(np.complex128)
+    plan = oz.Plan(n, 1)
+    y, gt = plan.execute_taps(torch.from_numpy(x).cuda())
+    yo, ot = O.Plan(n).execute(x[0], taps=True)
+    d = gt["digits"][0].cpu().numpy()
+    # |x'| = 1 up to rounding: mu is 1 or just above, so the level-0 digits are all 2^alpha
+    # or all 2^(alpha - 1) (E = 0 or 1)
+    assert np.min(np.abs(d[0, 0])) >= 2 ** (plan.alpha - 1) - 1
+    check_taps(gt, ot, n, 3, 0)
+    assert np.array_equal(y[0].cpu().numpy(), yo)
