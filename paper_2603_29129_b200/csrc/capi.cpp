@@ -235,6 +235,8 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     if (logm > 12 && decomposition_supported(logm - v, v)) pl->logC = v;
   }
   pl->logR = logm - pl->logC;
+  if (const char* t = std::getenv("OZFFT_SPLIT_CLUSTER_MAXLEN"))  // knob (tests/tools): 0 = off
+    pl->split_cluster_max = std::atoll(t);
   // image mode: a real output sums L n complex products (|Re| <= 2 4^alpha each)
   pl->alpha = compute_alpha(pl->image ? 2 * desc.n : desc.n, desc.L, p0, p1);
   if (pl->alpha < 1) {

@@ -31,6 +31,7 @@ struct Plan {
   int K = 3, L = 3, alpha = 0, rho = 0;
   uint32_t p[2] = {0, 0};
   int logm = 0, logC = 0, logR = 0;  // m = R * C
+  int64_t split_cluster_max = -1;     // longest vector for the one-launch split (-1: build default)
   int conv_mode = 0;                 // OZFFT_CONV_PADDED (m >= 2n-1) or OZFFT_CONV_CYCLIC (m = n)
   int image = 0;                     // OZFFT_ACCUM_IMAGE: complex-image accumulation (f2)
   int ts = 0;                        // OZFFT_PREC_TS: triple-single a1 / a2 / a7 (f4)

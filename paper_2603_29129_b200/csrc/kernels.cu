@@ -5,6 +5,8 @@
 //                                 of the Ozaki split (Alg.6 l.778/786), one launch per level
 //   k_split_digits<TS>    a2     int32 digits D = fl(fl(hi+sigma)-sigma) 2^(alpha-E)
 //                                 (Alg.6 l.781-785) + the Alg.8 flush schedules
+//   k_split_cluster<TS>   a1+a2  n <= 2^15: both of the above in one launch, one thread-block
+//                                 cluster per transform (x' in shared memory, DSMEM max)
 //   k_col_fwd<R,C,IMG>    a3     residue lift (or digit images, f2) + the first log2 R DIF
 //                                 stages of the length-m forward NTT on column tiles
 //   k_row_fused<C,2PASS>  a3-a5  last log2 C DIF stages of the slices of one row, pointwise
@@ -24,6 +26,7 @@
 // bit-reversed to natural order, so the pointwise stage needs no permutation.
 // m^{-1} of eq:intt is folded into the cached W spectra.  Compile-time tuning knobs
 // (OZ_*) default to the measured best (DESIGN.md section 6 lists the rejected ones).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -32,6 +35,7 @@
 #include "internal.h"
 
 namespace ozfft {
+namespace cg = cooperative_groups;
 
 // ============================================================== modular arithmetic
 __device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) {
@@ -169,11 +173,24 @@ __device__ __forceinline__ TSv ts_ldexp(TSv a, int e) {
 }
 // TS split step (ruling 25): x = fl32(fl32(r0 + sigma) - sigma), digit x 2^(alpha-E),
 // (r0, t) = FastTwoSum(fl32(r0 - x), r1), (r1, r2) = FastTwoSum(t, r2).
-__device__ __forceinline__ int32_t split_step_ts(TSv& r, int E, int alpha, int rho) {
-  const float sigma = ldexpf(1.0f, E + rho);
+// The level constants sigma = 2^(E + rho) and 2^(alpha - E) depend on (part, level) only:
+// SplitC holds them, computed once per CTA (or level), not per element.
+template <bool TS>
+struct SplitC {
+  std::conditional_t<TS, float, double> sigma, scale;
+};
+template <bool TS>
+__device__ __forceinline__ SplitC<TS> split_c(int E, int alpha, int rho) {
+  if constexpr (TS)
+    return SplitC<TS>{ldexpf(1.0f, E + rho), ldexpf(1.0f, alpha - E)};
+  else
+    return SplitC<TS>{scalbn(1.0, E + rho), scalbn(1.0, alpha - E)};
+}
+__device__ __forceinline__ int32_t split_step_ts(TSv& r, SplitC<true> c) {
+  const float sigma = c.sigma;
   const float t = __fadd_rn(r.x0, sigma);
   const float x = __fsub_rn(t, sigma);
-  const int32_t D = __float2int_rz(__fmul_rn(x, ldexpf(1.0f, alpha - E)));
+  const int32_t D = __float2int_rz(__fmul_rn(x, c.scale));
   const float d = __fsub_rn(r.x0, x);
   float a, b;
   fast_two_sum_f(d, r.x1, a, b);
@@ -199,6 +216,18 @@ __device__ __forceinline__ int ceil_log2_bits(unsigned long long u) {
 constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
 
 // ============================================================== split kernels
+#ifndef OZ_SPLIT_EPT
+#define OZ_SPLIT_EPT 8  // elements per thread of k_split_max / k_split_digits
+#endif
+#ifndef OZ_SPLIT_CL_EPT
+#define OZ_SPLIT_CL_EPT 1  // elements per thread per iteration of k_split_cluster
+#endif
+#ifndef OZ_SPLIT_CL_MAXLEN
+#define OZ_SPLIT_CL_MAXLEN (1 << 15)  // longest vector split by k_split_cluster
+#endif
+#ifndef OZ_SPLIT_CL_CHUNK
+#define OZ_SPLIT_CL_CHUNK 256  // target elements per CTA of k_split_cluster
+#endif
 struct SplitParams {
   const double2* x;       // mode 0: input complex [nb][len]; mode 1: raw DD hi values [len]
   const double2* chirp;   // [len] (C, S)
@@ -218,8 +247,8 @@ struct SplitParams {
 __device__ __forceinline__ void load_xprime(const SplitParams& P, int64_t b, int64_t j, double& hr,
                                             double& lr, double& hi, double& li) {
   if (P.mode == 0) {
-    const double2 xv = P.x[b * P.len + j];
-    const double2 w = P.chirp[j];
+    const double2 xv = __ldg(&P.x[b * P.len + j]);
+    const double2 w = __ldg(&P.chirp[j]);
     const double xr = xv.x, xi = P.conj ? -xv.y : xv.y;
     double p1, e1, p2, e2;
     two_prod(xr, w.x, p1, e1);
@@ -229,7 +258,7 @@ __device__ __forceinline__ void load_xprime(const SplitParams& P, int64_t b, int
     two_prod(xi, w.x, p2, e2);
     dd_add(p1, e1, p2, e2, hi, li);
   } else {
-    const double2 wv = P.x[j];
+    const double2 wv = __ldg(&P.x[j]);
     hr = wv.x;
     hi = wv.y;
     lr = 0.0;
@@ -241,25 +270,25 @@ __device__ __forceinline__ void load_xprime(const SplitParams& P, int64_t b, int
 __device__ __forceinline__ void load_xprime_ts(const SplitParams& P, int64_t b, int64_t j, TSv& re,
                                                TSv& im) {
   if (P.mode == 0) {
-    const double2 xv = P.x[b * P.len + j];
-    const double2 w = P.chirp[j];
+    const double2 xv = __ldg(&P.x[b * P.len + j]);
+    const double2 w = __ldg(&P.chirp[j]);
     const TSv xr = ts_from_double(xv.x), xi = ts_from_double(P.conj ? -xv.y : xv.y);
     const TSv c = ts_from_double(w.x), sn = ts_from_double(w.y);
     re = ts_add(ts_mul(xr, c), ts_neg(ts_mul(xi, sn)));
     im = ts_add(ts_mul(xr, sn), ts_mul(xi, c));
   } else {
-    const double2 wv = P.x[j];
+    const double2 wv = __ldg(&P.x[j]);
     re = ts_from_double(wv.x);
     im = ts_from_double(wv.y);
   }
 }
 
 // One Ozaki extraction step on (h, l) with level exponent E (Alg.6 l.781-783).
-__device__ __forceinline__ int32_t split_step(double& h, double& l, int E, int alpha, int rho) {
-  const double sigma = scalbn(1.0, E + rho);
+__device__ __forceinline__ int32_t split_step(double& h, double& l, SplitC<false> c) {
+  const double sigma = c.sigma;
   const double t = __dadd_rn(h, sigma);
   const double d = __dsub_rn(t, sigma);
-  const int32_t D = __double2int_rz(__dmul_rn(d, scalbn(1.0, alpha - E)));
+  const int32_t D = __double2int_rz(__dmul_rn(d, c.scale));
   const double r = __dsub_rn(h, d);
   fast_two_sum(r, l, h, l);
   return D;
@@ -290,6 +319,12 @@ __global__ void __launch_bounds__(256) k_split_max(SplitParams P, int level) {
       E[v][k] = (u == 0 || u >= kInfBits) ? 0 : ceil_log2_bits(u);
     }
   if (bad) return;  // non-finite transform: nothing more to compute
+  __shared__ SplitC<TS> s_c[2][kMaxK];
+  if (threadIdx.x < 2 * kMaxK) {
+    const int v = threadIdx.x / kMaxK, k = threadIdx.x % kMaxK;
+    s_c[v][k] = split_c<TS>(k < lv[v] ? E[v][k] : 0, P.alpha, P.rho);
+  }
+  __syncthreads();
   unsigned long long m0 = 0, m1 = 0;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P.len;
        j += (int64_t)gridDim.x * blockDim.x) {
@@ -299,7 +334,7 @@ __global__ void __launch_bounds__(256) k_split_max(SplitParams P, int level) {
       load_xprime_ts(P, b, j, r[0], r[1]);
 #pragma unroll
       for (int v = 0; v < 2; ++v)
-        for (int k = 0; k < lv[v]; ++k) (void)split_step_ts(r[v], E[v][k], P.alpha, P.rho);
+        for (int k = 0; k < lv[v]; ++k) (void)split_step_ts(r[v], s_c[v][k]);
       a0 = ts_key(r[0]);
       a1 = ts_key(r[1]);
     } else {
@@ -307,7 +342,7 @@ __global__ void __launch_bounds__(256) k_split_max(SplitParams P, int level) {
       load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
 #pragma unroll
       for (int v = 0; v < 2; ++v)  // a level with mu == 0 ended this part's split (Alg.6 l.780)
-        for (int k = 0; k < lv[v]; ++k) (void)split_step(h[v], l[v], E[v][k], P.alpha, P.rho);
+        for (int k = 0; k < lv[v]; ++k) (void)split_step(h[v], l[v], s_c[v][k]);
       a0 = (unsigned long long)__double_as_longlong(fabs(h[0]));
       a1 = (unsigned long long)__double_as_longlong(fabs(h[1]));
     }
@@ -368,13 +403,12 @@ __device__ void alg8_schedule(int kx, const int* sx, int ky, const int* sy, int 
   row[0] = ng + 1;
 }
 
-// Digits for every level, per-transform stats and (block 0) the schedules.
-template <bool TS>
-__global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
-  const int64_t b = blockIdx.y;
-  const unsigned long long* mub = P.mu + b * 2 * P.K;
-  int E[2][kMaxK];
-  int kv[2];
+// Level exponents E, slice counts kv and the non-finite flag of one transform from its
+// per-level maxima mu (Alg.6 l.778-780; ruling 8); `lead` threads (thread 0 / threads < 4)
+// write the stats row and the four Alg.8 schedules.
+__device__ __forceinline__ bool split_exponents(const SplitParams& P, int64_t b,
+                                                const unsigned long long* mub, int (&E)[2][kMaxK],
+                                                int (&kv)[2], bool lead) {
   bool bad = false;
   for (int v = 0; v < 2; ++v) {
     kv[v] = P.K;
@@ -389,7 +423,7 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
   for (int v = 0; v < 2; ++v)
     for (int k = kv[v]; k < P.K; ++k) E[v][k] = 0;
   if (bad) { kv[0] = 0; kv[1] = 0; }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (lead && threadIdx.x == 0) {
     int32_t* st = P.stats + b * stats_stride(P.K);
     st[0] = kv[0];
     st[1] = kv[1];
@@ -397,7 +431,7 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
       for (int k = 0; k < P.K; ++k) st[2 + v * P.K + k] = E[v][k];
     st[2 + 2 * P.K] = bad ? 1 : 0;
   }
-  if (P.sched && blockIdx.x == 0 && threadIdx.x < 4) {
+  if (P.sched && lead && threadIdx.x < 4) {
     const int cv = threadIdx.x;
     const int a = conv_a(cv), bw = conv_b(cv);
     int sx[kMaxK], sy[kMaxK];
@@ -410,7 +444,23 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
     alg8_schedule(bad || (P.shared && cv > 0) ? 0 : kv[a], sx, kw, sy, P.K, P.L,
                   P.sched + (b * 4 + cv) * sched_stride(P.K, P.L));
   }
+  return bad;
+}
+
+// Digits for every level, per-transform stats and (block 0) the schedules.
+template <bool TS>
+__global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
+  const int64_t b = blockIdx.y;
+  int E[2][kMaxK];
+  int kv[2];
+  const bool bad = split_exponents(P, b, P.mu + b * 2 * P.K, E, kv, blockIdx.x == 0);
   if (bad) return;
+  __shared__ SplitC<TS> s_c[2][kMaxK];
+  if (threadIdx.x < 2 * kMaxK) {
+    const int v = threadIdx.x / kMaxK, k = threadIdx.x % kMaxK;
+    s_c[v][k] = split_c<TS>(k < P.K ? E[v][k] : 0, P.alpha, P.rho);
+  }
+  __syncthreads();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P.len;
        j += (int64_t)gridDim.x * blockDim.x) {
     if constexpr (TS) {
@@ -421,7 +471,7 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
         int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j;
         for (int k = 0; k < P.K; ++k) {
           int32_t D = 0;
-          if (k < kv[v]) D = split_step_ts(r[v], E[v][k], P.alpha, P.rho);
+          if (k < kv[v]) D = split_step_ts(r[v], s_c[v][k]);
           dv[k * P.len] = D;
         }
       }
@@ -433,12 +483,156 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
         int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j;
         for (int k = 0; k < P.K; ++k) {
           int32_t D = 0;
-          if (k < kv[v]) D = split_step(h[v], l[v], E[v][k], P.alpha, P.rho);
+          if (k < kv[v]) D = split_step(h[v], l[v], s_c[v][k]);
           dv[k * P.len] = D;
         }
       }
     }
   }
+}
+
+// ============================================================== fused small-n split
+// n <= kSplitClusterMaxLen: a1 + a2 of one transform in ONE launch.  One thread-block
+// cluster of CS <= 8 CTAs per transform; each CTA keeps its chunk of x' (DD: hi, lo of both
+// parts; TS: the three words of both parts) in shared memory across the K levels, and the
+// per-level max |hi| (Alg.6 l.778/786) is a block reduction plus a DSMEM exchange of the
+// CS partial maxima (one cluster barrier per level).  Level k's digits are written in the
+// pass that computes level k+1's max.  Every element goes through the same operation
+// sequence as in k_split_max + k_split_digits and max is exact, so the digits, stats and
+// schedules are bitwise those of the multi-launch path (which stays for larger n).
+// (For a non-finite transform both leave the digits unused: stats say kv = 0.)
+constexpr int kSplitClusterMaxLen = OZ_SPLIT_CL_MAXLEN;
+constexpr int kSplitClusterThreads = 512;
+
+template <bool TS>
+__global__ void __launch_bounds__(kSplitClusterThreads) k_split_cluster(SplitParams P, int chunk) {
+  extern __shared__ __align__(16) unsigned char split_sm[];
+  __shared__ unsigned long long s_part[kMaxK][2];           // this CTA's max per level / part
+  __shared__ unsigned long long s_red[2][kSplitClusterThreads / 32];
+  __shared__ unsigned long long s_mu[2 * kMaxK];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int cs = (int)cl.num_blocks();
+  const int64_t b = blockIdx.y;
+  const int K = P.K;
+  const int64_t j0 = (int64_t)rank * chunk;
+  const int cnt = (int)(P.len - j0 < chunk ? (P.len - j0 > 0 ? P.len - j0 : 0) : chunk);
+  double* sh = reinterpret_cast<double*>(split_sm);  // DD: h[2][chunk], l[2][chunk]
+  float* sr = reinterpret_cast<float*>(split_sm);    // TS: r[2][3][chunk]
+  unsigned long long mu[2][kMaxK];
+  int E[2][kMaxK], kv[2] = {K, K};
+  for (int v = 0; v < 2; ++v)
+    for (int k = 0; k < kMaxK; ++k) { mu[v][k] = 0; E[v][k] = 0; }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int level = 0; level <= K; ++level) {
+    SplitC<TS> lc[2];  // level - 1's constants
+#pragma unroll
+    for (int v = 0; v < 2; ++v) lc[v] = split_c<TS>(level > 0 ? E[v][level - 1] : 0, P.alpha, P.rho);
+    unsigned long long m0 = 0, m1 = 0;
+    for (int i0 = threadIdx.x; i0 < cnt; i0 += OZ_SPLIT_CL_EPT * blockDim.x)
+#pragma unroll
+    for (int u = 0; u < OZ_SPLIT_CL_EPT; ++u) {
+      // out-of-range slots recompute element cnt - 1 and store nothing (as in k_split_max)
+      const bool ok = i0 + u * (int)blockDim.x < cnt;
+      const int i = ok ? i0 + u * (int)blockDim.x : cnt - 1;
+      const int64_t j = j0 + i;
+      unsigned long long a0, a1;
+      if constexpr (TS) {
+        TSv r[2];
+        if (level == 0) {
+          load_xprime_ts(P, b, j, r[0], r[1]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            r[v] = TSv{sr[(v * 3 + 0) * chunk + i], sr[(v * 3 + 1) * chunk + i], sr[(v * 3 + 2) * chunk + i]};
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {  // level - 1's digits (Alg.6 l.781-785)
+            int32_t D = 0;
+            if (level - 1 < kv[v]) D = split_step_ts(r[v], lc[v]);
+            if (ok) P.digits[((b * 2 + v) * K + level - 1) * P.len + j] = D;
+          }
+        }
+        if (level == K) continue;
+#pragma unroll
+        for (int v = 0; v < 2 && ok; ++v) {
+          sr[(v * 3 + 0) * chunk + i] = r[v].x0;
+          sr[(v * 3 + 1) * chunk + i] = r[v].x1;
+          sr[(v * 3 + 2) * chunk + i] = r[v].x2;
+        }
+        a0 = ts_key(r[0]);
+        a1 = ts_key(r[1]);
+      } else {
+        double h[2], l[2];
+        if (level == 0) {
+          load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            h[v] = sh[v * chunk + i];
+            l[v] = sh[(2 + v) * chunk + i];
+          }
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            int32_t D = 0;
+            if (level - 1 < kv[v]) D = split_step(h[v], l[v], lc[v]);
+            if (ok) P.digits[((b * 2 + v) * K + level - 1) * P.len + j] = D;
+          }
+        }
+        if (level == K) continue;
+#pragma unroll
+        for (int v = 0; v < 2 && ok; ++v) {
+          sh[v * chunk + i] = h[v];
+          sh[(2 + v) * chunk + i] = l[v];
+        }
+        a0 = (unsigned long long)__double_as_longlong(fabs(h[0]));
+        a1 = (unsigned long long)__double_as_longlong(fabs(h[1]));
+      }
+      if (!ok) a0 = a1 = 0;
+      m0 = a0 > m0 ? a0 : m0;  // NaN bits exceed +Inf bits: a NaN sticks
+      m1 = a1 > m1 ? a1 : m1;
+    }
+    if (level == K) break;
+    m0 = warp_max_u64(m0);
+    m1 = warp_max_u64(m1);
+    if (lane == 0) { s_red[0][warp] = m0; s_red[1][warp] = m1; }
+    __syncthreads();
+    if (warp == 0) {
+      const int nw = blockDim.x >> 5;
+      m0 = lane < nw ? s_red[0][lane] : 0;
+      m1 = lane < nw ? s_red[1][lane] : 0;
+      m0 = warp_max_u64(m0);
+      m1 = warp_max_u64(m1);
+      if (lane == 0) { s_part[level][0] = m0; s_part[level][1] = m1; }
+    }
+    cl.sync();  // every CTA's partial max of this level is visible cluster-wide
+    m0 = m1 = 0;
+    for (int r = 0; r < cs; ++r) {
+      const unsigned long long* rp = cl.map_shared_rank(&s_part[level][0], r);
+      m0 = rp[0] > m0 ? rp[0] : m0;
+      m1 = rp[1] > m1 ? rp[1] : m1;
+    }
+    if (P.shared) m0 = m1 = m0 > m1 ? m0 : m1;  // mu = max over both parts (f2)
+    mu[0][level] = m0;
+    mu[1][level] = m1;
+    // the exponents and slice counts as k_split_max / k_split_digits derive them
+    bool bad = false;
+    for (int v = 0; v < 2; ++v) {
+      const unsigned long long u = mu[v][level];
+      if (u >= kInfBits) bad = true;
+      E[v][level] = (u == 0 || u >= kInfBits) ? 0 : ceil_log2_bits(u);
+      if (u == 0 && kv[v] == K) kv[v] = level;
+    }
+    if (bad) break;  // k_split_max stops here too: later levels keep mu = 0
+  }
+  // mu (as the multi-launch path leaves it), stats and schedules: rank 0
+  if (rank == 0) {
+    if (threadIdx.x < 2 * K) s_mu[threadIdx.x] = mu[threadIdx.x / K][threadIdx.x % K];
+    __syncthreads();
+    if (threadIdx.x < 2 * K) P.mu[b * 2 * K + threadIdx.x] = s_mu[threadIdx.x];
+    int Ef[2][kMaxK], kvf[2];
+    (void)split_exponents(P, b, s_mu, Ef, kvf, true);
+  }
+  cl.sync();  // no CTA leaves while another may still read its s_part
 }
 
 // ============================================================== NTT building blocks
@@ -1823,8 +2017,14 @@ static int col_threads(int logR, int logCb) {
   const int Tv = logR >= le ? (1 << (logR - le)) : 1;
   return Tv << logCb;
 }
-#ifndef OZ_SPLIT_EPT
-#define OZ_SPLIT_EPT 8  // elements per thread of the split kernels' grid-stride loops
+template <class K>
+static void set_smem(K kern, size_t bytes) {
+  if (bytes > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+#ifndef OZ_SPLIT_CLUSTER
+#define OZ_SPLIT_CLUSTER 1  // fused one-launch split for n <= kSplitClusterMaxLen
 #endif
 static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cudaStream_t st) {
   const int threads = 256;
@@ -1832,6 +2032,47 @@ static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cud
   if (blocks_per < 1) blocks_per = 1;
   if (blocks_per > 65535) blocks_per = 65535;
   dim3 grid((unsigned)blocks_per, (unsigned)nb);
+#if OZ_SPLIT_CLUSTER
+  const int64_t cl_max = pl.split_cluster_max >= 0 && pl.split_cluster_max < kSplitClusterMaxLen
+                            ? pl.split_cluster_max : kSplitClusterMaxLen;
+  if (SP.len <= cl_max) {  // one cluster per transform, one launch (a1 + a2)
+    int cs = 1;
+    while (cs < 8 && (int64_t)cs * OZ_SPLIT_CL_CHUNK < SP.len) cs *= 2;
+    const int chunk = (int)((SP.len + cs - 1) / cs);
+    int thr = (chunk + OZ_SPLIT_CL_EPT - 1) / OZ_SPLIT_CL_EPT;
+    thr = thr < 32 ? 32 : (thr > kSplitClusterThreads ? kSplitClusterThreads : (thr + 31) & ~31);
+    const size_t smem = (size_t)chunk * (pl.ts ? 6 * sizeof(float) : 4 * sizeof(double));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cs, (unsigned)nb);
+    cfg.blockDim = dim3((unsigned)thr);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // static + dynamic shared memory may pass 48 KB: opt in once to the largest chunk
+    static const bool smem_set = [] {
+      const int mx = 160 * 1024;
+      cudaFuncSetAttribute(k_split_cluster<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(k_split_cluster<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      return true;
+    }();
+    (void)smem_set;
+    prof_mark(pl, OZFFT_STAGE_SPLIT_MAX, true, st);
+    if (pl.ts)
+      cudaLaunchKernelEx(&cfg, k_split_cluster<true>, SP, chunk);
+    else
+      cudaLaunchKernelEx(&cfg, k_split_cluster<false>, SP, chunk);
+    prof_mark(pl, OZFFT_STAGE_SPLIT_MAX, false, st);
+    count_launches(1);
+    return cuda_check("k_split_cluster");
+  }
+#endif
+  cudaMemsetAsync(SP.mu, 0, sizeof(unsigned long long) * 2 * SP.K * nb, st);
   prof_mark(pl, OZFFT_STAGE_SPLIT_MAX, true, st);
   for (int level = 0; level < SP.K; ++level) {
     if (pl.ts)
@@ -1906,11 +2147,6 @@ bool decomposition_supported(int logR, int logC) {
   return (logC == 11 && logR >= 2 && logR <= 8) || (logC == 12 && logR >= 7 && logR <= 10);
 }
 
-template <class K>
-static void set_smem(K kern, size_t bytes) {
-  if (bytes > 48 * 1024)
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
 
 static void launch_col_fwd(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
                            const ColParams& CP) {
@@ -1996,7 +2232,6 @@ ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
   int32_t* stats = reinterpret_cast<int32_t*>(carve(sizeof(int32_t) * stats_stride(K)));
   uint32_t* Y = reinterpret_cast<uint32_t*>(carve(sizeof(uint32_t) * 4 * K * m));
   uint32_t* X = reinterpret_cast<uint32_t*>(carve(sizeof(uint32_t) * 4 * K * m));
-  cudaMemsetAsync(mu, 0, sizeof(unsigned long long) * 2 * K, st);
   cudaMemsetAsync(X, 0, sizeof(uint32_t) * 4 * K * m, st);
   SplitParams SP{};
   SP.x = reinterpret_cast<const double2*>(pl.pers + pl.poff.W);  // wstar staged in the W area
@@ -2069,7 +2304,6 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   const int32_t* wsplit = reinterpret_cast<const int32_t*>(pl.pers + pl.poff.wsplit);
   const ozfft_taps* taps = A.taps;
 
-  cudaMemsetAsync(mu, 0, sizeof(unsigned long long) * 2 * K * nb, st);
   SplitParams SP{};
   SP.x = reinterpret_cast<const double2*>(A.in);
   SP.chirp = chirp;
