@@ -1248,7 +1248,8 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   // ---- forward: last log2(C) DIF stages of each slice's NTT (Alg.6 l.787)
   for (int s = 0; s < ka; ++s) {
     uint32_t* xs = Xs + s * C;
-    uint32_t* outX = P.Xout ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff : nullptr;
+    uint32_t* outX = P.Xout && blockIdx.z == 0 ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff
+                                              : nullptr;
     uint32_t* wk = work;
     if (s > 0) __syncthreads();  // `work` free (previous last reads done)
     auto store_x = [&](int i, uint32_t e, uint32_t v) {
@@ -1334,9 +1335,11 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   const uint32_t nlim = TWO_PASS ? C : (uint32_t)P.n;
   // (processing two items at once with sub_ntt_multi<..., 2> shares twiddles and barriers
   // but measured slower on B200 -- fewer resident CTAs -- so items run one at a time)
-  for (int it = 0; it < nitems; ++it) {
+  // Small one-pass plans spread the items over gridDim.z CTAs (each recomputes the few
+  // forward spectra): latency, not throughput, bounds them.
+  for (int it = blockIdx.z; it < nitems; it += gridDim.z) {
     uint32_t* wk = work;
-    if (it > 0) __syncthreads();  // exchange buffer free
+    if (it >= (int)gridDim.z) __syncthreads();  // exchange buffer free
     int ci0, g0;
     item(it, ci0, g0);
     uint32_t z[E];
@@ -1417,12 +1420,18 @@ __device__ __forceinline__ long long garner2(uint32_t z0, uint32_t z1, const Fin
   return Zp > P.halfP ? (long long)(Zp - P.P) : (long long)Zp;
 }
 
+// CTA = 64 outputs x 4 real convolutions: thread (cv, jl) forms conv cv's DD sum of
+// output j (Garner + scaled sum in flush order), then the cv = 0 threads combine the four
+// sums and post-chirp.  (The four per-conv chains are independent: one thread per conv
+// quarters the dependent-latency chain of the small one-pass plans this kernel serves.)
+constexpr int kFinishCols = 64;
 __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
   const int64_t b = blockIdx.y;
   const int K = P.K, L = P.L, G = K * K;
   // per-transform schedule: group counts and exact scales 2^-cexp (l.975), in smem
   __shared__ int s_ng[4];
   __shared__ double s_sc[4][kMaxK * kMaxK];
+  __shared__ double2 s_S[4][kFinishCols];
   if (threadIdx.x < 4) {
     const int cv = threadIdx.x;
     const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(K, L);
@@ -1431,19 +1440,12 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
     for (int g = 0; g < ng; ++g) s_sc[cv][g] = scalbn(1.0, -srow[1 + g * (2 + 2 * L)]);
   }
   __syncthreads();
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= P.n) return;
+  const int cvt = threadIdx.x / kFinishCols, jl = threadIdx.x % kFinishCols;
+  const int64_t j = (int64_t)blockIdx.x * kFinishCols + jl;
   const int32_t* st = P.stats + b * stats_stride(K);
-  double2 o;
-  if (st[2 + 2 * K] & 1) {
-    o.x = __longlong_as_double(0x7FF8000000000000ll);
-    o.y = o.x;
-    P.out[b * P.n + j] = o;
-    return;
-  }
-  double Sh[4], Sl[4];
-#pragma unroll 1
-  for (int cv = 0; cv < 4; ++cv) {
+  const bool bad = st[2 + 2 * K] & 1;
+  if (j < P.n && !bad) {
+    const int cv = cvt;
     double sh = 0.0, sl = 0.0;
     const int ng = s_ng[cv];
     const uint32_t* r0 = P.res + (((b * 4 + cv) * 2 + 0) * G) * P.n + j;
@@ -1471,10 +1473,22 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
         }
       }
     }
-    if (cv == 0) { Sh[0] = sh; Sl[0] = sl; }
-    else if (cv == 1) { Sh[1] = sh; Sl[1] = sl; }
-    else if (cv == 2) { Sh[2] = sh; Sl[2] = sl; }
-    else { Sh[3] = sh; Sl[3] = sl; }
+    s_S[cv][jl] = make_double2(sh, sl);
+  }
+  __syncthreads();
+  if (cvt != 0 || j >= P.n) return;
+  double2 o;
+  if (bad) {
+    o.x = __longlong_as_double(0x7FF8000000000000ll);
+    o.y = o.x;
+    P.out[b * P.n + j] = o;
+    return;
+  }
+  double Sh[4], Sl[4];
+#pragma unroll
+  for (int cv = 0; cv < 4; ++cv) {
+    Sh[cv] = s_S[cv][jl].x;
+    Sl[cv] = s_S[cv][jl].y;
   }
   double yrh, yrl, yih, yil;
   dd_add(Sh[0], Sl[0], -Sh[1], -Sl[1], yrh, yrl);  // rr - ii
@@ -2026,6 +2040,18 @@ static void set_smem(K kern, size_t bytes) {
 #ifndef OZ_SPLIT_CLUSTER
 #define OZ_SPLIT_CLUSTER 1  // fused one-launch split for n <= kSplitClusterMaxLen
 #endif
+static int sm_count() {
+  static const int c = [] {
+    int d = 0, v = 148;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    return v;
+  }();
+  return c;
+}
+#ifndef OZ_ROW_ZMAX
+#define OZ_ROW_ZMAX 18  // most CTAs one (transform, part, prime) row of a one-pass plan uses
+#endif
 static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cudaStream_t st) {
   const int threads = 256;
   int64_t blocks_per = (SP.len + threads * OZ_SPLIT_EPT - 1) / (threads * OZ_SPLIT_EPT);
@@ -2356,6 +2382,12 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   fill_iota(pl, RP.io);
   {
     dim3 grid((unsigned)nb, (unsigned)(4u << pl.logR));
+    if (pl.logR == 0) {  // one-pass plan: split the (conv, group) items over gridDim.z
+      const int64_t ctas = nb * 4;
+      int64_t z = ctas < sm_count() ? sm_count() / ctas : 1;
+      z = z > 2 * K * K ? 2 * K * K : (z < 1 ? 1 : z);
+      grid.z = (unsigned)(z > OZ_ROW_ZMAX ? OZ_ROW_ZMAX : z);
+    }
     prof_mark(pl, OZFFT_STAGE_ROW_FUSED, true, st);
     launch_row(pl.logC, pl.logR, grid, c, st, RP);
     prof_mark(pl, OZFFT_STAGE_ROW_FUSED, false, st);
@@ -2438,13 +2470,14 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     FP.chirp = chirp; FP.out = reinterpret_cast<double2*>(A.out); FP.direction = A.direction;
     FP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)nb);
+    const dim3 grid4((unsigned)((n + kFinishCols - 1) / kFinishCols), (unsigned)nb);
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
     if (pl.image)
       k_crt_finish_img<<<grid, 256, 0, st>>>(FP);
     else if (pl.ts)
       k_crt_finish_ts<<<grid, 256, 0, st>>>(FP);
     else
-      k_crt_finish<<<grid, 256, 0, st>>>(FP);
+      k_crt_finish<<<grid4, 256, 0, st>>>(FP);
     prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
     count_launches(1);
     s = cuda_check("k_crt_finish");
@@ -2567,11 +2600,12 @@ ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, do
   FP.out = reinterpret_cast<double2*>(out);
   FP.direction = direction;
   dim3 grid((unsigned)((pl.n + 255) / 256), 1);
+  const dim3 grid4((unsigned)((pl.n + kFinishCols - 1) / kFinishCols), 1);
   prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
   if (pl.ts)
     k_crt_finish_ts<<<grid, 256, 0, st>>>(FP);
   else
-    k_crt_finish<<<grid, 256, 0, st>>>(FP);
+    k_crt_finish<<<grid4, 256, 0, st>>>(FP);
   prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
   count_launches(1);
   return cuda_check("k_crt_finish (shard)");
