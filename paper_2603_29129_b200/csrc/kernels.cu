@@ -502,7 +502,10 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
 // schedules are bitwise those of the multi-launch path (which stays for larger n).
 // (For a non-finite transform both leave the digits unused: stats say kv = 0.)
 constexpr int kSplitClusterMaxLen = OZ_SPLIT_CL_MAXLEN;
-constexpr int kSplitClusterThreads = 512;
+#ifndef OZ_SPLIT_CL_THREADS
+#define OZ_SPLIT_CL_THREADS 512
+#endif
+constexpr int kSplitClusterThreads = OZ_SPLIT_CL_THREADS;
 
 template <bool TS>
 __global__ void __launch_bounds__(kSplitClusterThreads) k_split_cluster(SplitParams P, int chunk) {
@@ -604,7 +607,10 @@ __global__ void __launch_bounds__(kSplitClusterThreads) k_split_cluster(SplitPar
       m1 = warp_max_u64(m1);
       if (lane == 0) { s_part[level][0] = m0; s_part[level][1] = m1; }
     }
-    cl.sync();  // every CTA's partial max of this level is visible cluster-wide
+    if (cs > 1)
+      cl.sync();  // every CTA's partial max of this level is visible cluster-wide
+    else
+      __syncthreads();
     m0 = m1 = 0;
     for (int r = 0; r < cs; ++r) {
       const unsigned long long* rp = cl.map_shared_rank(&s_part[level][0], r);
@@ -632,7 +638,7 @@ __global__ void __launch_bounds__(kSplitClusterThreads) k_split_cluster(SplitPar
     int Ef[2][kMaxK], kvf[2];
     (void)split_exponents(P, b, s_mu, Ef, kvf, true);
   }
-  cl.sync();  // no CTA leaves while another may still read its s_part
+  if (cs > 1) cl.sync();  // no CTA leaves while another may still read its s_part
 }
 
 // ============================================================== NTT building blocks
