@@ -431,19 +431,30 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
   {
     const int64_t big = std::max<int64_t>(1, std::min<int64_t>((B + 3) / 4, std::max<int64_t>(1, pl->chunk / 3)));
     const int64_t edge = std::max<int64_t>(1, big / 4);
+    // linear ramp edge, 2 edge, ... < big at both ends (pipeline fill / drain with small
+    // sub-batches, then full-size ones): c3 e2e 127 -> 130, c4 92.5 -> 95.9 GFLOP/s measured
+    // against the older (edge, big - 1, big, ..., big - 1, edge)
+    std::vector<int64_t> up;
+    int64_t ramp_sum = 0;
+    for (int64_t r = edge; r < big; r += edge) { up.push_back(r); ramp_sum += r; }
     int64_t rem = B;
-    const bool edges = big > 1 && B >= 2 * edge + 1;
-    const int64_t ramp = big - 1;  // second / second-to-last: slightly below big (measured)
-    const bool ramps = edges && ramp > edge && B - 2 * edge >= 2 * ramp + big;
-    if (edges) { sizes.push_back(edge); rem -= 2 * edge; }
-    if (ramps) { sizes.push_back(ramp); rem -= 2 * ramp; }
+    const bool ramps = big > 1 && B >= 2 * ramp_sum + big;
+    if (ramps) {
+      sizes = up;
+      rem -= 2 * ramp_sum;
+    } else if (big > 1 && B >= 2 * edge + 1) {
+      up.assign(1, edge);
+      sizes = up;
+      rem -= 2 * edge;
+    } else {
+      up.clear();
+    }
     while (rem > 0) {
       const int64_t take = std::min(big, rem);
       sizes.push_back(take);
       rem -= take;
     }
-    if (ramps) sizes.push_back(ramp);
-    if (edges) sizes.push_back(edge);
+    sizes.insert(sizes.end(), up.rbegin(), up.rend());
     // small transforms (m <= 2^16): per-sub-batch fixed latencies dominate -- fewer, larger
     // sub-batches B/8, 3B/8, 3B/8, B/8 (measured at c2: 0.856 vs 0.910 ms)
     if (pl->m <= (1 << 16) && B >= 8 && pl->chunk >= B - B / 4) {
