@@ -449,11 +449,9 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
     } else {
       up.clear();
     }
-    while (rem > 0) {
-      const int64_t take = std::min(big, rem);
-      sizes.push_back(take);
-      rem -= take;
-    }
+    // the middle: ceil(rem / big) sub-batches of near-equal size (no small straggler)
+    const int64_t nmid = (rem + big - 1) / big;
+    for (int64_t i = 0; i < nmid; ++i) sizes.push_back(rem / nmid + (i < rem % nmid ? 1 : 0));
     sizes.insert(sizes.end(), up.rbegin(), up.rend());
     // small transforms (m <= 2^16): per-sub-batch fixed latencies dominate -- fewer, larger
     // sub-batches B/8, 3B/8, 3B/8, B/8 (measured at c2: 0.856 vs 0.910 ms)
