@@ -973,6 +973,12 @@ __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32
 #ifndef OZ_CI_MINB
 #define OZ_CI_MINB 3
 #endif
+#ifndef OZ_CI_SNAKE_MIN  // k_col_inv_crt tile order q0 q1 | q1 q0 | ... for these log2 R
+#define OZ_CI_SNAKE_MIN 6  // (measured: R = 2^6 c5 -3.6 %, 2^7 c4 -7 %; 2^4 c2 and 2^8 c3 +1 %)
+#endif
+#ifndef OZ_CI_SNAKE_MAX
+#define OZ_CI_SNAKE_MAX 7
+#endif
 #ifndef OZ_CF_MINB
 #define OZ_CF_MINB 5
 #endif
@@ -1699,17 +1705,22 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   for (int i = 0; i < NH; ++i) Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
   const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
   uint32_t nxt[E];
-  auto fetch = [&](int t) {  // tile t = 2 g + q
-    const int g = t >> 1, q = t & 1;
+  // tile t -> (group g, prime q): t = 2 g + (q xor snake(g)).  With OZ_CI_SNAKE the primes
+  // alternate q0 q1 | q1 q0 | q0 q1 ..., so each prime's column twiddles serve two tiles in a
+  // row (L1 reuse); the group's second tile runs Garner either way.
+  constexpr bool SNAKE = LOGR >= OZ_CI_SNAKE_MIN && LOGR <= OZ_CI_SNAKE_MAX;
+  auto tile_q = [](int t) { return SNAKE ? ((t & 1) ^ ((t >> 1) & 1)) : (t & 1); };
+  auto fetch = [&](int t) {
+    const int g = t >> 1, q = tile_q(t);
     const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * (int64_t)m + col;
 #pragma unroll
     for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0, LOGE>(tv, i) * C]);
   };
   if (ng > 0) fetch(0);
   __syncthreads();  // s_sc ready
-  uint32_t r0[NH];
+  uint32_t r0[NH];  // the group's first tile's residues
   for (int t = 0; t < 2 * ng; ++t) {
-    const int g = t >> 1, q = t & 1;
+    const int g = t >> 1, q = tile_q(t);
     uint32_t cur[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) cur[i] = nxt[i];
@@ -1732,7 +1743,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
         if (e * C < lim) rt[e * C] = rr[hslot(i)];
       }
     }
-    if (q == 0) {
+    if ((t & 1) == 0) {
 #pragma unroll
       for (int i = 0; i < NH; ++i) r0[i] = rr[i];
     } else {
@@ -1743,7 +1754,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
         const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
         const int h = hslot(i);
         if (e * C < lim) {
-          const long long Z = garner2(r0[h], rr[h], P.F);  // l.974
+          const long long Z = q ? garner2(r0[h], rr[h], P.F) : garner2(rr[h], r0[h], P.F);  // l.974
           if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + col + e * C] = Z;
           if constexpr (TS) {  // f4: TSAdd of z 2^-cexp (slot holds the TS words)
             Sacc[h * THREADS + tid] = ts_accum(Sacc[h * THREADS + tid], Z, s_ce[g]);
