@@ -11,12 +11,14 @@
 //                                 stages of the length-m forward NTT on column tiles
 //   k_row_fused<C,2PASS>  a3-a5  last log2 C DIF stages of the slices of one row, pointwise
 //                                 products + NTT-domain accumulation per Alg.8 group, first
-//                                 log2 C DIT stages of each group's inverse NTT
+//                                 log2 C DIT stages of each group's inverse NTT (one-pass
+//                                 plans: whole NTTs, groups spread over gridDim.z CTAs)
 //   k_col_inv_crt<R,C,PRUNE,TS>  a5-a7  last log2 R DIT stages, Garner CRT, exact 2^-c
 //                                 scaling and the DD (TS) sum in flush order per real conv
 //   k_finish_dd           a7     rr - ii, ir + ri, post-chirp, fp64 (inverse: conj, 1/n)
 // Variants: k_col_inv_crt_img / k_crt_finish_img (complex images, f2), k_crt_finish(_ts)
-// (one-pass plans, m <= 4096), k_col_inv + k_crt_finish (unit-sharded single transform,
+// (one-pass plans, m <= 4096; one thread per (output, real conv)), k_col_inv + k_crt_finish
+// (unit-sharded single transform,
 // SURVEY 8(e)), k_w_finalize (plan time), k_tap_permute (test taps).
 //
 // NTT arithmetic: canonical residues in [0,p), Shoup multiplication by precomputed
