@@ -95,6 +95,19 @@ def test_other_K_L(oz, K, L):
         assert np.array_equal(y[b].cpu().numpy(), yo)
 
 
+@pytest.mark.parametrize("n,K,L", [(5000, 8, 8), (5000, 1, 1), (40000, 4, 3), (40000, 8, 2)])
+def test_other_K_L_two_pass(oz, n, K, L):
+    """Other split caps through the two-pass NTT (column + row kernels; K = 8 is the cap,
+    kMaxK) and both split paths (cluster for n <= 2^15, multi-launch above)."""
+    x = workloads.phi_input(n, 4.0, seed=n + K * 10 + L, batch=1)
+    plan = oz.Plan(n, 1, K=K, L=L)
+    assert plan.m >= 8192
+    y, gt = plan.execute_taps(torch.from_numpy(x).cuda())
+    yo, ot = oplan(n, K, L).execute(x[0], taps=True)
+    check_taps(gt, ot, n, L, 0)
+    assert np.array_equal(y[0].cpu().numpy(), yo)
+
+
 def test_edge_cases(oz):
     n = 300
     plan = oz.Plan(n, 4)
