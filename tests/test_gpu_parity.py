@@ -166,7 +166,8 @@ def test_host_entry_point(oz):
     assert torch.equal(yh, yd)
 
 
-@pytest.mark.parametrize("n,B,ws", [(4096, 16, 0), (5000, 13, 3 << 20), (1000, 40, 0)])
+@pytest.mark.parametrize("n,B,ws", [(4096, 16, 0), (5000, 13, 3 << 20), (1000, 40, 0), (40000, 16, 0),
+                                    (40000, 23, 0)])
 def test_host_pipeline_schedules(oz, n, B, ws):
     """execute_host over sub-batches on two compute streams (edge sub-batches, disjoint
     workspace slots, slot reuse when the workspace chunk is smaller than the batch) gives
