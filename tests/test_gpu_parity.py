@@ -285,3 +285,18 @@ def test_max_digit_input(oz, n):
     assert np.min(np.abs(d[0, 0])) >= 2 ** (plan.alpha - 1) - 1
     check_taps(gt, ot, n, 3, 0)
     assert np.array_equal(y[0].cpu().numpy(), yo)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_sizes(oz, seed):
+    """Seeded random lengths (one- and two-pass, both split paths, prime and composite n)
+    and distributions: every tap and the fp64 output bit-exact against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 48000))
+    dist = ["uniform", "normal", "signexp"][seed % 3]
+    x = workloads.draw(dist, 2000 + seed, 1, n)
+    plan = oz.Plan(n, 1)
+    y, gt = plan.execute_taps(torch.from_numpy(x).cuda())
+    yo, ot = oplan(n).execute(x[0], taps=True)
+    check_taps(gt, ot, n, 3, 0)
+    assert np.array_equal(y[0].cpu().numpy(), yo), n
