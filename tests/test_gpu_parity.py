@@ -300,3 +300,18 @@ def test_random_sizes(oz, seed):
     yo, ot = oplan(n).execute(x[0], taps=True)
     check_taps(gt, ot, n, 3, 0)
     assert np.array_equal(y[0].cpu().numpy(), yo), n
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("mode", [dict(precision="ts"), dict(accum="image"), dict(conv="cyclic"),
+                                  dict(conv="cyclic", accum="image")])
+def test_random_sizes_modes(oz, seed, mode):
+    """As test_random_sizes, for the f1 / f2 / f4 plan modes against the oracle's modes."""
+    rng = np.random.default_rng(3000 + seed)
+    cyc = mode.get("conv") == "cyclic"
+    n = 1 << int(rng.integers(2, 16)) if cyc else int(rng.integers(1, 40000))
+    x = workloads.draw(["uniform", "normal", "signexp"][seed % 3], 4000 + seed, 1, n)
+    plan = oz.Plan(n, 1, **mode)
+    op = O.Plan(n, cyclic=cyc, image=mode.get("accum") == "image", ts=mode.get("precision") == "ts")
+    y = plan.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(y[0], op.execute(x[0])), (n, mode)
