@@ -65,8 +65,9 @@ struct Plan {
   struct GraphCache* graphs = nullptr;  // captured executes (ozfft_execute, small plans)
 };
 
-// CUDA graphs of ozfft_execute keyed by (in, out, direction): the launch sequence of a
-// small plan is latency-bound, so it is captured once and replayed (small-n).
+// CUDA graphs of ozfft_execute keyed by (in, out, direction): the launch sequence is
+// captured on the second execute with the same buffers and replayed from then on (SURVEY 7,
+// small-n latency; also the inter-kernel gaps of mid-size plans).
 struct GraphCache {
   struct Entry {
     const void* in;
@@ -77,6 +78,15 @@ struct GraphCache {
   };
   std::vector<Entry> entries;  // at most kMax, oldest replaced first
   size_t next = 0;
+  // (in, out, direction) keys seen once: a key is captured on its second execute, so a
+  // caller whose buffers change every call never pays for a capture
+  struct Key {
+    const void* in;
+    void* out;
+    int direction;
+  };
+  std::vector<Key> seen;  // at most kMax, oldest replaced first
+  size_t seen_next = 0;
   void* capture = nullptr;     // cudaStream_t used for capture
   static constexpr size_t kMax = 8;
 };
