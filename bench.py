@@ -301,7 +301,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
-    # timed region: the production path (no stage timers; small plans replay a CUDA graph)
+    # timed region: the production path (no stage timers; plans with batch*m <= 2^25 replay a
+    # CUDA graph, captured during the warm-up)
     launches0 = oz.kernel_launches()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
