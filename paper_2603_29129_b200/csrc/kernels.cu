@@ -31,6 +31,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <type_traits>
 
@@ -2059,14 +2060,19 @@ static void set_smem(K kern, size_t bytes) {
 #ifndef OZ_SPLIT_CLUSTER
 #define OZ_SPLIT_CLUSTER 1  // fused one-launch split for n <= kSplitClusterMaxLen
 #endif
+// SM count of the current device (cached per device id; a process may drive several GPUs)
 static int sm_count() {
-  static const int c = [] {
-    int d = 0, v = 148;
-    cudaGetDevice(&d);
+  static std::atomic<int> cache[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) d = 0;
+  int v = cache[d].load(std::memory_order_relaxed);
+  if (v == 0) {
+    v = 148;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
-    return v;
-  }();
-  return c;
+    cache[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
 }
 #ifndef OZ_ROW_ZMAX
 #define OZ_ROW_ZMAX 18  // most CTAs one (transform, part, prime) row of a one-pass plan uses
@@ -2099,14 +2105,18 @@ static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cud
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    // static + dynamic shared memory may pass 48 KB: opt in once to the largest chunk
-    static const bool smem_set = [] {
+    // static + dynamic shared memory may pass 48 KB: opt in once per device to the largest
+    // chunk (function attributes are per device)
+    static std::atomic<bool> smem_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!smem_set[dev].load(std::memory_order_relaxed)) {
       const int mx = 160 * 1024;
       cudaFuncSetAttribute(k_split_cluster<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
       cudaFuncSetAttribute(k_split_cluster<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      return true;
-    }();
-    (void)smem_set;
+      smem_set[dev].store(true, std::memory_order_relaxed);
+    }
     prof_mark(pl, OZFFT_STAGE_SPLIT_MAX, true, st);
     if (pl.ts)
       cudaLaunchKernelEx(&cfg, k_split_cluster<true>, SP, chunk);
