@@ -171,7 +171,8 @@ ozfft_status ozfft_plan_get_info(const ozfft_plan* plan, ozfft_plan_info* info);
  * info.workspace_bytes, both 256-byte aligned) and precompute on `stream`: uploads
  * tables, splits omega~* (Alg.6) and runs its 4K forward NTTs into the
  * cached W spectra, using the workspace as scratch (no device allocation).
- * Synchronizes `stream` (plan time, not on the hot path).
+ * Synchronizes `stream` (plan time, not on the hot path).  Re-binding is allowed; it
+ * drops the execute graphs captured against the previous buffers.
  * Errors: INVALID_ARGUMENT, MISALIGNED, BUFFER_TOO_SMALL, CUDA. */
 ozfft_status ozfft_plan_bind(ozfft_plan* plan, void* persistent, size_t persistent_bytes,
                              void* workspace, size_t workspace_bytes, void* stream);
@@ -179,9 +180,10 @@ ozfft_status ozfft_plan_bind(ozfft_plan* plan, void* persistent, size_t persiste
 /* y = DFT(x) (direction -1) or x = DFT^-1(y) (direction +1, P:158-160,
  * computed as conj(DFT(conj(y)))/n with RN division, ruling 16), for the plan's
  * batch.  `in` and `out` are device complex128 [batch][n]; in == out is allowed.
- * Asynchronous on `stream`.  Small plans (batch * m <= 2^22, env OZFFT_GRAPH_MAX_WORK)
- * capture the launch sequence once per (in, out, direction) as a CUDA graph and replay
- * it (up to 8 cached per plan); not while the stage profiler is on.
+ * Asynchronous on `stream`.  Plans with batch * m <= 2^25 (env OZFFT_GRAPH_MAX_WORK) and
+ * one workspace chunk capture the launch sequence as a CUDA graph on the second execute
+ * with the same (in, out, direction) and replay it from then on (up to 8 cached per plan;
+ * a re-bind drops them); not while the stage profiler is on.
  * Errors: NOT_BOUND, INVALID_ARGUMENT, MISALIGNED, CUDA. */
 ozfft_status ozfft_execute(const ozfft_plan* plan, const void* in, void* out, int direction,
                            void* stream);

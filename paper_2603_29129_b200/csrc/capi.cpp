@@ -292,6 +292,13 @@ ozfft_status ozfft_plan_bind(ozfft_plan* pl, void* persistent, size_t pbytes, vo
   ozfft_status s = check_cuda(cudaSetDevice(pl->device), "cudaSetDevice");
   if (s) return s;
   cudaStream_t st = (cudaStream_t)stream;
+  if (pl->graphs) {  // captured executes hold the previous buffers' addresses
+    cudaDeviceSynchronize();
+    for (const GraphCache::Entry& e : pl->graphs->entries) cudaGraphExecDestroy((cudaGraphExec_t)e.exec);
+    pl->graphs->entries.clear();
+    pl->graphs->seen.clear();
+    pl->graphs->next = pl->graphs->seen_next = 0;
+  }
   pl->pers = (uint8_t*)persistent;
   pl->ws = (uint8_t*)workspace;
   const int64_t m = pl->m;

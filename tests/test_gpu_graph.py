@@ -57,3 +57,28 @@ def test_changing_buffers(oz):
     for _ in range(2):
         for x, r in zip(xs, refs):
             assert torch.equal(plan.forward(x), r)  # new output buffer every call
+
+
+def test_rebind_drops_graphs(oz):
+    """Re-binding the plan to new persistent / workspace buffers (ozfft_plan_bind again)
+    must not replay graphs captured against the old ones."""
+    n, B = 3000, 2
+    x = torch.from_numpy(workloads.draw("normal", 91, B, n)).cuda()
+    plan = oz.Plan(n, B)
+    out = torch.empty_like(x)
+    for _ in range(3):  # direct, capture, replay
+        plan.forward(x, out=out)
+    ref = out.clone()
+    old_ws, old_pers = plan.workspace, plan.persistent
+    plan.persistent = torch.empty_like(plan.persistent)
+    plan.workspace = torch.empty_like(plan.workspace)
+    lib = oz.load_library()
+    rc = lib.ozfft_plan_bind(plan._h, plan.persistent.data_ptr(), plan.persistent.numel(),
+                             plan.workspace.data_ptr(), plan.workspace.numel(), None)
+    assert rc == 0
+    old_ws.fill_(0xFF)
+    old_pers.fill_(0xFF)  # a stale graph would read garbage tables (twiddles, W, chirp)
+    for _ in range(3):
+        out.zero_()
+        plan.forward(x, out=out)
+        assert torch.equal(out, ref)
