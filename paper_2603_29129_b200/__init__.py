@@ -131,8 +131,8 @@ def kernel_launches() -> int:
     return int(load_library().ozfft_kernel_launches())
 
 
-def _stream_ptr(stream) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream_ptr(stream, device=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
 
 
@@ -184,7 +184,7 @@ class Plan:
             self.workspace = torch.empty(max(info.workspace_bytes, 256), dtype=torch.uint8, device=dev)
             _check(self._lib.ozfft_plan_bind(h, self.persistent.data_ptr(), self.persistent.numel(),
                                              self.workspace.data_ptr(), self.workspace.numel(),
-                                             _stream_ptr(stream)))
+                                             _stream_ptr(stream, dev)))
         info2 = PlanInfo()
         _check(self._lib.ozfft_plan_get_info(h, C.byref(info2)))
         self.cached_ntts = info2.cached_ntts
@@ -210,8 +210,13 @@ class Plan:
 
     def execute(self, x: torch.Tensor, direction: int = -1, out=None, stream=None) -> torch.Tensor:
         out = self._check_io(x, out)
-        _check(self._lib.ozfft_execute(self._h, x.data_ptr(), out.data_ptr(), direction,
-                                       _stream_ptr(stream)))
+        if self.device.index is None or torch.cuda.current_device() == self.device.index:
+            _check(self._lib.ozfft_execute(self._h, x.data_ptr(), out.data_ptr(), direction,
+                                           _stream_ptr(stream, self.device)))
+        else:
+            with torch.cuda.device(self.device):  # the library launches on the current device
+                _check(self._lib.ozfft_execute(self._h, x.data_ptr(), out.data_ptr(), direction,
+                                               _stream_ptr(stream, self.device)))
         return out
 
     def forward(self, x, out=None, stream=None):
@@ -230,7 +235,7 @@ class Plan:
             out_host = torch.empty_like(x_host, pin_memory=x_host.is_pinned())
         with torch.cuda.device(self.device):
             _check(self._lib.ozfft_execute_host(self._h, x_host.data_ptr(), out_host.data_ptr(),
-                                                direction, _stream_ptr(stream)))
+                                                direction, _stream_ptr(stream, self.device)))
         return out_host
 
     def execute_taps(self, x: torch.Tensor, direction: int = -1, stream=None):
@@ -247,8 +252,9 @@ class Plan:
                  W=z(2, K, 2, m, dt=torch.int32))
         tp = Taps(*[t[f].data_ptr() for f, _ in Taps._fields_])
         out = torch.empty_like(x)
-        _check(self._lib.ozfft_execute_taps(self._h, x.data_ptr(), out.data_ptr(), direction,
-                                            _stream_ptr(stream), C.byref(tp)))
+        with torch.cuda.device(dev):
+            _check(self._lib.ozfft_execute_taps(self._h, x.data_ptr(), out.data_ptr(), direction,
+                                                _stream_ptr(stream, dev), C.byref(tp)))
         torch.cuda.synchronize(dev)
         for k in ("X", "Z", "res", "W"):  # uint32 payloads carried in int32 tensors
             t[k] = t[k].to(torch.int64) & 0xFFFFFFFF
@@ -256,7 +262,8 @@ class Plan:
 
     def stats(self, stream=None) -> dict:
         s = ExecStats()
-        _check(self._lib.ozfft_last_stats(self._h, C.byref(s), _stream_ptr(stream)))
+        with torch.cuda.device(self.device):
+            _check(self._lib.ozfft_last_stats(self._h, C.byref(s), _stream_ptr(stream, self.device)))
         return dict(k=list(s.k), fwd_ntts=s.fwd_ntts, inv_ntts=s.inv_ntts,
                     cached_ntts=s.cached_ntts, groups=s.groups, nonfinite=s.nonfinite,
                     flags=s.flags)
@@ -270,7 +277,8 @@ class Plan:
         """{stage: (total_ms, launches)} since enable / last read (synchronizes)."""
         ms = (C.c_double * len(STAGES))()
         ln = (C.c_int64 * len(STAGES))()
-        _check(self._lib.ozfft_profile_read(self._h, ms, ln, _stream_ptr(stream)))
+        with torch.cuda.device(self.device):
+            _check(self._lib.ozfft_profile_read(self._h, ms, ln, _stream_ptr(stream, self.device)))
         return {s: (ms[i], ln[i]) for i, s in enumerate(STAGES)}
 
     # ------------------------------------------------------------------ sharding
@@ -279,11 +287,13 @@ class Plan:
 
     def shard_partial(self, x: torch.Tensor, shard: int, nshards: int, residues: torch.Tensor,
                       direction: int = -1, stream=None):
-        _check(self._lib.ozfft_shard_partial(self._h, shard, nshards, x.data_ptr(), direction,
-                                             residues.data_ptr(), _stream_ptr(stream)))
+        with torch.cuda.device(self.device):
+            _check(self._lib.ozfft_shard_partial(self._h, shard, nshards, x.data_ptr(), direction,
+                                                 residues.data_ptr(), _stream_ptr(stream, self.device)))
 
     def shard_finish(self, residues: torch.Tensor, out: torch.Tensor, direction: int = -1,
                      stream=None):
-        _check(self._lib.ozfft_shard_finish(self._h, residues.data_ptr(), out.data_ptr(),
-                                            direction, _stream_ptr(stream)))
+        with torch.cuda.device(self.device):
+            _check(self._lib.ozfft_shard_finish(self._h, residues.data_ptr(), out.data_ptr(),
+                                                direction, _stream_ptr(stream, self.device)))
         return out
