@@ -180,6 +180,8 @@ ozfft_status ozfft_plan_bind(ozfft_plan* plan, void* persistent, size_t persiste
 /* y = DFT(x) (direction -1) or x = DFT^-1(y) (direction +1, P:158-160,
  * computed as conj(DFT(conj(y)))/n with RN division, ruling 16), for the plan's
  * batch.  `in` and `out` are device complex128 [batch][n]; in == out is allowed.
+ * The calling thread's current device must be the plan's (desc.device), as for every
+ * call that takes a stream; `stream` belongs to that device.
  * Asynchronous on `stream`.  Plans with batch * m <= 2^25 (env OZFFT_GRAPH_MAX_WORK) and
  * one workspace chunk capture the launch sequence as a CUDA graph on the second execute
  * with the same (in, out, direction) and replay it from then on (up to 8 cached per plan;
