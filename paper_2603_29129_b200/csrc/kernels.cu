@@ -660,7 +660,9 @@ __device__ __forceinline__ uint2 tw_load(const uint2* p) {
 // x is [NV][E] (E = elements per thread); the group occupies x[v][off .. off + 2^S).
 // UNIT: the caller guarantees rmod == 0 and gstep == 1 (the step-1 round of a row), so the
 // twiddle index is compile-time and the butterflies with T[h] = w^0 = 1 skip the product.
-template <int S, int NV, int E, bool UNIT = false, bool SMEM_T = false>
+// ZHI: the upper half of the group's block is zero on entry (zero-padded input, n <= m/2),
+// so the first stage is (u, 0) -> (u, u * w).
+template <int S, int NV, int E, bool UNIT = false, bool SMEM_T = false, bool ZHI = false>
 __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_t rmod,
                                           uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
   if constexpr (UNIT) {
@@ -674,6 +676,12 @@ __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_
 #pragma unroll
     for (int k = 0; k < (1 << S); ++k) {
       if (k & d) continue;
+      if (ZHI && st == S - 1) {
+        const uint2 w = tw_load<SMEM_T>(&T[h + rmod + (uint32_t)(k & (d - 1)) * gstep]);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) x[v][off + k + d] = mul_shoup(x[v][off + k], w, p);
+        continue;
+      }
       if (UNIT && (k & (d - 1)) == 0) {  // (u - v) * 1
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
@@ -795,8 +803,8 @@ struct Tw0 {
   uint32_t gb, gs;
 };
 
-template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, class LoadF,
-          class StoreF>
+template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, bool ZHI,
+          class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int tv,
                                               uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
@@ -818,15 +826,16 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
     const uint32_t g = (uint32_t)(tv + u * RT::Tv);
     const uint32_t rmod = gb_mod + (g & (step - 1)) * gs;
     constexpr bool unit = UNIT && RT::logstep == 0;  // rmod == gb_mod == 0, gstep == gs == 1
+    constexpr bool zhi = ZHI && !INV && R == 0;  // first DIF stage of the first round
     if constexpr (T0S && RT::logstep == 0) {  // staged step-1 twiddles
       if constexpr (INV)
         dit_group<RT::S, NV, E, false, true>(x, u * (1 << RT::S), t0.gb, t0.gs, t0.T, p);
       else
-        dif_group<RT::S, NV, E, false, true>(x, u * (1 << RT::S), t0.gb, t0.gs, t0.T, p);
+        dif_group<RT::S, NV, E, false, true, zhi>(x, u * (1 << RT::S), t0.gb, t0.gs, t0.T, p);
     } else if constexpr (INV) {
       dit_group<RT::S, NV, E, unit>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     } else {
-      dif_group<RT::S, NV, E, unit>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+      dif_group<RT::S, NV, E, unit, false, zhi>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     }
   }
 #pragma unroll
@@ -846,16 +855,16 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
   }
 }
 
-template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, class LoadF,
-          class StoreF>
+template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, bool ZHI,
+          class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int tv,
                                                uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                                uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
                                                uint32_t p, LoadF& load_first, StoreF& store_last) {
   if constexpr (R < RoundT<LOGN, INV, 0, LOGE>::nr) {
-    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE, UNIT, T0S>(x, tv, sm, gb_mod, gs, T, t0, p,
+    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE, UNIT, T0S, ZHI>(x, tv, sm, gb_mod, gs, T, t0, p,
                                                          load_first, store_last);
-    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE, UNIT, T0S>(x, tv, sm, gb_mod, gs, T, t0, p,
+    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE, UNIT, T0S, ZHI>(x, tv, sm, gb_mod, gs, T, t0, p,
                                                               load_first,
                                                    store_last);
   }
@@ -872,7 +881,7 @@ __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int
 // consumes the final values.  The buffers must be free for writes on entry.  UNIT: the
 // caller passes gb_mod == 0 and gs == 1 (rows), enabling the compile-time step-1 round.
 template <int LOGN, bool INV, int CB, int NV, int LOGE = 4, bool UNIT = false, bool T0S = false,
-          class LoadF, class StoreF>
+          bool ZHI = false, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
                                               uint32_t p, LoadF&& load_first, StoreF&& store_last) {
@@ -882,7 +891,7 @@ __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV],
       for (int v = 0; v < NV; ++v) store_last(v, 0, 0u, load_first(v, 0, 0u));
   } else {
     uint32_t x[NV][1 << LOGE];
-    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE, UNIT, T0S>(x, tv, sm, gb_mod, gs, T, t0, p,
+    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE, UNIT, T0S, ZHI>(x, tv, sm, gb_mod, gs, T, t0, p,
                                                           load_first, store_last);
   }
 }
@@ -899,12 +908,12 @@ __device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, uint3
       [&](int, int i, uint32_t e, uint32_t v) { store_last(i, e, v); });
 }
 // ... with the step-1 round's twiddles read from a staged copy (Tw0).
-template <int LOGN, bool INV, int CB, int LOGE = 4, class LoadF, class StoreF>
+template <int LOGN, bool INV, int CB, int LOGE = 4, bool ZHI = false, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_t0(int tv, uint32_t* __restrict__ sm, uint32_t gb_mod,
                                            uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
                                            uint32_t p, LoadF&& load_first, StoreF&& store_last) {
   uint32_t* const sms[1] = {sm};
-  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, false, true>(
+  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, false, true, ZHI>(
       tv, sms, gb_mod, gs, T, t0, p, [&](int, int i, uint32_t e) { return load_first(i, e); },
       [&](int, int i, uint32_t e, uint32_t v) { store_last(i, e, v); });
 }
@@ -973,6 +982,9 @@ __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32
 #ifndef OZ_IMG_CB_SHIFT
 #define OZ_IMG_CB_SHIFT 1
 #endif
+#ifndef OZ_COL_ZHI
+#define OZ_COL_ZHI 1  // forward column pass: zero upper half of padded inputs (dif_group ZHI)
+#endif
 #ifndef OZ_CI_MINB
 #define OZ_CI_MINB 3
 #endif
@@ -1009,7 +1021,9 @@ __host__ __device__ constexpr int col_s1(int logR) {
 // Forward column pass: global DIF stages len = m .. 2C on columns of the R x C view.
 // One CTA per (transform, prime, part, column block) loops over the part's slices; the
 // next slice's column tile is loaded while the current one is transformed.
-template <int LOGR, int LOGC, bool IMG>
+// ZHI: padded plan (n <= m/2): rows >= R/2 of every column are zero, the first DIF stage
+// is a plain product (dif_group ZHI).
+template <int LOGR, int LOGC, bool IMG, bool ZHI>
 __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(ColParams P) {
   extern __shared__ uint32_t smem[];
   constexpr int LOGCB = col_log_cb(LOGR, LOGC);
@@ -1070,7 +1084,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(C
     if (s + 1 < ka) fetch(s + 1);
     if (s > 0) __syncthreads();  // smem tile free
     uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (int64_t)m + col;
-    sub_ntt_t0<LOGR, false, Cb, LOGE>(
+    sub_ntt_t0<LOGR, false, Cb, LOGE, ZHI>(
         tv, smem + c, col, C, T, Tw0{tw0, (uint32_t)c, (uint32_t)Cb}, p,
         [&](int i, uint32_t) -> uint32_t { return cur[i]; },
         [&](int, uint32_t e, uint32_t val) { out[e * C] = val; });
@@ -2204,14 +2218,20 @@ bool decomposition_supported(int logR, int logC) {
 
 
 static void launch_col_fwd(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
-                           const ColParams& CP) {
+                           const ColParams& CP, bool zhi = false) {
   dispatch_rc(logR, logC, [&](auto I, auto J) {
-    if (CP.image) {
-      set_smem(k_col_fwd<I.value, J.value, true>, c.col_fwd_smem);
-      k_col_fwd<I.value, J.value, true><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
+    if (CP.image && zhi) {
+      set_smem(k_col_fwd<I.value, J.value, true, true>, c.col_fwd_smem);
+      k_col_fwd<I.value, J.value, true, true><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
+    } else if (CP.image) {
+      set_smem(k_col_fwd<I.value, J.value, true, false>, c.col_fwd_smem);
+      k_col_fwd<I.value, J.value, true, false><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
+    } else if (zhi) {
+      set_smem(k_col_fwd<I.value, J.value, false, true>, c.col_fwd_smem);
+      k_col_fwd<I.value, J.value, false, true><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
     } else {
-      set_smem(k_col_fwd<I.value, J.value, false>, c.col_fwd_smem);
-      k_col_fwd<I.value, J.value, false><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
+      set_smem(k_col_fwd<I.value, J.value, false, false>, c.col_fwd_smem);
+      k_col_fwd<I.value, J.value, false, false><<<nblk, c.col_threads, c.col_fwd_smem, st>>>(CP);
     }
   });
 }
@@ -2396,7 +2416,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     fill_iota(pl, CP.io);
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
     prof_mark(pl, OZFFT_STAGE_COL_FWD, true, st);
-    launch_col_fwd(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
+    launch_col_fwd(pl.logR, pl.logC, (unsigned)nblk, c, st, CP, OZ_COL_ZHI && 2 * n <= m);
     prof_mark(pl, OZFFT_STAGE_COL_FWD, false, st);
     count_launches(1);
     s = cuda_check("k_col_fwd");
