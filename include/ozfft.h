@@ -128,7 +128,7 @@ typedef struct {
   int64_t cached_ntts;   /* plan-time forward NTTs of omega~* slices                 */
   int64_t groups;        /* Alg.8 flush groups over the batch                        */
   int64_t nonfinite;     /* transforms whose input had NaN/Inf (output set to NaN)   */
-  uint32_t flags;        /* bit0: some input non-finite; bit1: CRT range fix (never expected) */
+  uint32_t flags;        /* bit0: some input non-finite; bits 1-31: reserved, 0 */
   int32_t reserved;
 } ozfft_exec_stats;
 
@@ -200,6 +200,12 @@ ozfft_status ozfft_execute(const ozfft_plan* plan, const void* in, void* out, in
  * Errors: NOT_BOUND, INVALID_ARGUMENT, CUDA. */
 ozfft_status ozfft_execute_host(const ozfft_plan* plan, const double* in, double* out,
                                 int direction, void* stream);
+
+/* The sub-batch sizes ozfft_execute_host uses for this plan (host-side planning, no device
+ * work, callable before bind): writes min(count, cap) sizes to `sizes` (may be NULL) and
+ * returns the count (-1 for a NULL plan).  Every size is <= plan_get_info's chunk (one
+ * workspace slot) and they sum to the batch. */
+int64_t ozfft_host_subbatches(const ozfft_plan* plan, int64_t* sizes, int64_t cap);
 
 /* As ozfft_execute, additionally writing the stage outputs listed in ozfft_taps.
  * Requires info.chunk == info.batch.  Test-only; not on the hot path. */

@@ -69,7 +69,8 @@ EXPORTS = ["ozfft_plan_create", "ozfft_plan_get_info", "ozfft_plan_bind", "ozfft
            "ozfft_execute_host", "ozfft_execute_taps", "ozfft_last_stats",
            "ozfft_shard_residue_bytes", "ozfft_shard_partial", "ozfft_shard_finish",
            "ozfft_plan_destroy", "ozfft_status_string", "ozfft_last_error_string",
-           "ozfft_version", "ozfft_profile_enable", "ozfft_profile_read", "ozfft_kernel_launches"]
+           "ozfft_version", "ozfft_profile_enable", "ozfft_profile_read", "ozfft_kernel_launches",
+           "ozfft_host_subbatches"]
 
 STAGES = ["split_max", "split_digits", "col_fwd", "row_fused", "col_inv", "crt_finish"]
 
@@ -100,6 +101,8 @@ def load_library() -> C.CDLL:
     L.ozfft_plan_destroy.argtypes = [vp]
     L.ozfft_profile_enable.argtypes = [vp, i32]
     L.ozfft_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), vp]
+    L.ozfft_host_subbatches.argtypes = [vp, C.POINTER(C.c_int64), i64]
+    L.ozfft_host_subbatches.restype = i64
     L.ozfft_kernel_launches.argtypes = []
     L.ozfft_kernel_launches.restype = u64
     for f in ("ozfft_plan_create", "ozfft_plan_get_info", "ozfft_plan_bind", "ozfft_execute",
@@ -131,6 +134,15 @@ def kernel_launches() -> int:
     return int(load_library().ozfft_kernel_launches())
 
 
+def _normalize_device(device) -> torch.device:
+    """torch.device('cuda', i) with an explicit index: None / 'cuda' mean the current device,
+    so the C plan, its buffers and the inputs' device checks all name the same GPU."""
+    d = torch.device("cuda") if device is None else torch.device(device)
+    if d.type != "cuda":
+        raise ValueError(f"ozfft runs on CUDA devices only, got {d}")
+    return torch.device("cuda", torch.cuda.current_device() if d.index is None else d.index)
+
+
 def _stream_ptr(stream, device=None) -> int:
     s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
@@ -159,15 +171,14 @@ class Plan:
         if not torch.cuda.is_available():
             raise RuntimeError("ozfft needs a CUDA device (sm_100a); there is no CPU fallback")
         self._lib = load_library()
-        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        self.device = dev
+        self.device = dev = _normalize_device(device)
         if conv not in self.CONV:
             raise ValueError(f"conv must be one of {sorted(self.CONV)}")
         if accum not in self.ACCUM:
             raise ValueError(f"accum must be one of {sorted(self.ACCUM)}")
         if precision not in self.PREC:
             raise ValueError(f"precision must be one of {sorted(self.PREC)}")
-        d = PlanDesc(n=n, batch=batch, K=K, L=L, p0=p0, p1=p1, device=dev.index or 0,
+        d = PlanDesc(n=n, batch=batch, K=K, L=L, p0=p0, p1=p1, device=dev.index,
                      conv_mode=self.CONV[conv], accum_mode=self.ACCUM[accum],
                      precision=self.PREC[precision], max_workspace_bytes=max_workspace_bytes)
         h = C.c_void_p()
@@ -210,7 +221,7 @@ class Plan:
 
     def execute(self, x: torch.Tensor, direction: int = -1, out=None, stream=None) -> torch.Tensor:
         out = self._check_io(x, out)
-        if self.device.index is None or torch.cuda.current_device() == self.device.index:
+        if torch.cuda.current_device() == self.device.index:
             _check(self._lib.ozfft_execute(self._h, x.data_ptr(), out.data_ptr(), direction,
                                            _stream_ptr(stream, self.device)))
         else:

@@ -81,7 +81,12 @@ void prof_mark(const Plan& pl, int stage, bool begin, void* stream) {
 
 static uint64_t align256(uint64_t v) { return (v + 255) & ~(uint64_t)255; }
 
-static void layout(Plan& pl) {
+// Plan memory layout.  The workspace is [batch-sized stats + schedules][chunk x per-transform
+// regions]; chunk is the largest count whose whole workspace (fixed regions, 256-byte
+// alignment of every region, per-transform regions) stays within max_workspace_bytes, and the
+// bind-time scratch must fit the cap too.  Fails (OZFFT_ERR_BUFFER_TOO_SMALL) if not even one
+// transform fits.
+static ozfft_status layout(Plan& pl) {
   const int64_t n = pl.n, m = pl.m, K = pl.K, L = pl.L, G = K * K;
   // persistent
   uint64_t o = 0;
@@ -91,33 +96,40 @@ static void layout(Plan& pl) {
   pl.poff.wsplit = o; o = align256(o + (uint64_t)(2 + 2 * K) * 4);
   pl.poff.end = o;
   pl.persistent_bytes = o;
-  // workspace: per-transform bytes of the chunked region
   const bool two = pl.logR > 0;
-  const uint64_t per = (uint64_t)2 * K * 8 + (uint64_t)8 * K * n +
-                       (two ? (uint64_t)16 * K * m + (uint64_t)32 * G * m : 0) +
-                       (uint64_t)32 * G * n + (uint64_t)32 * n + (two ? (uint64_t)64 * n : 0);
-  int64_t chunk = (int64_t)std::max<uint64_t>(1, pl.max_ws / std::max<uint64_t>(per, 1));
-  chunk = std::min<int64_t>(chunk, pl.batch);
-  chunk = std::min<int64_t>(chunk, 65535);  // per-transform kernels index transforms by gridDim.y
-  pl.chunk = chunk;
-  o = 0;
-  pl.woff.stats = o;  o = align256(o + (uint64_t)pl.batch * stats_stride(K) * 4);
-  pl.woff.sched = o;  o = align256(o + (uint64_t)pl.batch * 4 * sched_stride(K, L) * 4);
-  pl.woff.mu = o;     o = align256(o + (uint64_t)chunk * 2 * K * 8);
-  pl.woff.digits = o; o = align256(o + (uint64_t)chunk * 2 * K * n * 4);
-  pl.woff.Y = o;      o = align256(o + (two ? (uint64_t)chunk * 4 * K * m * 4 : 0));
-  pl.woff.G = o;      o = align256(o + (two ? (uint64_t)chunk * 8 * G * m * 4 : 0));
-  pl.woff.res = o;    o = align256(o + (uint64_t)chunk * 8 * G * n * 4);
-  pl.woff.S = o;      o = align256(o + (two ? (uint64_t)chunk * 4 * n * 16 : 0));
-  pl.woff.io_in = o;  o = align256(o + (uint64_t)chunk * n * 16);
-  pl.woff.io_out = o; o = align256(o + (uint64_t)chunk * n * 16);
-  pl.woff.end = o;
+  auto place = [&](int64_t chunk) {
+    uint64_t w = 0;
+    pl.woff.stats = w;  w = align256(w + (uint64_t)pl.batch * stats_stride(K) * 4);
+    pl.woff.sched = w;  w = align256(w + (uint64_t)pl.batch * 4 * sched_stride(K, L) * 4);
+    pl.woff.mu = w;     w = align256(w + (uint64_t)chunk * 2 * K * 8);
+    pl.woff.digits = w; w = align256(w + (uint64_t)chunk * 2 * K * n * 4);
+    pl.woff.Y = w;      w = align256(w + (two ? (uint64_t)chunk * 4 * K * m * 4 : 0));
+    pl.woff.G = w;      w = align256(w + (two ? (uint64_t)chunk * 8 * G * m * 4 : 0));
+    pl.woff.res = w;    w = align256(w + (uint64_t)chunk * 8 * G * n * 4);
+    pl.woff.S = w;      w = align256(w + (two ? (uint64_t)chunk * 4 * n * 16 : 0));
+    pl.woff.io_in = w;  w = align256(w + (uint64_t)chunk * n * 16);
+    pl.woff.io_out = w; w = align256(w + (uint64_t)chunk * n * 16);
+    pl.woff.end = w;
+    return w;
+  };
   // bind-time scratch (launch_plan_precompute: mu, digits, stats, Y, X of omega~*) reuses
   // the workspace before the first execute
   const uint64_t bind_scratch = align256((uint64_t)2 * K * 8) + align256((uint64_t)2 * K * m * 4) +
                                 align256((uint64_t)stats_stride(K) * 4) +
                                 2 * align256((uint64_t)4 * K * m * 4);
+  const uint64_t fixed = place(0);  // batch-sized regions + alignment of the empty ones
+  const uint64_t per = place(1) - fixed + 10 * 256;  // one transform, padding headroom
+  if (fixed + per > pl.max_ws || bind_scratch > pl.max_ws)
+    return fail(OZFFT_ERR_BUFFER_TOO_SMALL,
+                "max_workspace_bytes is below the workspace of a single transform");
+  int64_t chunk = (int64_t)std::max<uint64_t>(1, (pl.max_ws - fixed) / per);
+  chunk = std::min<int64_t>(chunk, pl.batch);
+  chunk = std::min<int64_t>(chunk, 65535);  // per-transform kernels index transforms by gridDim.y
+  while (chunk > 1 && place(chunk) > pl.max_ws) --chunk;  // exact check (alignment)
+  pl.chunk = chunk;
+  o = place(chunk);
   pl.workspace_bytes = std::max<uint64_t>(o, bind_scratch);
+  return OZFFT_OK;
 }
 
 #ifndef OZFFT_GRAPH_MAX_WORK_DEFAULT
@@ -255,7 +267,11 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     delete pl;
     return s;
   }
-  layout(*pl);
+  s = layout(*pl);
+  if (s) {
+    delete pl;
+    return s;
+  }
   *out = pl;
   return OZFFT_OK;
 }
@@ -289,8 +305,20 @@ ozfft_status ozfft_plan_bind(ozfft_plan* pl, void* persistent, size_t pbytes, vo
     return fail(OZFFT_ERR_MISALIGNED, "plan buffers must be 256-byte aligned");
   if (pbytes < pl->persistent_bytes || wbytes < pl->workspace_bytes)
     return fail(OZFFT_ERR_BUFFER_TOO_SMALL, "persistent/workspace smaller than plan_get_info");
+  // the caller's current device is restored on every return path
+  int caller_dev = -1;
+  if (cudaGetDevice(&caller_dev) != cudaSuccess) caller_dev = -1;
+  struct Restore {
+    int d;
+    ~Restore() {
+      if (d >= 0) cudaSetDevice(d);
+    }
+  } restore{caller_dev};
   ozfft_status s = check_cuda(cudaSetDevice(pl->device), "cudaSetDevice");
   if (s) return s;
+  // from here on the plan's device state changes: it is unbound until every step succeeded
+  // (a failed re-bind must not leave half-initialised tables behind a "bound" plan)
+  pl->bound = false;
   cudaStream_t st = (cudaStream_t)stream;
   if (pl->graphs) {  // captured executes hold the previous buffers' addresses
     cudaDeviceSynchronize();
@@ -438,23 +466,10 @@ ozfft_status ozfft_execute(const ozfft_plan* pl, const void* in, void* out, int 
   return OZFFT_OK;
 }
 
-// Concurrent host pipeline (the whole batch fits one workspace chunk): sub-batches use
-// disjoint workspace and staging slots, so they need no slot-reuse waits and alternate
-// between two compute streams -- the small first / last sub-batches (short pipeline fill
-// and drain) overlap the large ones on the GPU instead of running it half-empty.
-// Host-buffer pipeline: the batch runs as sub-batches (small first and last ones shorten
-// the fill -- the first H2D -- and the drain -- the last D2H); sub-batch j uses staging and
-// workspace slot j mod nslots and alternates between two compute streams, so H2D, D2H and
-// the kernels of neighbouring sub-batches overlap, and the small edge sub-batches share the
-// GPU with large ones instead of running it half-empty.  Slot reuse waits for the previous
-// occupant's kernels (input consumed) and D2H (output and workspace free).
-ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* out, int direction,
-                                void* stream) {
-  ozfft_status s = check_exec(pl, in, out, direction);
-  if (s) return s;
-  ozfft_plan* mp = const_cast<ozfft_plan*>(pl);
-  cudaStream_t st = (cudaStream_t)stream;
-  const int64_t n = pl->n, B = pl->batch;
+// Sub-batch sizes of ozfft_execute_host (every size <= pl.chunk, summing to the batch).
+static std::vector<int64_t> host_subbatches(const Plan& plan) {
+  const Plan* pl = &plan;
+  const int64_t B = pl->batch;
   std::vector<int64_t> sizes;
   {
     const int64_t big = std::max<int64_t>(1, std::min<int64_t>((B + 3) / 4, std::max<int64_t>(1, pl->chunk / 3)));
@@ -484,9 +499,13 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
     // small transforms (m <= 2^16): per-sub-batch fixed latencies dominate -- fewer, larger
     // sub-batches B/8, B/4, B/4, B/4, B/8 (measured at c2: e2e 89.8 vs 86 GFLOP/s for
     // B/8, 3B/8, 3B/8, B/8, which beat the generic ramp)
-    if (pl->m <= (1 << 16) && B >= 8 && pl->chunk >= B / 4 + 1) {
+    // (used only when its largest sub-batch fits one workspace chunk: for B = 8k + 7 the
+    // middle ones are ceil(rest / 3) > B / 4 + 1)
+    if (pl->m <= (1 << 16) && B >= 8) {
       const int64_t e8 = B / 8, rest = B - 2 * e8;
-      sizes = {e8, rest / 3 + (rest % 3 > 0), rest / 3 + (rest % 3 > 1), rest / 3, e8};
+      const std::vector<int64_t> v = {e8, rest / 3 + (rest % 3 > 0), rest / 3 + (rest % 3 > 1),
+                                      rest / 3, e8};
+      if (*std::max_element(v.begin(), v.end()) <= pl->chunk) sizes = v;
     }
     if (const char* t = std::getenv("OZFFT_HOST_SUBS")) {  // tuning knob (tools/), "1,4,4,..."
       std::vector<int64_t> v;
@@ -501,8 +520,31 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
       if (tot == B && *std::max_element(v.begin(), v.end()) <= pl->chunk) sizes = v;
     }
   }
+  return sizes;
+}
+
+// Concurrent host pipeline (the whole batch fits one workspace chunk): sub-batches use
+// disjoint workspace and staging slots, so they need no slot-reuse waits and alternate
+// between two compute streams -- the small first / last sub-batches (short pipeline fill
+// and drain) overlap the large ones on the GPU instead of running it half-empty.
+// Host-buffer pipeline: the batch runs as sub-batches (small first and last ones shorten
+// the fill -- the first H2D -- and the drain -- the last D2H); sub-batch j uses staging and
+// workspace slot j mod nslots and alternates between two compute streams, so H2D, D2H and
+// the kernels of neighbouring sub-batches overlap, and the small edge sub-batches share the
+// GPU with large ones instead of running it half-empty.  Slot reuse waits for the previous
+// occupant's kernels (input consumed) and D2H (output and workspace free).
+ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* out, int direction,
+                                void* stream) {
+  ozfft_status s = check_exec(pl, in, out, direction);
+  if (s) return s;
+  ozfft_plan* mp = const_cast<ozfft_plan*>(pl);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = pl->n;
+  const std::vector<int64_t> sizes = host_subbatches(*pl);
   const int64_t nsub = (int64_t)sizes.size();
   const int64_t sb = *std::max_element(sizes.begin(), sizes.end());
+  if (sb > pl->chunk)  // every sub-batch runs in one workspace slot (never expected)
+    return fail(OZFFT_ERR_INVALID_ARGUMENT, "internal: host sub-batch larger than the workspace chunk");
   const int64_t nslots = std::max<int64_t>(1, std::min<int64_t>(nsub, pl->chunk / sb));
   if (!mp->pipe) mp->pipe = new HostPipe();
   HostPipe& hp = *mp->pipe;
@@ -561,6 +603,13 @@ ozfft_status ozfft_execute_host(const ozfft_plan* pl, const double* in, double* 
   cudaStreamWaitEvent(st, ev(3 * (nsub - 1) + 2), 0);
   mp->last_batch = pl->batch;
   return check_cuda(cudaStreamSynchronize(st), "execute_host sync");
+}
+
+int64_t ozfft_host_subbatches(const ozfft_plan* pl, int64_t* sizes, int64_t cap) {
+  if (!pl) return -1;
+  const std::vector<int64_t> v = host_subbatches(*pl);
+  for (int64_t i = 0; i < (int64_t)v.size() && i < cap && sizes; ++i) sizes[i] = v[i];
+  return (int64_t)v.size();
 }
 
 ozfft_status ozfft_execute_taps(const ozfft_plan* pl, const void* in, void* out, int direction,

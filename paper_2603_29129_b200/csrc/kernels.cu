@@ -41,6 +41,7 @@ namespace ozfft {
 namespace cg = cooperative_groups;
 
 // ============================================================== modular arithmetic
+
 __device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) {
   const uint32_t s = a + b;  // a, b < p < 2^31
   return min(s, s - p);
@@ -56,15 +57,57 @@ __device__ __forceinline__ uint32_t mul_shoup(uint32_t a, uint2 w, uint32_t p) {
   return min(r, r - p);
 }
 
-// T * 2^-32 mod p for T < 3 p^2 (a sum of at most three products of residues), p < 2^31:
-// fold the high word below p (T < 2p 2^32), then Montgomery REDC with pinv = -p^{-1} mod 2^32.
-__device__ __forceinline__ uint32_t redc_lazy3(unsigned long long T, uint32_t p, uint32_t pinv) {
+// T * 2^-32 mod p (canonical) for T < 3 p^2 (a sum of at most three products of residues),
+// p < 2^31: fold the high word below p (T < 2p 2^32), then the subtractive Montgomery REDC
+// with pinv_pos = +p^{-1} mod 2^32: mq p = tl (mod 2^32), so (T - mq p) / 2^32 = th - hi(mq p)
+// exactly, in (-p, p); one conditional add of p makes it canonical.
+__device__ __forceinline__ uint32_t redc_lazy3(unsigned long long T, uint32_t p, uint32_t pinv_pos) {
   uint32_t th = (uint32_t)(T >> 32);
   const uint32_t tl = (uint32_t)T;
   th = min(th, th - p);
-  const uint32_t mq = tl * pinv;
-  const uint32_t r = th + __umulhi(mq, p) + (tl != 0u ? 1u : 0u);  // (T + mq p) / 2^32 < 2p
-  return min(r, r - p);
+  const uint32_t mq = tl * pinv_pos;
+  const uint32_t d = th - __umulhi(mq, p);
+  return min(d, d + p);
+}
+
+// ============================================================== async copies (TMA bulk, mbarrier)
+// One-shot global -> shared bulk copies (cp.async.bulk, the TMA engine's 1-D form; SASS
+// UBLKCP) completing on an mbarrier (transaction bytes), and the waits on it.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+// make the initialised barriers visible to the async proxy (the bulk-copy engine)
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// order this thread's earlier generic-proxy shared-memory accesses before later async-proxy
+// writes to the same bytes (a buffer re-filled by a bulk copy after threads used it)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+// bytes: multiple of 16; src, dst 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // ============================================================== double-double (DD)
@@ -1174,6 +1217,12 @@ struct RowParams {
 #ifndef OZ_ROW_NA
 #define OZ_ROW_NA 1
 #endif
+#ifndef OZ_PW_BATCH
+#define OZ_PW_BATCH 1  // pointwise: all W loads of a group (<= 3 pairs) issued up front
+#endif
+#ifndef OZ_ROW_BULKY
+#define OZ_ROW_BULKY 1  // two-pass rows: Y rows bulk-copied (TMA) into shared memory up front
+#endif
 // streaming read-only load that does not allocate in L1 (keeps the twiddle tables there)
 __device__ __forceinline__ uint32_t ldg_stream(const uint32_t* p) {
 #if OZ_ROW_NA
@@ -1255,25 +1304,51 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   // group table for 2 convs x K*K groups: npairs, then (X row offset, W row offset) x L
   uint32_t* tab = work + padC;
   const int tstride = 1 + 2 * L;
-  for (int ci = tv; ci < 2 && !P.fwd_only; ci += blockDim.x) {  // blockDim may be 1 (C < 32)
-    const int cv = ci ? cv1 : cv0;
-    const bool want = ci ? want1 : want0;
-    const int32_t* srow = P.sched + (b * 4 + (P.image ? 0 : cv)) * sched_stride(K, L);
-    const int ng = want ? srow[0] : 0;
-    s_ng[ci] = ng;
-    for (int g = 0; g < ng; ++g) {
-      const int32_t* grp = srow + 1 + g * (2 + 2 * L);
-      uint32_t* tg = tab + (ci * G + g) * tstride;
-      tg[0] = (uint32_t)grp[1];
-      for (int i = 0; i < grp[1]; ++i) {
-        tg[1 + 2 * i] = (uint32_t)grp[2 + 2 * i] * C;
-        tg[2 + 2 * i] = (uint32_t)grp[3 + 2 * i] * (uint32_t)m;
-      }
-    }
-  }
   const uint2* Tf = P.tw + (size_t)(q * 2 + 0) * m;
   const uint2* Ti = P.tw + (size_t)(q * 2 + 1) * m;
   const uint32_t rowoff = row << logC;
+#if OZ_ROW_BULKY
+  // two-pass plans: the ka rows of Y this CTA transforms are bulk-copied into the X area at
+  // the start (one mbarrier per slice), so their HBM latency is paid once, overlapped with
+  // the earlier slices' NTTs, instead of once per slice behind the sub-transform barriers.
+  // Slice s's first round reads Y[s] from there; its last round overwrites it with X[s]
+  // (every read of Y[s] precedes the round-0 exchange barrier).
+  __shared__ __align__(8) unsigned long long s_ybar[kMaxK];
+  if constexpr (TWO_PASS) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < ka; ++s) mbar_init(&s_ybar[s], 1);
+      mbar_fence_init();
+      for (int s = 0; s < ka; ++s) {
+        mbar_expect_tx(&s_ybar[s], C * 4u);
+        bulk_g2s(Xs + s * C, P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff, C * 4u, &s_ybar[s]);
+      }
+    }
+  }
+#endif
+  // one (conv, group) entry per thread, every schedule load independent of the others (the
+  // whole table costs one L2 latency; a serial walk over the groups cost ~10 dependent ones)
+  for (int it = tv; it < 2 * G && !P.fwd_only; it += blockDim.x) {  // blockDim may be 1 (C < 32)
+    const int ci = it / G, g = it - (it / G) * G;
+    const int cv = ci ? cv1 : cv0;
+    const bool want = ci ? want1 : want0;
+    const int32_t* srow = P.sched + (b * 4 + (P.image ? 0 : cv)) * sched_stride(K, L);
+    const int32_t* grp = srow + 1 + g * (2 + 2 * L);
+    const int ng = want ? __ldg(&srow[0]) : 0;
+    const int np = __ldg(&grp[1]);
+    uint32_t* tg = tab + (ci * G + g) * tstride;
+    for (int i = 0; i < L; ++i) {
+      const uint32_t sx = (uint32_t)__ldg(&grp[2 + 2 * i]), tw = (uint32_t)__ldg(&grp[3 + 2 * i]);
+      if (g < ng && i < np) {
+        tg[1 + 2 * i] = sx * C;
+        tg[2 + 2 * i] = tw * (uint32_t)m;
+      }
+    }
+    if (g < ng) tg[0] = (uint32_t)np;
+    if (g == 0) s_ng[ci] = ng;
+  }
+#if OZ_ROW_BULKY
+  if constexpr (TWO_PASS) __syncthreads();  // barriers initialised
+#endif
   // ---- forward: last log2(C) DIF stages of each slice's NTT (Alg.6 l.787)
   for (int s = 0; s < ka; ++s) {
     uint32_t* xs = Xs + s * C;
@@ -1286,9 +1361,15 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
       if (outX) outX[e] = v;
     };
     if constexpr (TWO_PASS) {
+#if OZ_ROW_BULKY
+      mbar_wait(&s_ybar[s], 0u);  // Y[s] landed in xs
+      sub_ntt<LOGC, false, 1, LOGE, true>(tv, wk, 0u, 1u, Tf, p,
+                           [&](int, uint32_t e) -> uint32_t { return xs[e]; }, store_x);
+#else
       const uint32_t* y = P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff;
       sub_ntt<LOGC, false, 1, LOGE, true>(tv, wk, 0u, 1u, Tf, p,
                            [&](int, uint32_t e) -> uint32_t { return ldg_stream(&y[e]); }, store_x);
+#endif
     } else {
       const int32_t* D = P.digits + ((b * 2 + a) * K + s) * P.in_len;
       const uint32_t in_len = (uint32_t)P.in_len;
@@ -1315,7 +1396,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   // stages of its inverse NTT (l.973).  The (conv, group) items of both convolutions are
   // processed two at a time: their twiddles are shared and one barrier serves both.
   constexpr int CNT = RoundT<LOGC, true, 0, LOGE>::cnt;
-  const uint32_t pinv = q ? P.pinv[1] : P.pinv[0];
+  const uint32_t pinv = 0u - (q ? P.pinv[1] : P.pinv[0]);  // +p^{-1} mod 2^32 (redc_lazy3)
   __syncthreads();  // group table visible
   const int ng0 = s_ng[0], nitems = s_ng[0] + s_ng[1];
   auto item = [&](int it, int& ci, int& g) {
@@ -1329,6 +1410,42 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
     const uint32_t* Wb = P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff;
     const uint32_t* tg = tab + (ci * G + g) * tstride;
     const int np = (int)tg[0];
+#if OZ_PW_BATCH
+    if (np <= 3) {  // (L <= 3 always): the W loads of two pairs in flight ahead of the
+                    // products (one L2 latency per group instead of one per pair)
+      uint32_t w0[CNT], w1[CNT];
+      const uint32_t* wr0 = Wb + tg[2];
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) w0[i] = ldg_stream(&wr0[row_slot<LOGC, TWO_PASS>(tv, i)]);
+      if (np > 1) {
+        const uint32_t* wr1 = Wb + tg[4];
+#pragma unroll
+        for (int i = 0; i < CNT; ++i) w1[i] = ldg_stream(&wr1[row_slot<LOGC, TWO_PASS>(tv, i)]);
+      }
+      unsigned long long T[E];
+      const uint32_t* x0 = Xs + tg[1];
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) T[i] = (unsigned long long)x0[row_slot<LOGC, TWO_PASS>(tv, i)] * w0[i];
+      if (np > 2) {
+        const uint32_t* wr2 = Wb + tg[6];
+#pragma unroll
+        for (int i = 0; i < CNT; ++i) w0[i] = ldg_stream(&wr2[row_slot<LOGC, TWO_PASS>(tv, i)]);
+      }
+      if (np > 1) {
+        const uint32_t* x1 = Xs + tg[3];
+#pragma unroll
+        for (int i = 0; i < CNT; ++i) T[i] += (unsigned long long)x1[row_slot<LOGC, TWO_PASS>(tv, i)] * w1[i];
+      }
+      if (np > 2) {
+        const uint32_t* x2 = Xs + tg[5];
+#pragma unroll
+        for (int i = 0; i < CNT; ++i) T[i] += (unsigned long long)x2[row_slot<LOGC, TWO_PASS>(tv, i)] * w0[i];
+      }
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) z[i] = redc_lazy3(T[i], p, pinv);
+      return;
+    }
+#endif
 #pragma unroll
     for (int i = 0; i < E; ++i) z[i] = 0;
     for (int ip0 = 0; ip0 < np; ip0 += 3) {
@@ -2359,6 +2476,10 @@ ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
 
 ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (A.nb < 1 || A.ws0 < 0 || A.ws0 + A.nb > pl.chunk) {  // the chunked workspace regions
+    set_error("internal: sub-batch does not fit the workspace chunk");
+    return OZFFT_ERR_INVALID_ARGUMENT;
+  }
   const int K = pl.K, L = pl.L, G = K * K;
   const int64_t nb = A.nb, m = pl.m, n = pl.n;
   uint8_t* ws = pl.ws;

@@ -132,3 +132,66 @@ def test_entry_point_errors_without_device(lib):
     assert L.ozfft_status_string(9) == b"OZFFT_ERR_BUFFER_TOO_SMALL"
     assert L.ozfft_plan_destroy(h) == 0
     assert L.ozfft_plan_destroy(None) == 0
+
+
+def _raw_plan(L, **kw):
+    import paper_2603_29129_b200 as oz
+    d = oz.PlanDesc(**{"n": 1024, "batch": 1, "K": 3, "L": 3, "p0": 0, "p1": 0, "device": 0,
+                       "conv_mode": 0, "accum_mode": 0, "precision": 0,
+                       "max_workspace_bytes": 0, **kw})
+    h = ctypes.c_void_p()
+    st = L.ozfft_plan_create(ctypes.byref(d), ctypes.byref(h))
+    return st, h
+
+
+def test_host_subbatches_fit_the_chunk(lib):
+    """ozfft_execute_host's sub-batches: every one fits a workspace chunk and they cover the
+    batch.  Regression: the m <= 2^16 schedule B/8, B/4, ... gave a middle
+    sub-batch of ceil(rest/3) > chunk for B = 8k + 7 with chunk = 2k + 2 (e.g. B = 15,
+    chunk 4 -> 5), overrunning the workspace slot."""
+    import paper_2603_29129_b200 as oz
+    L = oz.load_library()
+    info = oz.PlanInfo()
+
+    def ok(n, B, cap):
+        st, h = _raw_plan(L, n=n, batch=B, max_workspace_bytes=cap)
+        if st == 0:
+            L.ozfft_plan_destroy(h)
+        return st == 0
+
+    for n, Bs in ((1000, list(range(1, 70)) + [127, 199, 1024]), (3000, [7, 15, 23, 31, 64]),
+                  (20000, [7, 15, 23])):
+        st, h = _raw_plan(L, n=n, batch=1)
+        assert st == 0
+        assert L.ozfft_plan_get_info(h, ctypes.byref(info)) == 0
+        L.ozfft_plan_destroy(h)
+        per = info.workspace_bytes  # >= one transform's chunked regions
+        for B in Bs:
+            lo, hi = 0, per + 64 * B * 1300 + (1 << 20)  # smallest cap that takes one transform
+            assert ok(n, B, hi)
+            while hi - lo > per // 16:
+                mid = (lo + hi) // 2
+                lo, hi = (lo, mid) if ok(n, B, mid) else (mid, hi)
+            for chunk_target in sorted({1, 2, 3, 4, 6, max(1, B // 4 + 1), B}):
+                cap = hi + per * (chunk_target - 1) + per // 2  # about chunk_target transforms
+                st, h = _raw_plan(L, n=n, batch=B, max_workspace_bytes=cap)
+                assert st == 0, (n, B, chunk_target)
+                assert L.ozfft_plan_get_info(h, ctypes.byref(info)) == 0
+                assert info.workspace_bytes <= cap, (n, B, info.workspace_bytes, cap)
+                cnt = L.ozfft_host_subbatches(h, None, 0)
+                sizes = (ctypes.c_int64 * cnt)()
+                assert L.ozfft_host_subbatches(h, sizes, cnt) == cnt
+                sz = list(sizes)
+                L.ozfft_plan_destroy(h)
+                assert sum(sz) == B and min(sz) >= 1, (n, B, sz)
+                assert max(sz) <= info.chunk, (n, B, info.chunk, sz)
+
+
+def test_workspace_cap_too_small(lib):
+    """A max_workspace_bytes below one transform's workspace is refused (BUFFER_TOO_SMALL)
+    instead of silently exceeding the cap."""
+    import paper_2603_29129_b200 as oz
+    L = oz.load_library()
+    st, h = _raw_plan(L, n=1 << 14, batch=4, max_workspace_bytes=4096)
+    assert st == 9
+    assert L.ozfft_host_subbatches(None, None, 0) == -1
