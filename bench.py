@@ -8,10 +8,13 @@ n = 2^18 (config c3: batch 16 complex fp64 DFTs, m = 2^19).  A "step" is one pas
 of the whole hot path (premultiply + split, 12 forward NTTs, NTT-domain
 accumulation, 40 inverse NTTs, CRT, recombination, post-chirp) over the batch.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling -- every rank transforms
-its own batch of B independent transforms (global batch N*B); there is no
-data-path collective; the timed region is bracketed by barriers and the reported
-time is the max over ranks (all_reduce MAX of each rank's CUDA-event time).
+Multi-GPU (one process per GPU: torchrun, or `--gpus N` alone, which starts the N ranks
+itself): the configured batch is sharded -- rank r transforms rows batch_slice(B, r, N) of
+the same seeded input (SURVEY 8(e), strong scaling of the configured job); there is no
+data-path collective; the timed region is bracketed by barriers, the reported time is the
+max over ranks (all_reduce MAX of each rank's CUDA-event time) and value = B / that time.
+After timing the rows are all-gathered and compared bit for bit with one GPU transforming
+the whole batch ("bitwise_vs_n1").
 
 --impl reference times the CPU oracle (oracle/, plain C, OpenMP over transforms)
 on this box's host cores: the reference arm of this tier.
@@ -191,12 +194,12 @@ def run_reference(args, cfg, rank, world):
 # ---------------------------------------------------------------------------- GPU arm
 def run_single(args, cfg, rank, world, local_rank):
     """--mode single: ONE transform (row 0 of the config) sharded over the ranks by
-    (prime, real convolution) units, one NCCL all_gather_into_tensor of the inverse-NTT
-    residues, then CRT + recombination on every rank.
-    Strong scaling; device time per step = max over ranks (CUDA events on the stream)."""
+    (prime, real convolution) units, one in-place NCCL all_gather_into_tensor of the
+    inverse-NTT residues (8 g n words, g = the schedule's group count), then CRT +
+    recombination on every rank.  Strong scaling; device
+    time per step = max over ranks (CUDA events on the stream)."""
     import torch
     import paper_2603_29129_b200 as oz
-    from paper_2603_29129_b200 import dist as ozd
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
@@ -207,24 +210,25 @@ def run_single(args, cfg, rank, world, local_rank):
     plan = oz.Plan(n, 1, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    nwords = plan.shard_residue_bytes() // 4
-    residues = torch.empty(nwords, dtype=torch.int32, device=dev)
+    residues = torch.empty(plan.shard_residue_bytes() // 4, dtype=torch.int32, device=dev)
     out = torch.empty(n, dtype=torch.complex128, device=dev)
     ag = []  # (start, end) events around the all-gather of each timed step
+    gsz = [0]
 
     def step(record=False):
-        plan.shard_partial(x, rank, world, residues)
+        g = plan.shard_partial(x, rank, world, residues)
+        gsz[0] = g
         if world > 1:
-            per = nwords // world
-            mine = residues[rank * per:(rank + 1) * per].clone()
+            buf = residues[:8 * g * n]
+            per = buf.numel() // world
             if record:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            dist.all_gather_into_tensor(residues, mine)
+            dist.all_gather_into_tensor(buf, buf[rank * per:(rank + 1) * per])  # in place
             if record:
                 e1.record(stream)
                 ag.append((e0, e1))
-        return plan.shard_finish(residues, out)
+        return plan.shard_finish(residues, g, out)
 
     for _ in range(max(args.warmup, 3)):
         y = step()
@@ -249,12 +253,16 @@ def run_single(args, cfg, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms, ag_ms = float(t[0].item()), float(t[1].item())
     if rank == 0:
-        nbytes = plan.shard_residue_bytes()
+        nbytes = plan.shard_residue_bytes(gsz[0])
         ag_per = ag_ms / args.steps
-        allgather = {"ms_per_step": ag_per, "bytes": nbytes,
-                     "busbw_GBs": (nbytes * (world - 1) / world) / (ag_per * 1e-3) / 1e9 if ag_per > 0 else None,
-                     "note": "NCCL all_gather_into_tensor of the inverse-NTT residues, CUDA events "
-                             "on the stream, max over ranks; busBW = bytes (N-1)/N / time"}
+        busbw = (nbytes * (world - 1) / world) / (ag_per * 1e-3) / 1e9 if ag_per > 0 else None
+        allgather = {"ms_per_step": ag_per, "bytes": nbytes, "groups": gsz[0],
+                     "busbw_GBs": busbw,
+                     "frac_of_peer_copy_770GBs": busbw / 770.0 if busbw else None,
+                     "note": "in-place NCCL all_gather_into_tensor of the inverse-NTT residues "
+                             "[8 units][g][n], CUDA events on the stream, max over ranks; busBW = "
+                             "bytes (N-1)/N / time; reference: 770 GB/s measured peer copy "
+                             "(B200_PROFILING.md)"}
         line = {"metric": METRIC, "value": args.steps * flops_per_transform(n) / (t_ms * 1e-3) / 1e9,
                 "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
                 "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
@@ -263,10 +271,62 @@ def run_single(args, cfg, rank, world, local_rank):
                                        f"units (prime, conv) split over {world} rank(s), one NCCL "
                                        "all-gather of the residues before CRT",
                            "n": n, "m": plan.m, "parallelism": f"unit-sharded x{world}",
-                           "residue_bytes_gathered": plan.shard_residue_bytes()},
+                           "residue_bytes_gathered": nbytes if world > 1 else 0},
                 "gpu_launches": int(oz.kernel_launches() - launches0),
                 "allgather": allgather if world > 1 else None}
         print(json.dumps(line), flush=True)
+
+
+class Coll:
+    """The collectives of the batch-sharded bench, in one fixed order on every rank (an idle
+    rank -- more ranks than transforms -- issues the same calls with empty data)."""
+
+    def __init__(self, world, dev):
+        import torch
+        self.world, self.dev, self.torch = world, dev, torch
+        self.dist = None
+        if world > 1:
+            import torch.distributed as dist
+            self.dist = dist
+            if dist.get_backend() == "gloo":  # (test knob --backend gloo: host tensors)
+                self.dev = torch.device("cpu")
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, v):
+        if not self.dist:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather_rows(self, y, total, n):
+        """All ranks' output rows (complex128 [count_r, n]) -> [total, n] on every rank, in
+        batch order (rank r's rows are batch_slice(total, r, world))."""
+        torch = self.torch
+        if not self.dist:
+            return y
+        from paper_2603_29129_b200.dist import batch_slice
+        cmax = -(-total // self.world)
+        pad = torch.zeros(cmax, n, dtype=torch.complex128, device=self.dev)
+        if y is not None and y.shape[0]:
+            pad[:y.shape[0]] = y.to(self.dev)
+        allr = torch.empty(self.world * cmax, n, dtype=torch.complex128, device=self.dev)
+        self.dist.all_gather_into_tensor(torch.view_as_real(allr), torch.view_as_real(pad))
+        rows = [allr[r * cmax: r * cmax + batch_slice(total, r, self.world)[1]] for r in range(self.world)]
+        return torch.cat(rows).to(y.device if y is not None else self.dev)
+
+
+def rank_input(cfg, rank, world):
+    """Rank r's contiguous slice of the config's ONE seeded batch (the batch of
+    independent transforms is sharded, B / N per rank; every rank draws the same bytes and
+    keeps its rows, so the N-GPU job transforms exactly the N = 1 input)."""
+    from paper_2603_29129_b200.dist import batch_slice
+    start, cnt = batch_slice(cfg.batch, rank, world)
+    x = workloads.config_input(cfg)
+    return start, cnt, np.ascontiguousarray(x[start:start + cnt])
 
 
 def run_ours(args, cfg, rank, world, local_rank):
@@ -277,13 +337,20 @@ def run_ours(args, cfg, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-    B, n = cfg.batch, cfg.n
-    # weak scaling: rank r owns transforms [r*B, (r+1)*B) of a global batch of world*B
-    # weak scaling: rank r draws its own batch of B with seed = 1000 seed + r (same recipe;
-    # drawing a slice of the world * B global batch would cost every rank world times the RNG
-    # work and host memory -- 8.6 GB per rank for c5 at N = 8)
-    x_np = workloads.draw(cfg.dist, 1000 * cfg.seed + rank, B, n) if world > 1 \
-        else workloads.config_input(cfg)
+    Bg, n = cfg.batch, cfg.n
+    # strong scaling over the configured batch: rank r transforms rows [start, start + B)
+    start, B, x_np = rank_input(cfg, rank, world)
+    coll = Coll(world, dev)
+    if B == 0:  # more ranks than transforms (c1 at N > 1): join the collectives only
+        coll.barrier()
+        coll.max(0.0)
+        coll.barrier()
+        coll.barrier()
+        coll.max(0.0)
+        coll.gather_rows(None, Bg, n)
+        if cfg.roundtrip:
+            coll.gather_rows(None, Bg, n)
+        return
     x = torch.from_numpy(x_np).to(dev)
     plan = oz.Plan(n, B, device=dev, conv=args.conv, accum=args.accum, precision=args.precision)
     out = torch.empty_like(x)
@@ -299,8 +366,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
+    coll.barrier()
     # timed region: the production path (no stage timers; plans with batch*m <= 2^25 replay a
     # CUDA graph, captured during the warm-up)
     launches0 = oz.kernel_launches()
@@ -328,15 +394,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     prof = plan.profile_read()
     plan.profile(False)
-    t_ms = sum(a.elapsed_time(b) for a, b in ev)
-    if dist:
-        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
-        dist.barrier()
+    t_ms = coll.max(sum(a.elapsed_time(b) for a, b in ev))  # max over ranks
+    coll.barrier()
     stats = plan.stats()
     dirs = 2 if cfg.roundtrip else 1
-    total_transforms = world * B * dirs * args.steps
+    total_transforms = Bg * dirs * args.steps
     value = total_transforms * flops_per_transform(n) / (t_ms * 1e-3) / 1e9
 
     # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the region
@@ -352,20 +414,30 @@ def run_ours(args, cfg, rank, world, local_rank):
     for _ in range(2):
         e2e_step()
     e2e_steps = max(3, min(args.steps, 10))
-    if dist:
-        dist.barrier()
+    coll.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_step()
     torch.cuda.synchronize(dev)
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_val = world * B * dirs * e2e_steps * flops_per_transform(n) / e2e_s / 1e9
-    io_bytes = B * n * 16 * dirs
+    e2e_s = coll.max(time.perf_counter() - t0)
+    e2e_val = Bg * dirs * e2e_steps * flops_per_transform(n) / e2e_s / 1e9
+    io_bytes = Bg * n * 16 * dirs
+
+    # ---- the N-rank outputs against one GPU transforming the whole batch (rank 0)
+    step()
+    torch.cuda.synchronize(dev)
+    y_all = coll.gather_rows(out, Bg, n)
+    b_all = coll.gather_rows(back, Bg, n) if cfg.roundtrip else None
+    bitwise = None
+    if world > 1 and rank == 0:
+        xf = torch.from_numpy(workloads.config_input(cfg)).to(dev)
+        pf = oz.Plan(n, Bg, device=dev, conv=args.conv, accum=args.accum, precision=args.precision)
+        yf = pf.forward(xf)
+        bitwise = bool(torch.equal(yf, y_all.to(dev)))
+        if cfg.roundtrip:
+            bitwise = bitwise and bool(torch.equal(pf.inverse(yf), b_all.to(dev)))
+        del pf, xf, yf
 
     if rank != 0:
         return
@@ -454,8 +526,6 @@ def run_ours(args, cfg, rank, world, local_rank):
         cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
         torch.cuda.synchronize(dev)
-        if dist:
-            dist.barrier()
         for i in range(args.steps):
             flush.zero_()
             cev[i][0].record(stream)
@@ -463,10 +533,6 @@ def run_ours(args, cfg, rank, world, local_rank):
             cev[i][1].record(stream)
         torch.cuda.synchronize(dev)
         c_ms = sum(a.elapsed_time(b) for a, b in cev)
-        if dist:
-            t = torch.tensor([c_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            c_ms = float(t.item())
         st = pc.stats()
         r = {"value": total_transforms * flops_per_transform(n) / (c_ms * 1e-3) / 1e9,
              "unit": UNIT, "ms_per_step": c_ms / args.steps, "m": pc.m, "alpha": pc.alpha,
@@ -478,7 +544,8 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     pow2 = n > 1 and n & (n - 1) == 0
     cyc = img = imgc = tsl = None
-    if args.conv == "padded" and args.accum == "real" and args.precision == "dd" and not args.no_extra:
+    if (args.conv == "padded" and args.accum == "real" and args.precision == "dd"
+            and not args.no_extra and world == 1):  # side lines at N = 1 only
         if pow2:
             cyc = side("cyclic", "real")
             cyc["note"] = "paper's N = n cyclic Bluestein (P:238-241); bitwise equal to the headline"
@@ -493,18 +560,20 @@ def run_ours(args, cfg, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "step_ms": step_ms,
         "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": workload_desc(cfg), "n": n, "m": m, "batch_per_gpu": B,
-                   "global_batch": world * B, "K": plan.K, "L": plan.L, "alpha": plan.alpha,
+                   "global_batch": Bg, "K": plan.K, "L": plan.L, "alpha": plan.alpha,
                    "ntt_split": f"m = 2^{logR} x 2^{logC}", "parallelism": f"batch-sharded x{world}",
                    "directions": "fwd+inv" if cfg.roundtrip else "fwd",
                    "l2": "flushed between timed steps (512 MiB write outside the events)",
-                   "inputs": "config recipe; N > 1: rank r uses seed 1000 seed + r",
+                   "inputs": "config recipe; rank r transforms rows batch_slice(B, r, N) of it",
                    "io_dtype": "complex128", "conv": args.conv, "accum": args.accum,
                    "precision": args.precision},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": io_bytes,
                 "d2h_bytes_per_step": io_bytes, "steps": e2e_steps},
         "gpu_launches": int(launches),
+        "bitwise_vs_n1": bitwise,
+        "test_knobs": ({"backend": args.backend, "one_device": True} if args.one_device else None),
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clocks,
@@ -521,9 +590,20 @@ def run_ours(args, cfg, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def _spawned_rank(local_rank, argv, world, port):
+    """Rank entry of `bench.py --gpus N` started without torchrun (one process per GPU)."""
+    os.environ.update({"RANK": str(local_rank), "LOCAL_RANK": str(local_rank),
+                       "WORLD_SIZE": str(world), "MASTER_ADDR": "127.0.0.1",
+                       "MASTER_PORT": str(port)})
+    sys.argv = argv
+    main()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="ranks (one per GPU); under torchrun it must equal WORLD_SIZE, "
+                         "without torchrun bench.py starts the N ranks itself")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c3", choices=sorted(workloads.CONFIGS))
@@ -532,19 +612,38 @@ def main():
     ap.add_argument("--conv", default="padded", choices=["padded", "cyclic"],
                     help="Bluestein length: m >= 2n-1 (north star) or m = n (P:238-241)")
     ap.add_argument("--mode", default="batch", choices=["batch", "single"],
-                    help="batch: weak-scaled batches (the headline); single: one transform "
-                         "sharded over the ranks with an NCCL all-gather (SURVEY 8(e))")
+                    help="batch: the configured batch sharded over the ranks (the headline); "
+                         "single: one transform sharded over the ranks by (prime, conv) units "
+                         "with an NCCL all-gather (SURVEY 8(e))")
     ap.add_argument("--precision", default="dd", choices=["dd", "ts"],
                     help="double-double O(n) steps (default) or the paper's triple-single (f4)")
     ap.add_argument("--accum", default="real", choices=["real", "image"],
                     help="four real convolutions (the paper) or complex images (SURVEY f2)")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the f1_cyclic / f2_image side measurements")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo + --one-device: a test of the N-rank "
+                         "batch path on a one-GPU box; its kernels never wait on each other)")
+    ap.add_argument("--one-device", action="store_true",
+                    help="every rank on cuda:0 (test knob; timings are not N-GPU numbers)")
     args = ap.parse_args()
     cfg = workloads.CONFIGS[args.config]
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus and args.gpus > 1:
+        import socket
+        import torch.multiprocessing as mp
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        mp.start_processes(_spawned_rank, args=(list(sys.argv), args.gpus, port),
+                           nprocs=args.gpus, join=True, start_method="spawn")
+        return
+    world = int(env_world or "1")
+    if args.gpus is not None and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    local_rank = 0 if args.one_device else int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
@@ -552,7 +651,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         if args.mode == "single":
             run_single(args, cfg, rank, world, local_rank)

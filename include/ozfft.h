@@ -219,18 +219,24 @@ ozfft_status ozfft_last_stats(const ozfft_plan* plan, ozfft_exec_stats* stats, v
  * Unit u in [0, 8) = (prime q = u % 2, real conv cv = u / 2) (conv order as in taps).
  * Rank `shard` computes the contiguous units [shard*8/nshards, (shard+1)*8/nshards)
  * (with 8 ranks: rank r = (prime r % 2, conv r / 2)) of transform 0: it redoes the O(n)
- * premultiply/split of `in` (identical digits on every rank), runs its forward NTTs,
- * NTT-domain accumulation and inverse NTTs, and writes residues into its contiguous
- * slice of `residues_out`, a device uint32 buffer of ozfft_shard_residue_bytes()
- * bytes laid out [8 units][K*K groups][n] (slice = units of this shard).  Shards are
- * then all-gathered by the caller (torch.distributed / NCCL) into every rank's full
- * buffer and ozfft_shard_finish() performs CRT, recombination and post-chirp.
- * nshards must divide 8.  Errors: SHARD, NOT_BOUND, CUDA. */
-uint64_t ozfft_shard_residue_bytes(const ozfft_plan* plan);
+ * premultiply/split of `in` (identical digits, exponents and Alg.8 schedules on every
+ * rank), then -- with nshards > 1 -- reads the four group counts ng_cv (one 16-byte D2H
+ * copy; synchronizes `stream`) and returns g = max_cv ng_cv in *groups (nshards == 1:
+ * g = K*K, no synchronization).  It runs its forward NTTs, NTT-domain accumulation and
+ * inverse NTTs and writes the residues of its units straight into their place of
+ * `residues`, a device uint32 buffer laid out [8 units][g groups][n]: bytes
+ * [shard * 8/nshards * g * n * 4, (shard + 1) * 8/nshards * g * n * 4).  An in-place
+ * all-gather of those equal slices (torch.distributed / NCCL all_gather_into_tensor)
+ * completes the buffer on every rank -- 8 g n 4 bytes, 160 n at (K, L) = (3, 3) -- and
+ * ozfft_shard_finish(g) performs Garner's CRT, the recombination and the post-chirp.
+ * `residues` must hold ozfft_shard_residue_bytes(plan, 0) bytes (the K*K-group capacity);
+ * ozfft_shard_residue_bytes(plan, g) is the exchanged size.  nshards must divide 8.
+ * Errors: SHARD, NOT_BOUND, INVALID_ARGUMENT, CUDA. */
+uint64_t ozfft_shard_residue_bytes(const ozfft_plan* plan, int32_t groups);
 ozfft_status ozfft_shard_partial(const ozfft_plan* plan, int shard, int nshards, const void* in,
-                                 int direction, void* residues_out, void* stream);
-ozfft_status ozfft_shard_finish(const ozfft_plan* plan, const void* residues_all, void* out,
-                                int direction, void* stream);
+                                 int direction, void* residues, int32_t* groups, void* stream);
+ozfft_status ozfft_shard_finish(const ozfft_plan* plan, const void* residues_all, int32_t groups,
+                                void* out, int direction, void* stream);
 
 /* ---- profiling (tracing) -----------------------------------------------------------
  * Per-stage CUDA-event timers.  While enabled, every execute records an event pair

@@ -94,10 +94,10 @@ def load_library() -> C.CDLL:
     L.ozfft_execute_host.argtypes = [vp, vp, vp, i32, vp]
     L.ozfft_execute_taps.argtypes = [vp, vp, vp, i32, vp, C.POINTER(Taps)]
     L.ozfft_last_stats.argtypes = [vp, C.POINTER(ExecStats), vp]
-    L.ozfft_shard_residue_bytes.argtypes = [vp]
+    L.ozfft_shard_residue_bytes.argtypes = [vp, C.c_int32]
     L.ozfft_shard_residue_bytes.restype = u64
-    L.ozfft_shard_partial.argtypes = [vp, i32, i32, vp, i32, vp, vp]
-    L.ozfft_shard_finish.argtypes = [vp, vp, vp, i32, vp]
+    L.ozfft_shard_partial.argtypes = [vp, i32, i32, vp, i32, vp, C.POINTER(C.c_int32), vp]
+    L.ozfft_shard_finish.argtypes = [vp, vp, C.c_int32, vp, i32, vp]
     L.ozfft_plan_destroy.argtypes = [vp]
     L.ozfft_profile_enable.argtypes = [vp, i32]
     L.ozfft_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), vp]
@@ -293,18 +293,25 @@ class Plan:
         return {s: (ms[i], ln[i]) for i, s in enumerate(STAGES)}
 
     # ------------------------------------------------------------------ sharding
-    def shard_residue_bytes(self) -> int:
-        return int(self._lib.ozfft_shard_residue_bytes(self._h))
+    def shard_residue_bytes(self, groups: int = 0) -> int:
+        """Bytes of the [8 units][groups][n] residue exchange buffer (groups <= 0: the K*K
+        capacity, the size to allocate)."""
+        return int(self._lib.ozfft_shard_residue_bytes(self._h, groups))
 
     def shard_partial(self, x: torch.Tensor, shard: int, nshards: int, residues: torch.Tensor,
-                      direction: int = -1, stream=None):
+                      direction: int = -1, stream=None) -> int:
+        """This shard's units of transform 0 into their place of `residues`; returns the
+        group count g of the buffer layout (see include/ozfft.h)."""
+        g = C.c_int32(0)
         with torch.cuda.device(self.device):
             _check(self._lib.ozfft_shard_partial(self._h, shard, nshards, x.data_ptr(), direction,
-                                                 residues.data_ptr(), _stream_ptr(stream, self.device)))
+                                                 residues.data_ptr(), C.byref(g),
+                                                 _stream_ptr(stream, self.device)))
+        return int(g.value)
 
-    def shard_finish(self, residues: torch.Tensor, out: torch.Tensor, direction: int = -1,
+    def shard_finish(self, residues: torch.Tensor, groups: int, out: torch.Tensor, direction: int = -1,
                      stream=None):
         with torch.cuda.device(self.device):
-            _check(self._lib.ozfft_shard_finish(self._h, residues.data_ptr(), out.data_ptr(),
+            _check(self._lib.ozfft_shard_finish(self._h, residues.data_ptr(), groups, out.data_ptr(),
                                                 direction, _stream_ptr(stream, self.device)))
         return out

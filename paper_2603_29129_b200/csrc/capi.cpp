@@ -671,21 +671,24 @@ ozfft_status ozfft_last_stats(const ozfft_plan* pl, ozfft_exec_stats* out, void*
   return OZFFT_OK;
 }
 
-uint64_t ozfft_shard_residue_bytes(const ozfft_plan* pl) {
+uint64_t ozfft_shard_residue_bytes(const ozfft_plan* pl, int32_t groups) {
   if (!pl) return 0;
-  return (uint64_t)8 * pl->K * pl->K * pl->n * 4;
+  const int64_t g = groups > 0 ? groups : (int64_t)pl->K * pl->K;
+  return (uint64_t)8 * g * pl->n * 4;
 }
 
 ozfft_status ozfft_shard_partial(const ozfft_plan* pl, int shard, int nshards, const void* in,
-                                 int direction, void* residues_out, void* stream) {
-  ozfft_status s = check_exec(pl, in, residues_out, direction);
+                                 int direction, void* residues, int32_t* groups, void* stream) {
+  ozfft_status s = check_exec(pl, in, residues, direction);
   if (s) return s;
+  if (!groups) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null groups pointer");
   if (nshards < 1 || 8 % nshards != 0 || shard < 0 || shard >= nshards)
     return fail(OZFFT_ERR_SHARD, "nshards must divide 8 and 0 <= shard < nshards");
   if (pl->image) return fail(OZFFT_ERR_SHARD, "sharding is not available for OZFFT_ACCUM_IMAGE");
   const int per = 8 / nshards;
   uint32_t mask = 0;
   for (int u = shard * per; u < (shard + 1) * per; ++u) mask |= 1u << u;
+  cudaStream_t st = (cudaStream_t)stream;
   ExecArgs a{};
   a.nb = 1;
   a.in = reinterpret_cast<const double*>(in);
@@ -694,22 +697,43 @@ ozfft_status ozfft_shard_partial(const ozfft_plan* pl, int shard, int nshards, c
   a.direction = direction;
   a.unit_mask = mask;
   a.finish = false;
+  int32_t g = pl->K * pl->K;
+  if (nshards > 1) {
+    // the exchange is sized by the schedule every rank computes identically: split, then
+    // read the four group counts (one small D2H + sync) -- 8 * max_cv ng * n words instead
+    // of the K*K capacity (160n vs 288n bytes at (K, L) = (3, 3))
+    a.phase = 1;
+    s = launch_execute(*pl, a, stream);
+    if (s) return s;
+    const int stride = sched_stride(pl->K, pl->L);
+    int32_t ng[4] = {0, 0, 0, 0};
+    for (int cv = 0; cv < 4 && !s; ++cv)
+      s = check_cuda(cudaMemcpyAsync(&ng[cv], pl->ws + pl->woff.sched + (size_t)cv * stride * 4, 4,
+                                     cudaMemcpyDeviceToHost, st), "schedule D2H");
+    if (!s) s = check_cuda(cudaStreamSynchronize(st), "schedule sync");
+    if (s) return s;
+    g = std::max(std::max(ng[0], ng[1]), std::max(ng[2], ng[3]));
+    if (g < 1) g = 1;  // no groups (zero or non-finite input): nothing is written
+    a.phase = 2;
+  }
+  *groups = g;
+  // this shard's units write straight into their place of the [8 units][g][n] exchange
+  // buffer (an in-place all-gather then completes it on every rank)
+  a.res_out = reinterpret_cast<uint32_t*>(residues);
+  a.res_groups = g;
   s = launch_execute(*pl, a, stream);
-  if (s) return s;
-  // res layout [b=0][cv][q][G][n] == [unit = cv*2+q][G][n]; copy this shard's units
-  const size_t unit_bytes = (size_t)pl->K * pl->K * pl->n * 4;
-  return check_cuda(cudaMemcpyAsync((uint8_t*)residues_out + (size_t)shard * per * unit_bytes,
-                                    pl->ws + pl->woff.res + (size_t)shard * per * unit_bytes,
-                                    per * unit_bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
-                    "shard copy");
+  const_cast<ozfft_plan*>(pl)->last_batch = 1;
+  return s;
 }
 
-ozfft_status ozfft_shard_finish(const ozfft_plan* pl, const void* residues_all, void* out,
-                                int direction, void* stream) {
+ozfft_status ozfft_shard_finish(const ozfft_plan* pl, const void* residues_all, int32_t groups,
+                                void* out, int direction, void* stream) {
   ozfft_status s = check_exec(pl, residues_all, out, direction);
   if (s) return s;
   if (pl->image) return fail(OZFFT_ERR_SHARD, "sharding is not available for OZFFT_ACCUM_IMAGE");
-  return launch_finish_from_residues(*pl, reinterpret_cast<const uint32_t*>(residues_all),
+  if (groups < 1 || groups > pl->K * pl->K)
+    return fail(OZFFT_ERR_INVALID_ARGUMENT, "groups must be the value ozfft_shard_partial returned");
+  return launch_finish_from_residues(*pl, reinterpret_cast<const uint32_t*>(residues_all), groups,
                                      reinterpret_cast<double*>(out), direction, stream);
 }
 

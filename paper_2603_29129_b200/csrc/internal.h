@@ -138,10 +138,13 @@ struct ExecArgs {
   const ozfft_taps* taps;
   int64_t ws0 = 0;     // first transform slot of the chunked workspace regions used
                        // (ws0 + nb <= chunk); disjoint slots may run on concurrent streams
+  uint32_t* res_out = nullptr;  // unit-sharded transform: residues written here, [unit][res_groups][n]
+  int res_groups = 0;
+  int phase = 0;       // 0: whole path; 1: split only (stats, schedules); 2: everything after the split
 };
 ozfft_status launch_plan_precompute(Plan& pl, void* stream);
 ozfft_status launch_execute(const Plan& pl, const ExecArgs& a, void* stream);
-ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, double* out,
+ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, int groups, double* out,
                                          int direction, void* stream);
 
 }  // namespace ozfft

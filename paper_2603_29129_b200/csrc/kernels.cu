@@ -41,6 +41,9 @@ namespace ozfft {
 namespace cg = cooperative_groups;
 
 // ============================================================== modular arithmetic
+// (ptxas issues part of the plain adds as IMAD.IADD on the FMA pipe, balancing it against
+// the ALU pipe; forcing every add onto the ALU (__viaddmin_u32 forms) measured slower:
+// c3 row kernel 1110 vs 1078 us -- the ALU pipe is the busier one)
 
 __device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) {
   const uint32_t s = a + b;  // a, b < p < 2^31
@@ -990,7 +993,8 @@ struct ColParams {
   uint32_t* Y;            // [nb][2 q][2 a][K][m]
   // inverse
   const uint32_t* G;      // [nb][2 q][4 cv][K*K][m]
-  uint32_t* res;          // [nb][4 cv][2 q][K*K][n]
+  uint32_t* res;          // [nb][4 cv][2 q][rg][n]
+  int rg;                 // group stride of res (K*K; the schedule's max group count when sharded)
   int64_t n;
   const int32_t* stats;   // [nb][stats_stride]
   const int32_t* sched;   // [nb][4][sched_stride]
@@ -1036,6 +1040,9 @@ __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32
 #endif
 #ifndef OZ_CI_SNAKE_MAX
 #define OZ_CI_SNAKE_MAX 7
+#endif
+#ifndef OZ_CI_ILP
+#define OZ_CI_ILP 4  // k_col_inv_crt: CRT + DD chains interleaved per batch
 #endif
 #ifndef OZ_CF_MINB
 #define OZ_CF_MINB 5
@@ -1176,7 +1183,7 @@ __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
     for (int i = 0; i < E; ++i) cur[i] = nxt[i];
     if (g + 1 < ng) fetch(g + 1);
     if (g > 0) __syncthreads();  // smem tile free
-    uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
+    uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * P.rg + g) * P.n + col;
     sub_ntt<LOGR, true, Cb, LOGE>(
         tv, smem + c, col, C, T, p, [&](int i, uint32_t) -> uint32_t { return cur[i]; },
         [&](int, uint32_t e, uint32_t val) {
@@ -1198,7 +1205,8 @@ struct RowParams {
   const uint32_t* W;      // [2 q][2 b][K][m] Montgomery form W m^{-1} 2^32 mod p (row_perm)
   uint32_t pinv[2];       // -p^{-1} mod 2^32 (Montgomery)
   uint32_t* G;            // R > 1: [nb][2 q][4][K*K][m]
-  uint32_t* res;          // R == 1: [nb][4][2][K*K][n]
+  uint32_t* res;          // R == 1: [nb][4][2][rg][n]
+  int rg;                 // group stride of res
   int64_t n;
   const int32_t* stats;
   const int32_t* sched;
@@ -1219,6 +1227,9 @@ struct RowParams {
 #endif
 #ifndef OZ_PW_BATCH
 #define OZ_PW_BATCH 1  // pointwise: all W loads of a group (<= 3 pairs) issued up front
+#endif
+#ifndef OZ_ROW_WSMEM
+#define OZ_ROW_WSMEM 0  // two-pass rows: the conv's W rows staged in shared memory
 #endif
 #ifndef OZ_ROW_BULKY
 #define OZ_ROW_BULKY 1  // two-pass rows: Y rows bulk-copied (TMA) into shared memory up front
@@ -1325,6 +1336,29 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
     }
   }
 #endif
+  // OZ_ROW_WSMEM (two-pass plans): the K cached W rows of the conv being processed live in
+  // shared memory (bulk-copied: conv 0's at the start, conv 1's while conv 0's last inverse
+  // NTT runs), so the pointwise products read W with LDS instead of L2-latency loads
+  constexpr bool kWsm = OZ_ROW_WSMEM && TWO_PASS;
+  uint32_t* const Wsm = smem + ((K * C + padC + 2 * G * tstride + 3) & ~3u);  // [K][C], 16B-aligned
+  __shared__ __align__(8) unsigned long long s_wbar;
+  auto w_rows = [&](int ci) -> const uint32_t* {  // global W rows (t = 0..K-1) of conv ci
+    const int cv = ci ? cv1 : cv0;
+    return P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff;
+  };
+  auto w_copy = [&](int ci) {  // one thread: bulk-copy conv ci's W rows into Wsm
+    fence_proxy_async_smem();  // earlier generic reads of Wsm (ordered by a CTA barrier)
+    mbar_expect_tx(&s_wbar, (uint32_t)K * C * 4u);
+    for (int t = 0; t < K; ++t) bulk_g2s(Wsm + t * C, w_rows(ci) + (size_t)t * m, C * 4u, &s_wbar);
+  };
+  if constexpr (kWsm) {
+    if (threadIdx.x == 0 && !P.fwd_only) {
+      const int ng0 = want0 ? __ldg(&P.sched[(b * 4 + (P.image ? 0 : cv0)) * sched_stride(K, L)]) : 0;
+      mbar_init(&s_wbar, 1);
+      mbar_fence_init();
+      if (ng0 > 0 || want1) w_copy(ng0 > 0 ? 0 : 1);
+    }
+  }
   // one (conv, group) entry per thread, every schedule load independent of the others (the
   // whole table costs one L2 latency; a serial walk over the groups cost ~10 dependent ones)
   for (int it = tv; it < 2 * G && !P.fwd_only; it += blockDim.x) {  // blockDim may be 1 (C < 32)
@@ -1340,15 +1374,13 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
       const uint32_t sx = (uint32_t)__ldg(&grp[2 + 2 * i]), tw = (uint32_t)__ldg(&grp[3 + 2 * i]);
       if (g < ng && i < np) {
         tg[1 + 2 * i] = sx * C;
-        tg[2 + 2 * i] = tw * (uint32_t)m;
+        tg[2 + 2 * i] = tw * (kWsm ? C : (uint32_t)m);  // W row offset (shared / global)
       }
     }
     if (g < ng) tg[0] = (uint32_t)np;
     if (g == 0) s_ng[ci] = ng;
   }
-#if OZ_ROW_BULKY
-  if constexpr (TWO_PASS) __syncthreads();  // barriers initialised
-#endif
+  if constexpr (TWO_PASS && (OZ_ROW_BULKY || kWsm)) __syncthreads();  // mbarriers initialised
   // ---- forward: last log2(C) DIF stages of each slice's NTT (Alg.6 l.787)
   for (int s = 0; s < ka; ++s) {
     uint32_t* xs = Xs + s * C;
@@ -1405,22 +1437,27 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   };
   // pointwise products for this thread's round-0 elements: 64-bit lazy sums of up to 3
   // products X * W~ (W~ = W m^{-1} 2^32, sums < 3 p^2 < 2^64), one Montgomery reduction each
+  auto wld = [&](const uint32_t* w) -> uint32_t {
+    if constexpr (kWsm) return *w;
+    else return ldg_stream(w);
+  };
   auto pointwise = [&](int ci, int g, uint32_t (&z)[E]) {
     const int cv = ci ? cv1 : cv0;
-    const uint32_t* Wb = P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff;
+    const uint32_t* Wb = kWsm ? Wsm : P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff;
     const uint32_t* tg = tab + (ci * G + g) * tstride;
     const int np = (int)tg[0];
+    if constexpr (kWsm) mbar_wait(&s_wbar, ci == 1 && s_ng[0] > 0 ? 1u : 0u);
 #if OZ_PW_BATCH
     if (np <= 3) {  // (L <= 3 always): the W loads of two pairs in flight ahead of the
                     // products (one L2 latency per group instead of one per pair)
       uint32_t w0[CNT], w1[CNT];
       const uint32_t* wr0 = Wb + tg[2];
 #pragma unroll
-      for (int i = 0; i < CNT; ++i) w0[i] = ldg_stream(&wr0[row_slot<LOGC, TWO_PASS>(tv, i)]);
+      for (int i = 0; i < CNT; ++i) w0[i] = wld(&wr0[row_slot<LOGC, TWO_PASS>(tv, i)]);
       if (np > 1) {
         const uint32_t* wr1 = Wb + tg[4];
 #pragma unroll
-        for (int i = 0; i < CNT; ++i) w1[i] = ldg_stream(&wr1[row_slot<LOGC, TWO_PASS>(tv, i)]);
+        for (int i = 0; i < CNT; ++i) w1[i] = wld(&wr1[row_slot<LOGC, TWO_PASS>(tv, i)]);
       }
       unsigned long long T[E];
       const uint32_t* x0 = Xs + tg[1];
@@ -1429,7 +1466,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
       if (np > 2) {
         const uint32_t* wr2 = Wb + tg[6];
 #pragma unroll
-        for (int i = 0; i < CNT; ++i) w0[i] = ldg_stream(&wr2[row_slot<LOGC, TWO_PASS>(tv, i)]);
+        for (int i = 0; i < CNT; ++i) w0[i] = wld(&wr2[row_slot<LOGC, TWO_PASS>(tv, i)]);
       }
       if (np > 1) {
         const uint32_t* x1 = Xs + tg[3];
@@ -1459,7 +1496,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
 #pragma unroll
         for (int i = 0; i < CNT; ++i) {
           const uint32_t pe = row_slot<LOGC, TWO_PASS>(tv, i);  // == row_perm(round-0 element)
-          T[i] += (unsigned long long)xr[pe] * ldg_stream(&wr[pe]);
+          T[i] += (unsigned long long)xr[pe] * wld(&wr[pe]);
         }
       }
 #pragma unroll
@@ -1472,7 +1509,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   auto out_ptr = [&](int ci, int g) -> uint32_t* {
     const int cv = ci ? cv1 : cv0;
     if constexpr (TWO_PASS) return P.G + (((b * 2 + q) * 4 + cv) * G + g) * m + rowoff;
-    return P.res + (((b * 4 + cv) * 2 + q) * G + g) * P.n;
+    return P.res + (((b * 4 + cv) * 2 + q) * P.rg + g) * P.n;
   };
   auto ztap_ptr = [&](int ci, int g) -> uint32_t* {
     const int cv = ci ? cv1 : cv0;
@@ -1490,6 +1527,12 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
     item(it, ci0, g0);
     uint32_t z[E];
     pointwise(ci0, g0, z);
+    if constexpr (kWsm) {
+      if (it == ng0 - 1 && nitems > ng0) {  // conv 0 done with Wsm: fetch conv 1's rows
+        __syncthreads();
+        if (threadIdx.x == 0) w_copy(1);
+      }
+    }
     uint32_t* const zt = ztap_ptr(ci0, g0);
     uint32_t* const op = out_ptr(ci0, g0);
     sub_ntt<LOGC, true, 1, LOGE, true>(
@@ -1511,7 +1554,8 @@ struct FinishParams {
   uint32_t p0, p1, p0inv, p0inv_sh;  // p0^{-1} mod p1 and its Shoup companion
   uint32_t p1_barrett;               // floor(2^32 / p1)
   unsigned long long P, halfP;       // p0 p1 and (p0 p1 - 1) / 2
-  const uint32_t* res;      // [nb][4][2][K*K][n]
+  const uint32_t* res;      // [nb][4][2][rg][n]
+  int rg;                   // group stride of res
   const int32_t* stats;
   const int32_t* sched;
   const double2* chirp;     // [n]
@@ -1594,8 +1638,8 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
     const int cv = cvt;
     double sh = 0.0, sl = 0.0;
     const int ng = s_ng[cv];
-    const uint32_t* r0 = P.res + (((b * 4 + cv) * 2 + 0) * G) * P.n + j;
-    const uint32_t* r1 = P.res + (((b * 4 + cv) * 2 + 1) * G) * P.n + j;
+    const uint32_t* r0 = P.res + (((b * 4 + cv) * 2 + 0) * P.rg) * P.n + j;
+    const uint32_t* r1 = P.res + (((b * 4 + cv) * 2 + 1) * P.rg) * P.n + j;
     for (int g0 = 0; g0 < ng; g0 += 9) {
       // issue every residue load of up to 9 groups before the dependent DD chain
       uint32_t z0[9], z1[9];
@@ -1685,8 +1729,8 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish_ts(FinishParams P) {
 #pragma unroll
   for (int cv = 0; cv < 4; ++cv) {
     TSv acc{0.0f, 0.0f, 0.0f};
-    const uint32_t* r0 = P.res + (((b * 4 + cv) * 2 + 0) * G) * P.n + j;
-    const uint32_t* r1 = P.res + (((b * 4 + cv) * 2 + 1) * G) * P.n + j;
+    const uint32_t* r0 = P.res + (((b * 4 + cv) * 2 + 0) * P.rg) * P.n + j;
+    const uint32_t* r1 = P.res + (((b * 4 + cv) * 2 + 1) * P.rg) * P.n + j;
     for (int g = 0; g < s_ng[cv]; ++g) {
       const long long Z = garner2(__ldcs(&r0[(int64_t)g * P.n]), __ldcs(&r1[(int64_t)g * P.n]), P);
       if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + j] = Z;
@@ -1732,8 +1776,8 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish_img(FinishParams P) {
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const uint32_t p = q ? P.p1 : P.p0;
-      const uint32_t zp = __ldcs(&P.res[(((b * 4 + 0) * 2 + q) * G + g) * P.n + j]);
-      const uint32_t zm = __ldcs(&P.res[(((b * 4 + 1) * 2 + q) * G + g) * P.n + j]);
+      const uint32_t zp = __ldcs(&P.res[(((b * 4 + 0) * 2 + q) * P.rg + g) * P.n + j]);
+      const uint32_t zm = __ldcs(&P.res[(((b * 4 + 1) * 2 + q) * P.rg + g) * P.n + j]);
       image_pair(zp, zm, P.inv2[q], P.inv2i[q], p, zr[q], zi[q]);
     }
     const double sc = s_sc[g];
@@ -1882,24 +1926,47 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
       for (int i = 0; i < NH; ++i) r0[i] = rr[i];
     } else {
       const double sc = s_sc[g];
+      if (P.crt_tap) {  // test-only tap: the CRT integers of the rows < n
 #pragma unroll
-      for (int i = 0; i < CNTL; ++i) {
-        if (!needed(i)) continue;
-        const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
-        const int h = hslot(i);
-        if (e * C < lim) {
-          const long long Z = q ? garner2(r0[h], rr[h], P.F) : garner2(rr[h], r0[h], P.F);  // l.974
-          if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + col + e * C] = Z;
-          if constexpr (TS) {  // f4: TSAdd of z 2^-cexp (slot holds the TS words)
-            Sacc[h * THREADS + tid] = ts_accum(Sacc[h * THREADS + tid], Z, s_ce[g]);
-            continue;
-          }
-          const double hi = __ll2double_rn(Z);
-          const double lo = __ll2double_rn(Z - __double2ll_rz(hi));
-          double2 a = Sacc[h * THREADS + tid];
-          dd_add(a.x, a.y, __dmul_rn(hi, sc), __dmul_rn(lo, sc), a.x, a.y);  // l.975-976
-          Sacc[h * THREADS + tid] = a;
+        for (int i = 0; i < CNTL; ++i) {
+          if (!needed(i)) continue;
+          const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
+          const int h = hslot(i);
+          if (e * C < lim)
+            P.crt_tap[((b * 4 + cv) * G + g) * P.n + col + e * C] =
+                q ? garner2(r0[h], rr[h], P.F) : garner2(rr[h], r0[h], P.F);
         }
+      }
+      // Garner (l.974) and the scaled sum in flush order (l.975-976) for every slot, without
+      // a per-row branch: rows >= n compute sums that are never stored, and the slots' chains
+      // are independent, so batches of OZ_CI_ILP of them interleave (a branch per row
+      // serialised them behind the DD add's dependent latency)
+#pragma unroll
+      for (int h0 = 0; h0 < NH; h0 += OZ_CI_ILP) {
+        constexpr int NB = OZ_CI_ILP;
+        double2 acc[NB];
+        long long Z[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (h0 + j < NH) {
+            const int h = h0 + j;
+            Z[j] = q ? garner2(r0[h], rr[h], P.F) : garner2(rr[h], r0[h], P.F);
+            acc[j] = Sacc[h * THREADS + tid];
+          }
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (h0 + j < NH) {
+            if constexpr (TS) {  // f4: TSAdd of z 2^-cexp (slot holds the TS words)
+              acc[j] = ts_accum(acc[j], Z[j], s_ce[g]);
+            } else {
+              const double hi = __ll2double_rn(Z[j]);
+              const double lo = __ll2double_rn(Z[j] - __double2ll_rz(hi));
+              dd_add(acc[j].x, acc[j].y, __dmul_rn(hi, sc), __dmul_rn(lo, sc), acc[j].x, acc[j].y);
+            }
+          }
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (h0 + j < NH) Sacc[(h0 + j) * THREADS + tid] = acc[j];
       }
     }
   }
@@ -2295,6 +2362,7 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   const int rle = row_loge(pl.logC, pl.logR > 0);
   const size_t padC = C + (C >> rle) + 1;
   c.row_smem = ((size_t)pl.K * C + padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
+  if (OZ_ROW_WSMEM && pl.logR > 0) c.row_smem = ((c.row_smem + 15) & ~(size_t)15) + (size_t)pl.K * C * 4;
   c.row_threads = pl.logC >= rle ? (1 << (pl.logC - rle)) : 1;  // exactly Tv: every thread active
   return c;
 }
@@ -2492,7 +2560,10 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   int32_t* digits = reinterpret_cast<int32_t*>(ws + pl.woff.digits) + w0 * 2 * K * n;
   uint32_t* Y = reinterpret_cast<uint32_t*>(ws + pl.woff.Y) + w0 * 4 * K * m;
   uint32_t* Gb = reinterpret_cast<uint32_t*>(ws + pl.woff.G) + w0 * 8 * G * m;
-  uint32_t* res = reinterpret_cast<uint32_t*>(ws + pl.woff.res) + w0 * 8 * G * n;
+  // residues: the workspace (stride K*K groups) or, for the unit-sharded single transform,
+  // the caller's exchange buffer (stride A.res_groups = the schedule's max group count)
+  uint32_t* res = A.res_out ? A.res_out : reinterpret_cast<uint32_t*>(ws + pl.woff.res) + w0 * 8 * G * n;
+  const int rg = A.res_out ? A.res_groups : G;
   double2* Sdd = reinterpret_cast<double2*>(ws + pl.woff.S) + w0 * 4 * n;
   const uint2* tw = reinterpret_cast<const uint2*>(pl.pers + pl.poff.tw);
   const uint32_t* W = reinterpret_cast<const uint32_t*>(pl.pers + pl.poff.W);
@@ -2516,8 +2587,8 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   SP.wsplit = wsplit;
   SP.L = L;
   SP.shared = pl.image;
-  ozfft_status s = launch_split(pl, SP, nb, st);
-  if (s) return s;
+  ozfft_status s = A.phase == 2 ? OZFFT_OK : launch_split(pl, SP, nb, st);
+  if (s || A.phase == 1) return s;
   const NttLaunch c = ntt_launch_cfg(pl);
   uint32_t* Xtap = nullptr;
   uint32_t* Ztap = nullptr;
@@ -2532,7 +2603,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.logm = pl.logm; CP.logC = pl.logC; CP.logR = pl.logR; CP.logCb = c.logCb;
     CP.nb = nb; CP.K = K; CP.L = L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
     CP.tw = tw; CP.digits = SP.digits; CP.in_len = n; CP.Y = Y; CP.stats = stats;
-    CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n; CP.unit_mask = A.unit_mask;
+    CP.sched = sched; CP.G = Gb; CP.res = res; CP.rg = rg; CP.n = n; CP.unit_mask = A.unit_mask;
     CP.image = pl.image;
     fill_iota(pl, CP.io);
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
@@ -2546,7 +2617,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   RowParams RP{};
   RP.logm = pl.logm; RP.logC = pl.logC; RP.logR = pl.logR; RP.nb = nb; RP.K = K; RP.L = L;
   RP.p[0] = pl.p[0]; RP.p[1] = pl.p[1]; RP.tw = tw; RP.digits = SP.digits; RP.in_len = n;
-  RP.Y = Y; RP.W = W; RP.pinv[0] = pl.pinv[0]; RP.pinv[1] = pl.pinv[1]; RP.G = Gb; RP.res = res; RP.n = n; RP.stats = stats; RP.sched = sched;
+  RP.Y = Y; RP.W = W; RP.pinv[0] = pl.pinv[0]; RP.pinv[1] = pl.pinv[1]; RP.G = Gb; RP.res = res; RP.rg = rg; RP.n = n; RP.stats = stats; RP.sched = sched;
   RP.unit_mask = A.unit_mask; RP.fwd_only = 0; RP.Xout = Xtap; RP.Zout = Ztap;
   RP.image = pl.image;
   fill_iota(pl, RP.io);
@@ -2624,7 +2695,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     ColParams CP{};
     CP.logm = pl.logm; CP.logC = pl.logC; CP.logR = pl.logR; CP.logCb = c.logCb;
     CP.nb = nb; CP.K = K; CP.L = L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
-    CP.tw = tw; CP.stats = stats; CP.sched = sched; CP.G = Gb; CP.res = res; CP.n = n;
+    CP.tw = tw; CP.stats = stats; CP.sched = sched; CP.G = Gb; CP.res = res; CP.rg = rg; CP.n = n;
     CP.unit_mask = A.unit_mask;
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 8;
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
@@ -2636,7 +2707,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   }
   if (A.finish && !fused) {
     FinishParams FP{};
-    FP.n = n; FP.nb = nb; FP.K = K; FP.L = L; fill_crt_consts(pl, FP); FP.res = res; FP.stats = stats; FP.sched = sched;
+    FP.n = n; FP.nb = nb; FP.K = K; FP.L = L; fill_crt_consts(pl, FP); FP.res = res; FP.rg = rg; FP.stats = stats; FP.sched = sched;
     FP.chirp = chirp; FP.out = reinterpret_cast<double2*>(A.out); FP.direction = A.direction;
     FP.crt_tap = taps ? reinterpret_cast<int64_t*>(taps->crt) : nullptr;
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)nb);
@@ -2759,11 +2830,11 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   return s;
 }
 
-ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, double* out,
+ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, int groups, double* out,
                                          int direction, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   FinishParams FP{};
-  FP.n = pl.n; FP.nb = 1; FP.K = pl.K; FP.L = pl.L; fill_crt_consts(pl, FP); FP.res = res;
+  FP.n = pl.n; FP.nb = 1; FP.K = pl.K; FP.L = pl.L; fill_crt_consts(pl, FP); FP.res = res; FP.rg = groups;
   FP.stats = reinterpret_cast<const int32_t*>(pl.ws + pl.woff.stats);
   FP.sched = reinterpret_cast<const int32_t*>(pl.ws + pl.woff.sched);
   FP.chirp = reinterpret_cast<const double2*>(pl.pers + pl.poff.chirp);

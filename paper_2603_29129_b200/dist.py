@@ -8,7 +8,8 @@ Two partitionings of the hot path:
   (u = 2 cv + q) are split into contiguous blocks of 8 / world units.  Every rank
   redoes the O(n) premultiply + split (identical digits everywhere), computes the
   forward NTTs, NTT-domain accumulation and inverse NTTs of its units, and the
-  residues [8 units][K*K groups][n] are all-gathered (one NCCL all_gather_into_tensor)
+  residues [8 units][g groups][n] (g = the schedule's largest group count, known to every
+  rank after the split) are all-gathered in place (one NCCL all_gather_into_tensor)
   before every rank runs Garner's CRT, the DD recombination and the post-chirp.
 
 The compute steps are passed in as callables so the gather/layout logic can be tested
@@ -44,35 +45,36 @@ def unit_of(cv: int, q: int) -> int:
     return 2 * cv + q
 
 
-def sharded_transform(residues: torch.Tensor, rank: int, world: int,
-                      partial: Callable[[int, int, torch.Tensor], None],
-                      finish: Callable[[torch.Tensor], torch.Tensor],
+def sharded_transform(residues: torch.Tensor, n: int, rank: int, world: int,
+                      partial: Callable[[int, int, torch.Tensor], int],
+                      finish: Callable[[torch.Tensor, int], torch.Tensor],
                       group=None) -> torch.Tensor:
-    """Run one transform split over `world` ranks.
+    """Run one length-n transform split over `world` ranks.
 
-    residues: flat int32 buffer of 8 * G * n words (layout [unit][group][n]) on this
-    rank's device; partial(rank, world, residues) fills this rank's contiguous slice;
-    finish(residues) returns the transform from the gathered buffer.
+    residues: flat buffer of at least 8 * K*K * n words on this rank's device.
+    partial(rank, world, residues) writes this rank's units into their place of the layout
+    [8 units][g][n] and returns g (the schedule's group count, the same on every rank);
+    one in-place all_gather_into_tensor of the equal rank slices completes the 8 g n words
+    on every rank (no staging copy); finish(residues, g) returns the transform.
     """
-    partial(rank, world, residues)
+    g = partial(rank, world, residues)
     if world > 1:
-        per = residues.numel() // world
-        mine = residues[rank * per:(rank + 1) * per].clone()
-        dist.all_gather_into_tensor(residues, mine, group=group)
-    return finish(residues)
+        buf = residues[:NUNITS * g * n]
+        per = buf.numel() // world
+        dist.all_gather_into_tensor(buf, buf[rank * per:(rank + 1) * per], group=group)
+    return finish(residues, g)
 
 
 def gpu_sharded_forward(plan, x: torch.Tensor, rank: int, world: int, direction: int = -1,
                         group=None) -> torch.Tensor:
-    """Single-transform sharded execute on GPUs (plan.batch transforms; transform 0 used)."""
-    nwords = plan.shard_residue_bytes() // 4
-    residues = torch.empty(nwords, dtype=torch.int32, device=x.device)
+    """Single-transform sharded execute on GPUs (transform 0 of x)."""
+    residues = torch.empty(plan.shard_residue_bytes() // 4, dtype=torch.int32, device=x.device)
     out = torch.empty(plan.n, dtype=torch.complex128, device=x.device)
 
     def partial(r, w, res):
-        plan.shard_partial(x, r, w, res, direction)
+        return plan.shard_partial(x, r, w, res, direction)
 
-    def finish(res):
-        return plan.shard_finish(res, out, direction)
+    def finish(res, g):
+        return plan.shard_finish(res, g, out, direction)
 
-    return sharded_transform(residues, rank, world, partial, finish, group)
+    return sharded_transform(residues, plan.n, rank, world, partial, finish, group)

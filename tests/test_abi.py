@@ -118,7 +118,10 @@ def test_entry_point_errors_without_device(lib):
     buf = ctypes.c_void_p(1 << 20)  # never dereferenced: the checks fail first
     assert L.ozfft_execute(h, buf, buf, -1, None) == 5          # NOT_BOUND
     assert L.ozfft_execute_host(h, buf, buf, -1, None) == 5
-    assert L.ozfft_shard_partial(h, 0, 2, buf, -1, buf, None) == 5
+    g = ctypes.c_int32(0)
+    assert L.ozfft_shard_partial(h, 0, 2, buf, -1, buf, ctypes.byref(g), None) == 5
+    assert L.ozfft_shard_residue_bytes(h, 0) == 8 * 9 * 1000 * 4   # K*K capacity
+    assert L.ozfft_shard_residue_bytes(h, 5) == 160 * 1000          # 8 g n words
     st = oz.ExecStats()
     assert L.ozfft_last_stats(h, ctypes.byref(st), None) == 5
     assert L.ozfft_plan_bind(h, None, 0, None, 0, None) == 1    # null buffers

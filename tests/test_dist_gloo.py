@@ -56,17 +56,23 @@ def _worker(rank, world, port, outq):
         for cv in range(4):
             for qq in range(2):
                 full[D.unit_of(cv, qq)] = taps["res"][cv, :, qq, :]
-        buf = torch.zeros(D.NUNITS * G * n, dtype=torch.int64)
+        # exchange sized by the schedule: g = max_cv ng_cv (every rank knows it after the
+        # split), layout [8 units][g][n] inside a K*K-capacity buffer
+        g = int(max(taps["sched"][cv, 0] for cv in range(4)))
+        assert 5 <= g <= G  # >= 2K - 1 anti-diagonal groups; Alg.8 gaps add groups (n = 37: 7)
+        buf = torch.full((D.NUNITS * G * n,), -1, dtype=torch.int64)
 
         def partial(r, w, res):
             for u in D.shard_units(r, w):
-                res.view(D.NUNITS, G, n)[u] = torch.from_numpy(full[u])
+                res[:D.NUNITS * g * n].view(D.NUNITS, g, n)[u] = torch.from_numpy(full[u][:g])
+            return g
 
-        def finish(res):
-            return res.view(D.NUNITS, G, n).clone()
+        def finish(res, gg):
+            return res[:D.NUNITS * gg * n].view(D.NUNITS, gg, n).clone()
 
-        got = D.sharded_transform(buf, rank, world, partial, finish)
-        assert np.array_equal(got.numpy(), full)
+        got = D.sharded_transform(buf, n, rank, world, partial, finish)
+        assert np.array_equal(got.numpy(), full[:, :g])
+        assert torch.all(buf[D.NUNITS * g * n:] == -1)  # nothing beyond the 8 g n words moved
         # ---- max over ranks (bench.py timing rule)
         t = torch.tensor([float(rank + 1)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -102,3 +108,53 @@ def test_partition_helpers():
     assert D.shard_units(1, 2) == [4, 5, 6, 7]
     with pytest.raises(ValueError):
         D.shard_units(0, 3)
+
+
+def test_bench_rank_inputs_cover_the_config():
+    """bench.py's batch sharding: the ranks' row slices of the seeded config input concatenate
+    to exactly workloads.config_input(cfg) (every rank transforms part of the N = 1 job)."""
+    import bench
+    for name in ("c1", "c2", "c3", "c4"):
+        cfg = workloads.CONFIGS[name]
+        full = workloads.config_input(cfg)
+        for world in (1, 2, 3, 4, 8):
+            parts = [bench.rank_input(cfg, r, world) for r in range(world)]
+            assert [p[0] for p in parts] == [D.batch_slice(cfg.batch, r, world)[0] for r in range(world)]
+            cat = np.concatenate([p[2] for p in parts if p[1]])
+            assert cat.shape == full.shape and np.array_equal(cat, full), (name, world)
+
+
+def _gather_worker(rank, world, port, outq):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        total, n = 7, 5
+        full = torch.from_numpy(workloads.draw("normal", 3, total, n))
+        start, cnt = D.batch_slice(total, rank, world)
+        coll = bench.Coll(world, torch.device("cpu"))
+        got = coll.gather_rows(full[start:start + cnt].clone() if cnt else None, total, n)
+        assert torch.equal(got, full)
+        assert coll.max(float(rank)) == float(world - 1)
+        outq.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover
+        outq.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_gather_rows_gloo(world):
+    """bench.Coll.gather_rows reassembles the ranks' output rows in batch order (the
+    bitwise_vs_n1 check), including ranks with unequal counts."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [(r, "ok") for r in range(world)], res

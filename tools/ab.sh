@@ -7,6 +7,12 @@ if [ -n "${TESTS-tests/test_gpu_parity.py}" ]; then
   tail -3 gpurun_out/ab/tests.log
 fi
 cp paper_2603_29129_b200/libozfft.so /tmp/libozfft_main.so
+for vt in $VTEST; do  # parity of variant builds too
+  cp variants/libozfft_$vt.so paper_2603_29129_b200/libozfft.so
+  timeout 900 python -m pytest ${VTESTS:-tests/test_gpu_parity.py tests/test_gpu_configs.py} -x -q > gpurun_out/ab/tests_$vt.log 2>&1
+  echo "tests $vt: $(tail -1 gpurun_out/ab/tests_$vt.log)"
+done
+cp /tmp/libozfft_main.so paper_2603_29129_b200/libozfft.so
 for tag in main "$@"; do
   [ "$tag" = main ] && f=/tmp/libozfft_main.so || f=variants/libozfft_$tag.so
   cp $f paper_2603_29129_b200/libozfft.so
