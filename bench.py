@@ -448,8 +448,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     fwd_vec = stats["fwd_ntts"]  # forward NTT vectors of the last execute (whole batch)
     inv_vec = stats["inv_ntts"]  # inverse NTT vectors (2 per Alg.8 group)
     per_exec = {  # (bytes, butterflies) per execute over the batch -- DESIGN.md "Algorithmic work"
-        "split_max": (3 * 32 * n * B, 0),
-        "split_digits": (32 * n * B + 24 * n * B, 0),
+        # x (16 n B per transform) per level; the chirp (16 n B) is shared by the batch
+        "split_max": (plan.K * (16 * n * B + 16 * n), 0) if prof["split_digits"][1]
+        else (16 * n * B + 16 * n + 24 * n * B, 0),  # n <= 2^15: one cluster launch (x once, digits)
+        "split_digits": (16 * n * B + 16 * n + 24 * n * B, 0),
         "col_fwd": (fwd_vec * 4 * (n + m), fwd_vec * (m // 2) * logR),
         "row_fused": (fwd_vec * 4 * m + inv_vec * 4 * m, (fwd_vec + inv_vec) * (m // 2) * logC),
         "col_inv": (inv_vec * 4 * (m + n), inv_vec * (m // 2) * logR),

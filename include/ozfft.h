@@ -52,6 +52,11 @@ typedef enum {
   OZFFT_ERR_BUFFER_TOO_SMALL = 9    /* persistent or workspace size below plan_get_info  */
 } ozfft_status;
 
+/* Test-only environment knob (read at ozfft_plan_create): OZFFT_FAULT_INJECT=1 flips one
+ * bit of one NTT-domain group value after the row pass of every execute (transform 0,
+ * prime 0, conv rr, the last Alg.8 group) -- the GPU parity tests must then fail
+ * (tests/test_gpu_fault.py).  Never set it otherwise. */
+
 /* Plan descriptor.  Defaults (zeros) mean: K = 3, L = 3, p0 = 2,130,706,433,
  * p1 = 2,113,929,217 (the paper's primes), device = current device,
  * max_workspace_bytes = 16 GiB (the batch is processed in chunks that fit). */

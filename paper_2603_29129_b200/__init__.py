@@ -149,7 +149,7 @@ def _stream_ptr(stream, device=None) -> int:
 
 
 class Plan:
-    """Plan for `batch` complex fp64 DFTs of length n (any n, 1 <= n <= 2^21; power-of-two n <= 2^22 with conv="cyclic").
+    """Plan for `batch` complex fp64 DFTs of length n (any n, 1 <= n <= 2^23: m <= 2^24, the paper primes' limit).
 
     K: split cap per real vector; L: NTT-domain accumulation bound
     (P:940-946).  p0, p1: NTT primes (default: the paper's).

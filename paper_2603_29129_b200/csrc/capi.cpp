@@ -2,6 +2,7 @@
 // Validation, plan sizing/memory layout, chunked execution and statistics.  All
 // compute is in kernels.cu; there is no CPU fallback anywhere in this library.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -12,9 +13,6 @@
 
 #include "internal.h"
 
-#ifndef OZFFT_GIT
-#define OZFFT_GIT "dev"
-#endif
 
 struct ozfft_plan : ozfft::Plan {};
 
@@ -61,7 +59,17 @@ static std::atomic<uint64_t> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 uint64_t launches_so_far() { return g_launches.load(std::memory_order_relaxed); }
 
+// NVTX ranges per stage (host timeline of the launches; free unless a tool such as ncu or
+// nsys is attached -- NVTX3 is header-only and resolves its injection library lazily)
+static const char* const kStageNames[OZFFT_NSTAGES] = {
+    "ozfft:split_max", "ozfft:split_digits", "ozfft:col_fwd", "ozfft:row_fused", "ozfft:col_inv",
+    "ozfft:crt_finish"};
+
 void prof_mark(const Plan& pl, int stage, bool begin, void* stream) {
+  if (begin)
+    nvtxRangePushA(kStageNames[stage]);
+  else
+    nvtxRangePop();
   Prof* pr = pl.prof;
   if (!pr || !pr->on) return;
   if (pr->next >= pr->pool.size()) {
@@ -166,7 +174,8 @@ const char* ozfft_status_string(ozfft_status s) {
 
 const char* ozfft_last_error_string(void) { return g_err.c_str(); }
 
-const char* ozfft_version(void) { return "ozfft sm_100a " OZFFT_GIT; }
+// ozfft_version() is defined in the generated _build/version.cpp (build.py): git revision +
+// a hash of every library source, rebuilt whenever any of them changes.
 
 ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
   if (!d || !out) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null descriptor or output pointer");
@@ -234,12 +243,12 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     delete pl;
     return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "m exceeds the primes' two-adicity");
   }
-  if (logm > 22) {
+  if (logm > 24) {  // (the paper's primes allow 2^24: two-adicity of p0)
     delete pl;
-    return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "this build supports m <= 2^22 (n <= 2^21 padded, 2^22 cyclic)");
+    return fail(OZFFT_ERR_UNSUPPORTED_LENGTH, "m <= 2^24 (n <= 2^23)");
   }
   // NTT decomposition: one pass up to m = 2^12, else rows of C = 2^11 (2^12 from m = 2^20) and
-  // columns of R = m / C <= 2^8 (up to 2^10 at m = 2^21, 2^22, with 32 elements per thread).
+  // columns of R = m / C <= 2^8 (up to 2^12 at m = 2^20 .. 2^24, with 32 elements per thread).
   // (Measured alternatives at c3: one-warp rows of C = 2^10, 122 vs 147 GFLOP/s; rows of
   // C = 2^12, 141 vs 154 GFLOP/s -- OZFFT_TUNE_LOGC=12 still selects the latter.)
   pl->logC = logm <= 12 ? logm : std::min(12, std::max(11, logm - 8));
@@ -248,6 +257,8 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     if (logm > 12 && decomposition_supported(logm - v, v)) pl->logC = v;
   }
   pl->logR = logm - pl->logC;
+  if (const char* t = std::getenv("OZFFT_FAULT_INJECT"))  // test-only: must trip the parity tests
+    pl->fault = std::atoi(t) != 0;
   if (const char* t = std::getenv("OZFFT_SPLIT_CLUSTER_MAXLEN"))  // knob (tests/tools): 0 = off
     pl->split_cluster_max = std::atoll(t);
   // image mode: a real output sums L n complex products (|Re| <= 2 4^alpha each)

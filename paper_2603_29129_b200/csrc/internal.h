@@ -38,6 +38,7 @@ struct Plan {
   uint32_t iota[2] = {0, 0};         // image mode: iota_q = g^((p_q - 1)/4), iota^2 = -1
   int device = 0;
   uint64_t max_ws = 0;
+  int fault = 0;                     // test-only (env OZFFT_FAULT_INJECT at create): corrupt one residue
   // host tables (built at create)
   std::vector<double> chirp;       // [n][2] = (C_j, S_j), omega(j) = C_j + i S_j
   std::vector<double> wstar;       // [m][2] omega~* = ZeroPad_pm(conj(omega), m)

@@ -1054,13 +1054,15 @@ struct ColCfg {
 };
 
 // Column tile geometry: R x Cb columns with (R / E) * Cb = 256 threads (Cb >= 8 so that each
-// row segment is at least one 32-byte sector).
+// row segment is at least one 32-byte sector; the long columns of R = 2^11, 2^12 -- m = 2^23,
+// 2^24, the primes' limit -- take Cb = 4, 2 to stay at 256 threads).
+__host__ __device__ constexpr int col_log_cb_raw(int logR) {
+  return logR >= col_loge(logR) ? 8 - (logR - col_loge(logR)) : 8;
+}
 __host__ __device__ constexpr int col_log_cb(int logR, int logC) {
-  return (logR >= col_loge(logR) ? (8 - (logR - col_loge(logR)) < 3 ? 3 : 8 - (logR - col_loge(logR)))
-                                 : 8) > logC
+  return (col_log_cb_raw(logR) < (logR >= 11 ? 1 : 3) ? (logR >= 11 ? 1 : 3) : col_log_cb_raw(logR)) > logC
              ? logC
-             : (logR >= col_loge(logR) ? (8 - (logR - col_loge(logR)) < 3 ? 3 : 8 - (logR - col_loge(logR)))
-                                       : 8);
+             : (col_log_cb_raw(logR) < (logR >= 11 ? 1 : 3) ? (logR >= 11 ? 1 : 3) : col_log_cb_raw(logR));
 }
 
 // Stages of the column pass's step-1 round (DIF: the last round; DIT: the first).
@@ -1102,7 +1104,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(C
   const uint2* T = P.tw + (size_t)(q * 2 + 0) * m;
   const uint32_t lim = P.in_len > col ? (uint32_t)(P.in_len - col) : 0u;  // e*C < lim <=> i < in_len
   constexpr int S1 = col_s1(LOGR);
-  constexpr uint32_t TILEW = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;  // even (Cb >= 8)
+  constexpr uint32_t TILEW = (((1u << LOGR) + (1u << LOGR) / E + 1) * Cb + 1) & ~1u;  // 8-byte aligned
   uint2* tw0 = reinterpret_cast<uint2*>(smem + TILEW);  // [2^S1][Cb] step-1 twiddles
   stage_col_tw0<S1, Cb>(tw0, T, C, cb << LOGCB);
   __syncthreads();
@@ -1876,7 +1878,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
     s_sc[g] = scalbn(1.0, -s_ce[g]);
   }
   constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;
-  double2* Sacc = reinterpret_cast<double2*>(smem + TILE + (TILE & 1));  // [NH][THREADS]
+  double2* Sacc = reinterpret_cast<double2*>(smem + ((TILE + 3) & ~3u));  // [NH][THREADS], 16B-aligned
   // (staging the step-1 round twiddles in shared memory, as k_col_fwd does, measured slower
   // here: 833 vs 813 us at c3 -- they already hit L1, shared by the 16 threads of a column)
 #pragma unroll
@@ -2024,7 +2026,7 @@ __global__ void __launch_bounds__(256, 2) k_col_inv_crt_img(ColCrtParams P) {
   const int ng = srow[0];
   for (int g = tid; g < ng; g += blockDim.x) s_sc[g] = scalbn(1.0, -srow[1 + g * (2 + 2 * P.L)]);
   constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;
-  double2* Sacc = reinterpret_cast<double2*>(smem + TILE + (TILE & 1));  // [2][NH][THREADS]
+  double2* Sacc = reinterpret_cast<double2*>(smem + ((TILE + 3) & ~3u));  // [2][NH][THREADS], 16B-aligned
 #pragma unroll
   for (int i = 0; i < 2 * NH; ++i) Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
   const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
@@ -2207,6 +2209,15 @@ __global__ void k_w_finalize(const uint32_t* __restrict__ X, uint32_t* __restric
   }
 }
 
+// Test-only fault injection (Plan::fault, env OZFFT_FAULT_INJECT): flip bit 0 of the first
+// word of one NTT-domain group value / residue vector -- the last group in Alg.8 flush order
+// (the leading digits, so the error reaches the fp64 output; the first groups hold the
+// smallest terms, 2^-144 below) -- so that the parity tests must fail (tests/test_gpu_fault.py).
+__global__ void k_fault_inject(uint32_t* base, int64_t gstride, const int32_t* sched) {
+  const int g = sched[0] > 0 ? sched[0] - 1 : 0;
+  base[g * gstride] ^= 1u;
+}
+
 // Tap conversion: internal bit-reversed order (optionally row-permuted, optionally times a
 // per-vector constant mod p) -> natural order:  dst[o(v)][k] = src[v][pos(bitrev(k))] * mult[v].
 __global__ void k_tap_permute(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
@@ -2356,7 +2367,7 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   NttLaunch c;
   c.logCb = col_logCb(pl.logR, pl.logC);
   c.col_smem = col_smem(pl.logR, c.logCb);
-  c.col_fwd_smem = c.col_smem + ((size_t)1 << col_s1(pl.logR)) * ((size_t)1 << c.logCb) * 8;
+  c.col_fwd_smem = ((c.col_smem + 7) & ~(size_t)7) + ((size_t)1 << col_s1(pl.logR)) * ((size_t)1 << c.logCb) * 8;
   c.col_threads = col_threads(pl.logR, c.logCb);
   const size_t C = 1ull << pl.logC;
   const int rle = row_loge(pl.logC, pl.logR > 0);
@@ -2380,7 +2391,7 @@ static void dispatch_log(int v, F&& f) {
 
 // Compile-time dispatch of the two-pass decompositions this build instantiates (capi.cpp
 // picks them): C = 2^11 with R = 2^2 .. 2^8 (m = 2^13 .. 2^19) and C = 2^12 with R = 2^7 ..
-// 2^10 (m = 2^19 tuning knob, 2^20 .. 2^22).  f(R, C) receives integral constants.
+// 2^12 (m = 2^19 tuning knob, 2^20 .. 2^24).  f(R, C) receives integral constants.
 template <int R, int C, class F>
 static void dispatch_rc_(int logR, int logC, F& f) {
   if constexpr (C == 11 && R <= 8) {
@@ -2388,7 +2399,7 @@ static void dispatch_rc_(int logR, int logC, F& f) {
     return dispatch_rc_<R + 1, C>(logR, logC, f);
   } else if constexpr (C == 11) {
     return dispatch_rc_<7, 12>(logR, logC, f);
-  } else if constexpr (R <= 10) {
+  } else if constexpr (R <= 12) {
     if (logR == R && logC == C) return f(std::integral_constant<int, R>{}, std::integral_constant<int, C>{});
     return dispatch_rc_<R + 1, C>(logR, logC, f);
   }
@@ -2398,7 +2409,7 @@ static void dispatch_rc(int logR, int logC, F&& f) {
   dispatch_rc_<2, 11>(logR, logC, f);
 }
 bool decomposition_supported(int logR, int logC) {
-  return (logC == 11 && logR >= 2 && logR <= 8) || (logC == 12 && logR >= 7 && logR <= 10);
+  return (logC == 11 && logR >= 2 && logR <= 8) || (logC == 12 && logR >= 7 && logR <= 12);
 }
 
 
@@ -2635,6 +2646,10 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     count_launches(1);
     s = cuda_check("k_row_fused");
     if (s) return s;
+    if (pl.fault && (A.unit_mask & 1u)) {  // test-only: unit (cv 0, prime 0), group 0, first word
+      k_fault_inject<<<1, 1, 0, st>>>(pl.logR > 0 ? Gb : res, pl.logR > 0 ? m : n, sched);
+      count_launches(1);
+    }
   }
   // fused inverse column pass + CRT + DD accumulation (full transforms with R > 1)
   const bool fused = pl.logR > 0 && A.unit_mask == 0xFFu && A.finish;
@@ -2652,7 +2667,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     const size_t tile = ((1ull << pl.logR) + ((1ull << pl.logR) >> cle) + 1) * (1ull << lcb);
     const bool prune = 2 * n <= m;  // padded plans; cyclic plans (m = n) need every row
     const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / (prune ? 2 : 1);
-    const size_t smem = (tile + (tile & 1)) * 4 + (size_t)nh * threads * 16 * (pl.image ? 2 : 1);
+    const size_t smem = ((tile + 3) & ~(size_t)3) * 4 + (size_t)nh * threads * 16 * (pl.image ? 2 : 1);
     const int64_t nblk = (1ll << (pl.logC - lcb)) * nb * (pl.image ? 1 : 4);
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
     dispatch_rc(pl.logR, pl.logC, [&](auto I, auto J) {

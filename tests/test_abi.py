@@ -78,7 +78,7 @@ def test_plan_create_validation(lib):
     assert create(K=9)[0] == 1
     assert create(p0=2130706433, p1=2130706433)[0] == 3
     assert create(p0=2130706431)[0] == 3          # not prime
-    assert create(n=1 << 22)[0] == 2              # m = 2^23 > this build's limit
+    assert create(n=(1 << 23) + 1)[0] == 2        # m = 2^25 > the primes' limit 2^24
     st, info = create(n=1)
     assert st == 0 and info.m == 1
     # cyclic Bluestein: m = n for power-of-two n, same alpha as the padded plan
@@ -86,9 +86,12 @@ def test_plan_create_validation(lib):
     assert st == 0 and info.m == 1 << 18 and info.alpha == 20 and info.conv_mode == 1
     st, info = create(n=1 << 20, conv_mode=1)     # m = 2^20
     assert st == 0 and info.m == 1 << 20
-    st, info = create(n=1 << 21)                  # m = 2^22 = 2^10 x 2^12, the largest
+    st, info = create(n=1 << 21)                  # m = 2^22 = 2^10 x 2^12
     assert st == 0 and info.m == 1 << 22 and info.log2_rows == 10 and info.log2_cols == 12
-    assert create(n=(1 << 21) + 1)[0] == 2        # m = 2^23: beyond this build
+    st, info = create(n=(1 << 21) + 1)            # m = 2^23 = 2^11 x 2^12
+    assert st == 0 and info.m == 1 << 23 and info.log2_rows == 11 and info.log2_cols == 12
+    st, info = create(n=1 << 23)                  # m = 2^24 = 2^12 x 2^12: the primes' limit
+    assert st == 0 and info.m == 1 << 24 and info.log2_rows == 12 and info.log2_cols == 12
     assert create(n=1 << 22, conv_mode=1)[0] == 0
     assert create(n=100003, conv_mode=1)[0] == 2  # not a power of two
     assert create(n=1024, conv_mode=2)[0] == 1    # unknown mode

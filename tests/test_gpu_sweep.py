@@ -53,3 +53,24 @@ def test_count_laws(oz, phi, n, K, L):
         assert total == 64  # P:1164, 24K - 8
     yo = O.Plan(n, K, L).execute(x[0])
     assert np.array_equal(y[0].cpu().numpy(), yo)
+
+
+@pytest.mark.parametrize("phi,n,K,L,count", [
+    (0.0, 1 << 17, 8, 1, 196),   # maximum count 196 for (K, L) = (inf, 1) at phi = 0, 1.0
+    (1.0, 1 << 18, 8, 1, 196),
+    (4.0, 1 << 18, 8, 1, 268),   # maximised at (phi, n) = (4.0, 2^17), (4.0, 2^18): 268
+    (4.0, 1 << 17, 3, 3, 80),    # for phi = 4.0 the maximum count for (3, 3) was 80
+    (4.0, 1 << 18, 3, 3, 80),
+])
+def test_paper_counts_triple_single(oz, phi, n, K, L, count):
+    """The paper's K = inf / accumulation counts, reproduced in its own triple-single working
+    precision (SURVEY f3 + f4; profiles/r02_ts_sweep.md): the largest per-transform count
+    over tools/sweep.py's 4 seeded phi-inputs of that point (K = inf is the cap K = 8)."""
+    x = workloads.phi_input(n, phi, seed=int(np.log2(n)) * 10 + int(phi), batch=4)
+    plan = oz.Plan(n, 1, K=K, L=L, precision="ts")
+    counts = []
+    for b in range(4):
+        plan.forward(torch.from_numpy(x[b:b + 1].copy()).cuda())
+        st = plan.stats()
+        counts.append(st["fwd_ntts"] + st["inv_ntts"] + st["cached_ntts"])
+    assert max(counts) == count, counts

@@ -117,7 +117,7 @@ def test_image_against_float128(n, dist):
     hi, lo = O.dft_f128(x)
     ref = hi + lo
     err = np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-300)
-    assert err <= 1e-15, err
+    assert err <= 4e-16, err  # measured <= 1.64e-16 (as tests/test_oracle_pipeline.py PIN)
 
 
 def test_image_roundtrip_and_nonfinite():

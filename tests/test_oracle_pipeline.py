@@ -95,6 +95,14 @@ def rel_err(y, hi, lo):
     return np.max(np.abs((y - hi) - lo)) / np.max(np.abs(hi))
 
 
+# The oracle's measured error against the __float128 DFT is <= 1.64e-16 relative to norm over
+# every case below (padded, cyclic, image and TS modes alike; dominated by the fp64 chirp
+# rounding).  The pin is 4e-16, well inside the paper's [1e-16, 1e-15] band, so
+# a slip in the DD recombination or post-chirp (a dropped low word, a wrong flush order)
+# that costs a few ulps shows up here.
+PIN = 4e-16
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 7, 16, 37, 64, 100, 256, 997, 1024])
 @pytest.mark.parametrize("dist", ["uniform", "normal", "signexp"])
 def test_against_float128_dft(golden, n, dist):
@@ -102,7 +110,8 @@ def test_against_float128_dft(golden, n, dist):
     y = O.Plan(n).execute(x)
     hi, lo = O.dft_f128(x)
     e = rel_err(y, hi, lo)
-    assert e <= golden["error_band"]["hi"], e
+    assert e <= PIN, e
+    assert e <= golden["error_band"]["hi"]
 
 
 def test_against_float128_bins_large():
@@ -112,7 +121,7 @@ def test_against_float128_bins_large():
     bins = np.random.default_rng(0).choice(n, 64, replace=False)
     hi, lo = O.dft_f128(x, bins=bins)
     full_hi, _ = O.dft_f128(x, bins=None) if n <= 4096 else (None, None)
-    assert np.max(np.abs((y[bins] - hi) - lo)) / np.max(np.abs(full_hi)) <= 1e-15
+    assert np.max(np.abs((y[bins] - hi) - lo)) / np.max(np.abs(full_hi)) <= PIN
 
 
 @pytest.mark.parametrize("n", [8, 13, 64, 100])
@@ -152,7 +161,7 @@ def test_parseval_linearity_roundtrip():
     xr = pl.execute(y, inverse=True)
     assert np.max(np.abs(xr - x)) / np.max(np.abs(x)) <= 1e-15
     hi, lo = O.dft_f128(y, inverse=True)
-    assert rel_err(xr, hi, lo) <= 1e-15
+    assert rel_err(xr, hi, lo) <= PIN
 
 
 def test_nonfinite_and_zero():

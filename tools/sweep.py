@@ -11,7 +11,8 @@ GPU path with seeded synthetic inputs and a __float128 reference instead of MPFR
           __float128 direct DFT (oracle.dft_f128) on all bins (n <= 4096) or 256 seeded bins
   alpha   the four split widths of Fig. 1 (oracle.alpha_formulas)
 
-Writes profiles/<tag>_sweep.json and .md.   python tools/sweep.py [tag] [max_log2n]
+Writes profiles/<tag>_sweep.json and .md.   python tools/sweep.py [tag] [max_log2n] [dd|ts]
+(ts: the paper's triple-single working precision, SURVEY f4 -- the setting of its counts)
 (TEST / EVIDENCE tooling: it uses oracle/ only for the float128 reference.)"""
 import json
 import os
@@ -28,6 +29,7 @@ import workloads  # noqa: E402
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 max_log = int(sys.argv[2]) if len(sys.argv) > 2 else 18
+prec = sys.argv[3] if len(sys.argv) > 3 else "dd"
 KL = [(8, 1), (1, 1), (2, 1), (3, 1), (3, 3)]
 PHIS = [0.0, 1.0, 4.0]
 B = 4
@@ -57,14 +59,20 @@ for phi in PHIS:
         x = workloads.phi_input(n, phi, seed=lg * 10 + int(phi), batch=B)
         xt = torch.from_numpy(x).cuda()
         for K, L in KL:
-            plan = oz.Plan(n, B, K=K, L=L)
-            y = plan.forward(xt).cpu().numpy()
-            st = plan.stats()
-            per = (st["fwd_ntts"] + st["inv_ntts"]) / B
-            mx, l2, nb = errors(y[0], x[0])
-            rows.append({"phi": phi, "n": n, "K": "inf(8)" if K == 8 else K, "L": L,
-                         "alpha": plan.alpha, "k_x": st["k"][:2], "k_w": st["k"][2:],
-                         "ntt_total": per + st["cached_ntts"], "ntt_runtime": per,
+            plan = oz.Plan(n, 1, K=K, L=L, precision=prec)
+            per_t, kx = [], []
+            for b in range(B):  # one transform at a time: per-transform counts (the paper's max)
+                yb = plan.forward(xt[b:b + 1].contiguous()).cpu().numpy()
+                st = plan.stats()
+                per_t.append(st["fwd_ntts"] + st["inv_ntts"] + st["cached_ntts"])
+                kx.append(st["k"][:2])
+                if b == 0:
+                    y0 = yb[0]
+            mx, l2, nb = errors(y0, x[0])
+            rows.append({"phi": phi, "n": n, "K": "inf(8)" if K == 8 else K, "L": L, "precision": prec,
+                         "alpha": plan.alpha, "k_x": kx[0], "k_x_all": kx, "k_w": st["k"][2:],
+                         "ntt_total": max(per_t), "ntt_per_transform": per_t,
+                         "ntt_runtime": max(per_t) - st["cached_ntts"],
                          "max_rel_err": mx, "rel_l2_err": l2, "bins": nb})
             print(json.dumps(rows[-1]), flush=True)
             del plan
@@ -72,12 +80,16 @@ alpha = {1 << k: O.alpha_formulas(1 << k) for k in range(10, 21)}
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
 json.dump({"rows": rows, "alpha_fig1": alpha}, open(os.path.join(ROOT, "profiles", f"{tag}_sweep.json"), "w"),
           indent=1)
-md = [f"# Accuracy / NTT-count sweep ({tag}; tools/sweep.py, one B200)", "",
+md = [f"# Accuracy / NTT-count sweep ({tag}; tools/sweep.py, one B200, precision {prec})", "",
       "Inputs (rand-0.5)exp(phi randn), 4 transforms per point, transform 0 scored against the",
-      "__float128 DFT (all bins for n <= 4096, else 256 seeded bins). Counts are per transform,",
-      "including the cached omega* NTTs (the paper's count). K = inf is the build's cap K = 8.",
-      "Working precision is double-double (DESIGN ruling 1), so split counts and errors are",
-      "not the paper's TS figures; the count laws and the (3,3) / (3,1) totals at phi = 0, 1 are.", "",
+      "__float128 DFT (all bins for n <= 4096, else 256 seeded bins). NTTs = the largest",
+      "per-transform count of the 4 (the paper reports maxima), cached omega* NTTs included;",
+      "k(Re x', Im x') of transform 0. K = inf is the build's cap K = 8.",
+      ("Working precision is double-double (DESIGN ruling 1), so split counts and errors are "
+       "not the paper's TS figures; the count laws and the (3,3) / (3,1) totals at phi = 0, 1 are."
+       if prec == "dd" else
+       "Working precision is the paper's triple-single (SURVEY f4, DESIGN section 15): the "
+       "setting of the paper's counts (P:1112, P:1164-1167)."), "",
       "| phi | n | (K, L) | alpha | k(Re x', Im x') | k(Re w, Im w) | NTTs | max rel err | rel l2 err |",
       "|---|---|---|---|---|---|---|---|---|"]
 for r in rows:
