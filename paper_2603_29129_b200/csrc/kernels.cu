@@ -64,6 +64,11 @@ __device__ __forceinline__ uint32_t mul_shoup(uint32_t a, uint2 w, uint32_t p) {
 // p < 2^31: fold the high word below p (T < 2p 2^32), then the subtractive Montgomery REDC
 // with pinv_pos = +p^{-1} mod 2^32: mq p = tl (mod 2^32), so (T - mq p) / 2^32 = th - hi(mq p)
 // exactly, in (-p, p); one conditional add of p makes it canonical.
+__device__ __forceinline__ uint32_t redc_lazy2(unsigned long long T, uint32_t p, uint32_t pinv_pos) {
+  // T < p 2^32 (at most two products): th < p already
+  const uint32_t d = (uint32_t)(T >> 32) - __umulhi((uint32_t)T * pinv_pos, p);
+  return min(d, d + p);
+}
 __device__ __forceinline__ uint32_t redc_lazy3(unsigned long long T, uint32_t p, uint32_t pinv_pos) {
   uint32_t th = (uint32_t)(T >> 32);
   const uint32_t tl = (uint32_t)T;
@@ -1041,6 +1046,10 @@ __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32
 #ifndef OZ_CI_SNAKE_MAX
 #define OZ_CI_SNAKE_MAX 7
 #endif
+#ifndef OZ_CI_T0S
+#define OZ_CI_T0S 8  // k_col_inv_crt: step-1 round column twiddles staged in shared memory
+#endif  // for log2 R >= this (c3 803 -> 769 us; shorter columns lose: c4 658 -> 715, c2 132 -> 215,
+        // wider column blocks make the table large and the snake order already reuses L1)
 #ifndef OZ_CI_ILP
 #define OZ_CI_ILP 4  // k_col_inv_crt: CRT + DD chains interleaved per batch
 #endif
@@ -1227,12 +1236,6 @@ struct RowParams {
 #ifndef OZ_ROW_NA
 #define OZ_ROW_NA 1
 #endif
-#ifndef OZ_PW_BATCH
-#define OZ_PW_BATCH 1  // pointwise: all W loads of a group (<= 3 pairs) issued up front
-#endif
-#ifndef OZ_ROW_WSMEM
-#define OZ_ROW_WSMEM 0  // two-pass rows: the conv's W rows staged in shared memory
-#endif
 #ifndef OZ_ROW_BULKY
 #define OZ_ROW_BULKY 1  // two-pass rows: Y rows bulk-copied (TMA) into shared memory up front
 #endif
@@ -1252,7 +1255,7 @@ struct RowCfg {
   static constexpr int E = 1 << LOGE;
   static constexpr int threads = LOGC >= LOGE ? (1 << (LOGC - LOGE)) : 1;
 #ifndef OZ_ROW_MINB
-#define OZ_ROW_MINB 6
+#define OZ_ROW_MINB 5  // 96 registers, 5 CTAs/SM (6 at 80 registers: c3 1074 vs 1065 us)
 #endif
   static constexpr int min_blocks = LOGC == 11 ? OZ_ROW_MINB : (LOGC == 10 && TWO_PASS ? 12 : 1);
   // stages of the first DIT round (= last DIF round): its groups are contiguous blocks
@@ -1338,29 +1341,6 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
     }
   }
 #endif
-  // OZ_ROW_WSMEM (two-pass plans): the K cached W rows of the conv being processed live in
-  // shared memory (bulk-copied: conv 0's at the start, conv 1's while conv 0's last inverse
-  // NTT runs), so the pointwise products read W with LDS instead of L2-latency loads
-  constexpr bool kWsm = OZ_ROW_WSMEM && TWO_PASS;
-  uint32_t* const Wsm = smem + ((K * C + padC + 2 * G * tstride + 3) & ~3u);  // [K][C], 16B-aligned
-  __shared__ __align__(8) unsigned long long s_wbar;
-  auto w_rows = [&](int ci) -> const uint32_t* {  // global W rows (t = 0..K-1) of conv ci
-    const int cv = ci ? cv1 : cv0;
-    return P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff;
-  };
-  auto w_copy = [&](int ci) {  // one thread: bulk-copy conv ci's W rows into Wsm
-    fence_proxy_async_smem();  // earlier generic reads of Wsm (ordered by a CTA barrier)
-    mbar_expect_tx(&s_wbar, (uint32_t)K * C * 4u);
-    for (int t = 0; t < K; ++t) bulk_g2s(Wsm + t * C, w_rows(ci) + (size_t)t * m, C * 4u, &s_wbar);
-  };
-  if constexpr (kWsm) {
-    if (threadIdx.x == 0 && !P.fwd_only) {
-      const int ng0 = want0 ? __ldg(&P.sched[(b * 4 + (P.image ? 0 : cv0)) * sched_stride(K, L)]) : 0;
-      mbar_init(&s_wbar, 1);
-      mbar_fence_init();
-      if (ng0 > 0 || want1) w_copy(ng0 > 0 ? 0 : 1);
-    }
-  }
   // one (conv, group) entry per thread, every schedule load independent of the others (the
   // whole table costs one L2 latency; a serial walk over the groups cost ~10 dependent ones)
   for (int it = tv; it < 2 * G && !P.fwd_only; it += blockDim.x) {  // blockDim may be 1 (C < 32)
@@ -1376,13 +1356,13 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
       const uint32_t sx = (uint32_t)__ldg(&grp[2 + 2 * i]), tw = (uint32_t)__ldg(&grp[3 + 2 * i]);
       if (g < ng && i < np) {
         tg[1 + 2 * i] = sx * C;
-        tg[2 + 2 * i] = tw * (kWsm ? C : (uint32_t)m);  // W row offset (shared / global)
+        tg[2 + 2 * i] = tw * (uint32_t)m;  // W row offset
       }
     }
     if (g < ng) tg[0] = (uint32_t)np;
     if (g == 0) s_ng[ci] = ng;
   }
-  if constexpr (TWO_PASS && (OZ_ROW_BULKY || kWsm)) __syncthreads();  // mbarriers initialised
+  if constexpr (TWO_PASS && OZ_ROW_BULKY) __syncthreads();  // mbarriers initialised
   // ---- forward: last log2(C) DIF stages of each slice's NTT (Alg.6 l.787)
   for (int s = 0; s < ka; ++s) {
     uint32_t* xs = Xs + s * C;
@@ -1439,23 +1419,24 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   };
   // pointwise products for this thread's round-0 elements: 64-bit lazy sums of up to 3
   // products X * W~ (W~ = W m^{-1} 2^32, sums < 3 p^2 < 2^64), one Montgomery reduction each
-  auto wld = [&](const uint32_t* w) -> uint32_t {
-    if constexpr (kWsm) return *w;
-    else return ldg_stream(w);
+  auto wld = [&](const uint32_t* w) -> uint32_t { return ldg_stream(w); };
+  auto load_w0 = [&](int ci, int g, uint32_t (&w)[E]) {  // W row of an item's first pair
+    const int cv = ci ? cv1 : cv0;
+    const uint32_t* wr0 = P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff +
+                          tab[(ci * G + g) * tstride + 2];
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) w[i] = wld(&wr0[row_slot<LOGC, TWO_PASS>(tv, i)]);
   };
   auto pointwise = [&](int ci, int g, uint32_t (&z)[E]) {
     const int cv = ci ? cv1 : cv0;
-    const uint32_t* Wb = kWsm ? Wsm : P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff;
+    const uint32_t* Wb = P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff;
     const uint32_t* tg = tab + (ci * G + g) * tstride;
     const int np = (int)tg[0];
-    if constexpr (kWsm) mbar_wait(&s_wbar, ci == 1 && s_ng[0] > 0 ? 1u : 0u);
-#if OZ_PW_BATCH
     if (np <= 3) {  // (L <= 3 always): the W loads of two pairs in flight ahead of the
-                    // products (one L2 latency per group instead of one per pair)
-      uint32_t w0[CNT], w1[CNT];
-      const uint32_t* wr0 = Wb + tg[2];
-#pragma unroll
-      for (int i = 0; i < CNT; ++i) w0[i] = wld(&wr0[row_slot<LOGC, TWO_PASS>(tv, i)]);
+                    // products (one L2 latency per group instead of one per pair; loading the
+                    // next item's W during this item's NTT measured slower -- registers)
+      uint32_t w0[E], w1[E];
+      load_w0(ci, g, w0);
       if (np > 1) {
         const uint32_t* wr1 = Wb + tg[4];
 #pragma unroll
@@ -1480,11 +1461,15 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
 #pragma unroll
         for (int i = 0; i < CNT; ++i) T[i] += (unsigned long long)x2[row_slot<LOGC, TWO_PASS>(tv, i)] * w0[i];
       }
+      if (np == 3) {
 #pragma unroll
-      for (int i = 0; i < CNT; ++i) z[i] = redc_lazy3(T[i], p, pinv);
+        for (int i = 0; i < CNT; ++i) z[i] = redc_lazy3(T[i], p, pinv);
+      } else {  // T < 2 p^2 < p 2^32: the high word is already below p
+#pragma unroll
+        for (int i = 0; i < CNT; ++i) z[i] = redc_lazy2(T[i], p, pinv);
+      }
       return;
     }
-#endif
 #pragma unroll
     for (int i = 0; i < E; ++i) z[i] = 0;
     for (int ip0 = 0; ip0 < np; ip0 += 3) {
@@ -1529,12 +1514,6 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
     item(it, ci0, g0);
     uint32_t z[E];
     pointwise(ci0, g0, z);
-    if constexpr (kWsm) {
-      if (it == ng0 - 1 && nitems > ng0) {  // conv 0 done with Wsm: fetch conv 1's rows
-        __syncthreads();
-        if (threadIdx.x == 0) w_copy(1);
-      }
-    }
     uint32_t* const zt = ztap_ptr(ci0, g0);
     uint32_t* const op = out_ptr(ci0, g0);
     sub_ntt<LOGC, true, 1, LOGE, true>(
@@ -1879,10 +1858,18 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   }
   constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;
   double2* Sacc = reinterpret_cast<double2*>(smem + ((TILE + 3) & ~3u));  // [NH][THREADS], 16B-aligned
-  // (staging the step-1 round twiddles in shared memory, as k_col_fwd does, measured slower
-  // here: 833 vs 813 us at c3 -- they already hit L1, shared by the 16 threads of a column)
 #pragma unroll
   for (int i = 0; i < NH; ++i) Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
+  // OZ_CI_T0S: for long columns, the step-1 round's column twiddles of both primes (the same
+  // for every group of the CTA) are staged in shared memory once, after the accumulators (ncu
+  // at c3: the first product of each tile waited on these L2 loads, 13 % of the samples)
+  constexpr int S1 = col_s1(LOGR);
+  constexpr bool kT0S = OZ_CI_T0S != 0 && LOGR >= OZ_CI_T0S;
+  [[maybe_unused]] uint2* tw0 = reinterpret_cast<uint2*>(Sacc + NH * THREADS);  // [2 q][2^S1][Cb]
+  if constexpr (kT0S) {
+    for (int q = 0; q < 2; ++q)
+      stage_col_tw0<S1, Cb>(tw0 + q * (Cb << S1), P.tw + (size_t)(q * 2 + 1) * m, C, cb << LOGCB);
+  }
   const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
   uint32_t nxt[E];
   // tile t -> (group g, prime q): t = 2 g + (q xor snake(g)).  With OZ_CI_SNAKE the primes
@@ -1909,11 +1896,18 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
     const uint32_t p = q ? P.F.p1 : P.F.p0;
     const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
     uint32_t rr[NH];
-    sub_ntt<LOGR, true, Cb, LOGE>(tv, smem + c, col, C, T, p,
-                            [&](int i, uint32_t) -> uint32_t { return cur[i]; },
-                            [&](int i, uint32_t, uint32_t val) {
-                              if (needed(i)) rr[hslot(i)] = val;  // rows >= R/2 never needed
-                            });
+    if constexpr (kT0S)
+      sub_ntt_t0<LOGR, true, Cb, LOGE>(tv, smem + c, col, C, T, Tw0{tw0 + q * (Cb << S1), (uint32_t)c, (uint32_t)Cb}, p,
+                              [&](int i, uint32_t) -> uint32_t { return cur[i]; },
+                              [&](int i, uint32_t, uint32_t val) {
+                                if (needed(i)) rr[hslot(i)] = val;  // rows >= R/2 never needed
+                              });
+    else
+      sub_ntt<LOGR, true, Cb, LOGE>(tv, smem + c, col, C, T, p,
+                              [&](int i, uint32_t) -> uint32_t { return cur[i]; },
+                              [&](int i, uint32_t, uint32_t val) {
+                                if (needed(i)) rr[hslot(i)] = val;  // rows >= R/2 never needed
+                              });
     if (P.res_tap) {
       uint32_t* rt = P.res_tap + (((b * 4 + cv) * 2 + q) * G + g) * P.n + col;
 #pragma unroll
@@ -2373,7 +2367,6 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   const int rle = row_loge(pl.logC, pl.logR > 0);
   const size_t padC = C + (C >> rle) + 1;
   c.row_smem = ((size_t)pl.K * C + padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
-  if (OZ_ROW_WSMEM && pl.logR > 0) c.row_smem = ((c.row_smem + 15) & ~(size_t)15) + (size_t)pl.K * C * 4;
   c.row_threads = pl.logC >= rle ? (1 << (pl.logC - rle)) : 1;  // exactly Tv: every thread active
   return c;
 }
@@ -2667,7 +2660,9 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     const size_t tile = ((1ull << pl.logR) + ((1ull << pl.logR) >> cle) + 1) * (1ull << lcb);
     const bool prune = 2 * n <= m;  // padded plans; cyclic plans (m = n) need every row
     const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / (prune ? 2 : 1);
-    const size_t smem = ((tile + 3) & ~(size_t)3) * 4 + (size_t)nh * threads * 16 * (pl.image ? 2 : 1);
+    const size_t smem = ((tile + 3) & ~(size_t)3) * 4 + (size_t)nh * threads * 16 * (pl.image ? 2 : 1) +
+                        (!pl.image && OZ_CI_T0S && pl.logR >= OZ_CI_T0S
+                             ? (size_t)2 * ((size_t)1 << col_s1(pl.logR)) * ((size_t)1 << lcb) * 8 : 0);
     const int64_t nblk = (1ll << (pl.logC - lcb)) * nb * (pl.image ? 1 : 4);
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
     dispatch_rc(pl.logR, pl.logC, [&](auto I, auto J) {
