@@ -180,7 +180,7 @@ def run_reference(args, cfg, rank, world):
               f"({'fwd+inv' if cfg.roundtrip else 'fwd'}), OpenMP over transforms")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64+u64", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "n": cfg.n, "batch": cfg.batch, "K": 3,
                        "L": 3, "impl": "CPU oracle (oracle/ozfft_oracle.c)"},

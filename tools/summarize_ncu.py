@@ -66,13 +66,29 @@ raw_keys = ["sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
             "sm__inst_executed.avg.per_cycle_active",
             "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+def pages(f):
+    """(details, raw, source CSV path) of a capture: an .ncu-rep, or its CSV pages exported on
+    the box by tools/ncu_full_csv.sh (<name>_details.csv, _raw.csv, _sass.csv)."""
+    if f.endswith(".ncu-rep"):
+        rep = os.path.join(ev, f)
+        det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        name = f.replace(".ncu-rep", "")
+        src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                             capture_output=True, text=True).stdout
+        tmp = os.path.join(ev, name + "_sass.csv")
+        open(tmp, "w").write(src)
+        return name, det, raw, tmp
+    name = f[:-len("_details.csv")]
+    return (name, open(os.path.join(ev, f)).read(), open(os.path.join(ev, name + "_raw.csv")).read(),
+            os.path.join(ev, name + "_sass.csv"))
+
+
 for f in sorted(os.listdir(ev)):
-    if not f.endswith(".ncu-rep"):
+    if not (f.endswith(".ncu-rep") or f.endswith("_details.csv")):
         continue
-    rep = os.path.join(ev, f)
-    det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    out = [f"# {f} ({tag})", ""]
+    name, det, raw, tmp = pages(f)
+    out = [f"# {name} ({tag})", ""]
     r = list(csv.reader(det.splitlines()))
     h = r[0]
     for row in r[1:]:
@@ -95,11 +111,6 @@ for f in sorted(os.listdir(ev)):
     out.append("\nwarp stall samples (share):")
     for x, k in sorted(stalls, reverse=True)[:10]:
         out.append(f"  {x / s:6.3f} {k}")
-    name = f.replace(".ncu-rep", "")
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
-    tmp = os.path.join(ev, name + "_sass.csv")
-    open(tmp, "w").write(src)
     hot = subprocess.run([sys.executable, os.path.join(root, "tools", "sass_hot.py"), tmp, "15"],
                          capture_output=True, text=True).stdout
     out.append("\nSASS opcode mix and hottest instructions (tools/sass_hot.py):")
