@@ -151,6 +151,27 @@ __device__ __forceinline__ void dd_mul_d(double ah, double al, double b, double&
   fast_two_sum(p, e, rh, rl);
 }
 
+#ifndef OZ_CVT32
+#define OZ_CVT32 1  // CRT integers to scaled double-doubles through 32-bit conversions
+#endif
+// (RN(Z) sc, (Z - RN(Z)) sc) for an exact integer Z and a power of two sc (Alg.8 l.975: z' / c
+// as a double-double, no rounding beyond RN(Z)).  OZ_CVT32: from the two 32-bit halves,
+// a = hi32(Z) 2^32 sc and b = lo32(Z) sc are exact, RN(a + b) = RN(Z) sc and FastTwoSum's
+// error term is (Z - RN(Z)) sc exactly (|a| >= |b| or a = 0) -- the same two doubles as the
+// 64-bit conversions (I2F.F64.S64, F2I.S64.F64, I2F.F64.S64), with 32-bit conversions.
+__device__ __forceinline__ void scaled_split(long long Z, double sc, double& hs, double& ls) {
+#if OZ_CVT32
+  const double a = __dmul_rn((double)(int)(Z >> 32), __dmul_rn(sc, 4294967296.0));
+  const double b = __dmul_rn((double)(unsigned)Z, sc);
+  fast_two_sum(a, b, hs, ls);
+#else
+  const double h = __ll2double_rn(Z);
+  const double l = __ll2double_rn(Z - __double2ll_rz(h));
+  hs = __dmul_rn(h, sc);
+  ls = __dmul_rn(l, sc);
+#endif
+}
+
 // ============================================================== triple-single (TS, f4)
 // x0 + x1 + x2 in fp32 words.  The op sequences are this build's reading of
 // TSAdd / TSMul (DESIGN ruling 24) and must match oracle/ozfft_oracle.c op for op.
@@ -1637,10 +1658,9 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
           const int g = g0 + i;
           const long long Z = garner2(z0[i], z1[i], P);
           if (P.crt_tap) P.crt_tap[((b * 4 + cv) * G + g) * P.n + j] = Z;
-          const double h = __ll2double_rn(Z);
-          const double l = __ll2double_rn(Z - __double2ll_rz(h));
-          const double sc = s_sc[cv][g];  // z' / c, exact power of two (l.975)
-          dd_add(sh, sl, __dmul_rn(h, sc), __dmul_rn(l, sc), sh, sl);  // flush order (l.976)
+          double hs, ls;
+          scaled_split(Z, s_sc[cv][g], hs, ls);  // z' / c, c an exact power of two (l.975)
+          dd_add(sh, sl, hs, ls, sh, sl);          // flush order (l.976)
         }
       }
     }
@@ -1766,9 +1786,9 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish_img(FinishParams P) {
     for (int part = 0; part < 2; ++part) {
       const long long Z = part ? garner2(zi[0], zi[1], P) : garner2(zr[0], zr[1], P);
       if (P.crt_tap) P.crt_tap[((b * 4 + part) * G + g) * P.n + j] = Z;
-      const double h = __ll2double_rn(Z);
-      const double l = __ll2double_rn(Z - __double2ll_rz(h));
-      dd_add(sh[part], sl[part], __dmul_rn(h, sc), __dmul_rn(l, sc), sh[part], sl[part]);
+      double hs, ls;
+      scaled_split(Z, sc, hs, ls);
+      dd_add(sh[part], sl[part], hs, ls, sh[part], sl[part]);
     }
   }
   const double2 w = P.chirp[j];
@@ -1955,9 +1975,9 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
             if constexpr (TS) {  // f4: TSAdd of z 2^-cexp (slot holds the TS words)
               acc[j] = ts_accum(acc[j], Z[j], s_ce[g]);
             } else {
-              const double hi = __ll2double_rn(Z[j]);
-              const double lo = __ll2double_rn(Z[j] - __double2ll_rz(hi));
-              dd_add(acc[j].x, acc[j].y, __dmul_rn(hi, sc), __dmul_rn(lo, sc), acc[j].x, acc[j].y);
+              double hs, ls;
+              scaled_split(Z[j], sc, hs, ls);
+              dd_add(acc[j].x, acc[j].y, hs, ls, acc[j].x, acc[j].y);
             }
           }
 #pragma unroll
@@ -2078,10 +2098,10 @@ __global__ void __launch_bounds__(256, 2) k_col_inv_crt_img(ColCrtParams P) {
           for (int part = 0; part < 2; ++part) {
             const long long Z = part ? garner2(zi0[h], zi1, P.F) : garner2(zr0[h], zr1, P.F);
             if (P.crt_tap) P.crt_tap[((b * 4 + part) * G + g) * P.n + col + e * C] = Z;
-            const double hi = __ll2double_rn(Z);
-            const double lo = __ll2double_rn(Z - __double2ll_rz(hi));
+            double hs, ls;
+            scaled_split(Z, sc, hs, ls);
             double2 a = Sacc[(part * NH + h) * THREADS + tid];
-            dd_add(a.x, a.y, __dmul_rn(hi, sc), __dmul_rn(lo, sc), a.x, a.y);
+            dd_add(a.x, a.y, hs, ls, a.x, a.y);
             Sacc[(part * NH + h) * THREADS + tid] = a;
           }
         }
