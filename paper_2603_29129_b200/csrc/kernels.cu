@@ -1257,6 +1257,9 @@ struct RowParams {
 #ifndef OZ_ROW_NA
 #define OZ_ROW_NA 1
 #endif
+#ifndef OZ_ROW_FWD3
+#define OZ_ROW_FWD3 1  // two-pass rows with three slices: the forward NTTs as one NV = 3 pass
+#endif
 #ifndef OZ_ROW_BULKY
 #define OZ_ROW_BULKY 1  // two-pass rows: Y rows bulk-copied (TMA) into shared memory up front
 #endif
@@ -1334,10 +1337,13 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   const bool want1 = !P.image && ((P.unit_mask >> (cv1 * 2 + q)) & 1u);
   if (!P.fwd_only && !want0 && !want1) return;
   if (ka == 0 && !P.fwd_only) return;  // no slices: the schedule has no groups here
-  uint32_t* Xs = smem;               // [K][C] forward spectra rows (row_perm order)
+  // [K][XS] forward spectra rows (row_perm order); two-pass rows are XS = C + C/16 + 4 words
+  // apart (the padded exchange layout of the three-slice forward fits in place, 16B-aligned)
+  constexpr uint32_t XS = TWO_PASS ? C + (C >> 4) + 4 : C;
+  uint32_t* Xs = smem;
   // [padC]: inter-round exchange buffer; a CTA barrier before each sub-transform frees it
   // (double buffering, which would drop that barrier, measured slower: more registers)
-  uint32_t* work = smem + K * C;
+  uint32_t* work = smem + K * XS;
   // group table for 2 convs x K*K groups: npairs, then (X row offset, W row offset) x L
   uint32_t* tab = work + padC;
   const int tstride = 1 + 2 * L;
@@ -1357,7 +1363,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
       mbar_fence_init();
       for (int s = 0; s < ka; ++s) {
         mbar_expect_tx(&s_ybar[s], C * 4u);
-        bulk_g2s(Xs + s * C, P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff, C * 4u, &s_ybar[s]);
+        bulk_g2s(Xs + s * XS, P.Y + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff, C * 4u, &s_ybar[s]);
       }
     }
   }
@@ -1376,7 +1382,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
     for (int i = 0; i < L; ++i) {
       const uint32_t sx = (uint32_t)__ldg(&grp[2 + 2 * i]), tw = (uint32_t)__ldg(&grp[3 + 2 * i]);
       if (g < ng && i < np) {
-        tg[1 + 2 * i] = sx * C;
+        tg[1 + 2 * i] = sx * XS;
         tg[2 + 2 * i] = tw * (uint32_t)m;  // W row offset
       }
     }
@@ -1385,12 +1391,51 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   }
   if constexpr (TWO_PASS && OZ_ROW_BULKY) __syncthreads();  // mbarriers initialised
   // ---- forward: last log2(C) DIF stages of each slice's NTT (Alg.6 l.787)
-  for (int s = 0; s < ka; ++s) {
-    uint32_t* xs = Xs + s * C;
+  int s_begin = 0;
+#if OZ_ROW_FWD3
+  if constexpr (TWO_PASS && OZ_ROW_BULKY) {
+    if (ka == 3) {
+      // The three slices together (sub_ntt_multi, NV = 3): one twiddle load per butterfly
+      // position serves the three vectors, three independent butterflies per position, and
+      // the whole forward takes three CTA barriers instead of six.  The exchange runs in
+      // place in each slice's own XS-word row (padded layout): Y[s] is read into registers
+      // first (barrier), and X[s] is written in row_perm order after the last round's reads
+      // (barrier).
+      constexpr int CNT0 = RoundT<LOGC, false, 0, LOGE>::cnt;
+      uint32_t yv[3][E];
+#pragma unroll
+      for (int v = 0; v < 3; ++v) {
+        mbar_wait(&s_ybar[v], 0u);
+#pragma unroll
+        for (int i = 0; i < CNT0; ++i) yv[v][i] = Xs[v * XS + round_elem<LOGC, false, 0, LOGE>(tv, i)];
+      }
+      __syncthreads();  // every Y read done before the in-place exchange writes
+      uint32_t* const sms[3] = {Xs, Xs + XS, Xs + 2 * XS};
+      uint32_t* const outX = P.Xout && blockIdx.z == 0 ? P.Xout + (((b * 2 + q) * 2 + a) * K) * m + rowoff
+                                                      : nullptr;  // tap / plan-time spectra
+      uint32_t xv[3][E];
+      sub_ntt_multi<LOGC, false, 1, 3, LOGE, true, false>(
+          tv, sms, 0u, 1u, Tf, Tw0{nullptr, 0u, 0u}, p,
+          [&](int v, int i, uint32_t) -> uint32_t { return yv[v][i]; },
+          [&](int v, int i, uint32_t e, uint32_t val) {
+            xv[v][i] = val;
+            if (outX) outX[(size_t)v * m + e] = val;
+          });
+      __syncthreads();  // every last-round read done before X overwrites the rows
+#pragma unroll
+      for (int v = 0; v < 3; ++v)
+#pragma unroll
+        for (int i = 0; i < CNT0; ++i) Xs[v * XS + row_slot<LOGC, TWO_PASS>(tv, i)] = xv[v][i];
+      s_begin = 3;
+    }
+  }
+#endif
+  for (int s = s_begin; s < ka; ++s) {
+    uint32_t* xs = Xs + s * XS;
     uint32_t* outX = P.Xout && blockIdx.z == 0 ? P.Xout + (((b * 2 + q) * 2 + a) * K + s) * m + rowoff
                                               : nullptr;
     uint32_t* wk = work;
-    if (s > 0) __syncthreads();  // `work` free (previous last reads done)
+    if (s > s_begin) __syncthreads();  // `work` free (previous last reads done)
     auto store_x = [&](int i, uint32_t e, uint32_t v) {
       xs[row_slot<LOGC, TWO_PASS>(tv, i)] = v;  // == row_perm(e)
       if (outX) outX[e] = v;
@@ -2386,7 +2431,8 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   const size_t C = 1ull << pl.logC;
   const int rle = row_loge(pl.logC, pl.logR > 0);
   const size_t padC = C + (C >> rle) + 1;
-  c.row_smem = ((size_t)pl.K * C + padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
+  const size_t XS = pl.logR > 0 ? C + (C >> 4) + 4 : C;  // X row stride (k_row_fused)
+  c.row_smem = ((size_t)pl.K * XS + padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
   c.row_threads = pl.logC >= rle ? (1 << (pl.logC - rle)) : 1;  // exactly Tv: every thread active
   return c;
 }
