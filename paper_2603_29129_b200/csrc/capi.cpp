@@ -261,6 +261,10 @@ ozfft_status ozfft_plan_create(const ozfft_plan_desc* d, ozfft_plan** out) {
     pl->fault = std::atoi(t) != 0;
   if (const char* t = std::getenv("OZFFT_SPLIT_CLUSTER_MAXLEN"))  // knob (tests/tools): 0 = off
     pl->split_cluster_max = std::atoll(t);
+  if (const char* t = std::getenv("OZFFT_SMALL_FUSED"))  // knob (tests/tools): 0 = three-kernel path
+    pl->small_fused = std::atoi(t) != 0;
+  if (const char* t = std::getenv("OZFFT_SMALL_Z"))  // knob (tools/): 1, 2 or 4
+    pl->small_z = std::atoi(t) == 1 || std::atoi(t) == 2 || std::atoi(t) == 4 ? std::atoi(t) : 0;
   // image mode: a real output sums L n complex products (|Re| <= 2 4^alpha each)
   pl->alpha = compute_alpha(pl->image ? 2 * desc.n : desc.n, desc.L, p0, p1);
   if (pl->alpha < 1) {

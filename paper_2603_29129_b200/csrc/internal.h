@@ -38,6 +38,8 @@ struct Plan {
   uint32_t iota[2] = {0, 0};         // image mode: iota_q = g^((p_q - 1)/4), iota^2 = -1
   int device = 0;
   uint64_t max_ws = 0;
+  int small_fused = 1;               // one-launch path of one-pass plans (env OZFFT_SMALL_FUSED=0: off)
+  int small_z = 0;                   // its CTAs per (prime, part) (env OZFFT_SMALL_Z; 0: build default)
   int fault = 0;                     // test-only (env OZFFT_FAULT_INJECT at create): corrupt one residue
   // host tables (built at create)
   std::vector<double> chirp;       // [n][2] = (C_j, S_j), omega(j) = C_j + i S_j

@@ -254,12 +254,18 @@ template <bool TS>
 struct SplitC {
   std::conditional_t<TS, float, double> sigma, scale;
 };
+// 2^e exactly: the exponent field directly in the normal range (scalbn costs ~84 clocks
+// of dependent FP64 work on B200, and the small-transform kernel computes these per level)
+__device__ __forceinline__ double pow2_exact(int e) {
+  if (e >= -1022 && e <= 1023) return __longlong_as_double((long long)(e + 1023) << 52);
+  return scalbn(1.0, e);
+}
 template <bool TS>
 __device__ __forceinline__ SplitC<TS> split_c(int E, int alpha, int rho) {
   if constexpr (TS)
     return SplitC<TS>{ldexpf(1.0f, E + rho), ldexpf(1.0f, alpha - E)};
   else
-    return SplitC<TS>{scalbn(1.0, E + rho), scalbn(1.0, alpha - E)};
+    return SplitC<TS>{pow2_exact(E + rho), pow2_exact(alpha - E)};
 }
 __device__ __forceinline__ int32_t split_step_ts(TSv& r, SplitC<true> c) {
   const float sigma = c.sigma;
@@ -448,9 +454,10 @@ __global__ void __launch_bounds__(256) k_split_max(SplitParams P, int level) {
 // Alg.8 flush schedule for one real convolution; writes the row layout
 // [ngroups, (cexp, npairs, s0, t0, ..., s_{L-1}, t_{L-1}) x K*K].
 __device__ void alg8_schedule(int kx, const int* sx, int ky, const int* sy, int K, int L,
-                              int32_t* row) {
+                              int32_t* row, bool prezeroed = false) {
   const int stride = 1 + K * K * (2 + 2 * L);
-  for (int i = 0; i < stride; ++i) row[i] = 0;
+  if (!prezeroed)
+    for (int i = 0; i < stride; ++i) row[i] = 0;
   if (kx <= 0 || ky <= 0) return;
   int ng = 0;
   int c = sx[kx - 1] + sy[ky - 1];
@@ -483,7 +490,7 @@ __device__ void alg8_schedule(int kx, const int* sx, int ky, const int* sy, int 
 // write the stats row and the four Alg.8 schedules.
 __device__ __forceinline__ bool split_exponents(const SplitParams& P, int64_t b,
                                                 const unsigned long long* mub, int (&E)[2][kMaxK],
-                                                int (&kv)[2], bool lead) {
+                                                int (&kv)[2], bool lead, bool prezeroed = false) {
   bool bad = false;
   for (int v = 0; v < 2; ++v) {
     kv[v] = P.K;
@@ -517,7 +524,7 @@ __device__ __forceinline__ bool split_exponents(const SplitParams& P, int64_t b,
     }
     // image mode: one complex schedule in row 0 (both parts share E), rows 1-3 empty
     alg8_schedule(bad || (P.shared && cv > 0) ? 0 : kv[a], sx, kw, sy, P.K, P.L,
-                  P.sched + (b * 4 + cv) * sched_stride(P.K, P.L));
+                  P.sched + (b * 4 + cv) * sched_stride(P.K, P.L), prezeroed);
   }
   return bad;
 }
@@ -876,7 +883,7 @@ struct Tw0 {
 };
 
 template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, bool ZHI,
-          class LoadF, class StoreF>
+          bool TGEN, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int tv,
                                               uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
@@ -905,9 +912,9 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
       else
         dif_group<RT::S, NV, E, false, true, zhi>(x, u * (1 << RT::S), t0.gb, t0.gs, t0.T, p);
     } else if constexpr (INV) {
-      dit_group<RT::S, NV, E, unit>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+      dit_group<RT::S, NV, E, unit, TGEN>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     } else {
-      dif_group<RT::S, NV, E, unit, false, zhi>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+      dif_group<RT::S, NV, E, unit, TGEN, zhi>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     }
   }
 #pragma unroll
@@ -928,17 +935,16 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
 }
 
 template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, bool ZHI,
-          class LoadF, class StoreF>
+          bool TGEN, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int tv,
                                                uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                                uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
                                                uint32_t p, LoadF& load_first, StoreF& store_last) {
   if constexpr (R < RoundT<LOGN, INV, 0, LOGE>::nr) {
-    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE, UNIT, T0S, ZHI>(x, tv, sm, gb_mod, gs, T, t0, p,
-                                                         load_first, store_last);
-    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE, UNIT, T0S, ZHI>(x, tv, sm, gb_mod, gs, T, t0, p,
-                                                              load_first,
-                                                   store_last);
+    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE, UNIT, T0S, ZHI, TGEN>(x, tv, sm, gb_mod, gs, T, t0, p,
+                                                               load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE, UNIT, T0S, ZHI, TGEN>(x, tv, sm, gb_mod, gs, T, t0, p,
+                                                                    load_first, store_last);
   }
 }
 
@@ -953,7 +959,7 @@ __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int
 // consumes the final values.  The buffers must be free for writes on entry.  UNIT: the
 // caller passes gb_mod == 0 and gs == 1 (rows), enabling the compile-time step-1 round.
 template <int LOGN, bool INV, int CB, int NV, int LOGE = 4, bool UNIT = false, bool T0S = false,
-          bool ZHI = false, class LoadF, class StoreF>
+          bool ZHI = false, bool TGEN = false, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
                                               uint32_t p, LoadF&& load_first, StoreF&& store_last) {
@@ -963,18 +969,20 @@ __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV],
       for (int v = 0; v < NV; ++v) store_last(v, 0, 0u, load_first(v, 0, 0u));
   } else {
     uint32_t x[NV][1 << LOGE];
-    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE, UNIT, T0S, ZHI>(x, tv, sm, gb_mod, gs, T, t0, p,
-                                                          load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE, UNIT, T0S, ZHI, TGEN>(x, tv, sm, gb_mod, gs, T, t0, p,
+                                                                load_first, store_last);
   }
 }
 
-// Single-vector form: load_first(i, e), store_last(i, e, val).
-template <int LOGN, bool INV, int CB, int LOGE = 4, bool UNIT = false, class LoadF, class StoreF>
+// Single-vector form: load_first(i, e), store_last(i, e, val).  TGEN: T may point to shared
+// memory (generic loads instead of the read-only global path).
+template <int LOGN, bool INV, int CB, int LOGE = 4, bool UNIT = false, bool TGEN = false, class LoadF,
+          class StoreF>
 __device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, uint32_t gb_mod,
                                         uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                         LoadF&& load_first, StoreF&& store_last) {
   uint32_t* const sms[1] = {sm};
-  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, UNIT, false>(
+  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, UNIT, false, false, TGEN>(
       tv, sms, gb_mod, gs, T, Tw0{nullptr, 0u, 0u}, p,
       [&](int, int i, uint32_t e) { return load_first(i, e); },
       [&](int, int i, uint32_t e, uint32_t v) { store_last(i, e, v); });
@@ -1657,6 +1665,29 @@ __device__ __forceinline__ long long garner2(uint32_t z0, uint32_t z1, const Fin
   return Zp > P.halfP ? (long long)(Zp - P.P) : (long long)Zp;
 }
 
+// y' = (S_rr - S_ii) + i (S_ir + S_ri) from the four convolutions' DD sums,
+// post-chirp y = y' (.) omega (Alg.4 l.480-484), fp64; inverse direction: conj and RN
+// division by n (O10).  One operation sequence for every kernel that finishes a transform.
+__device__ __forceinline__ double2 dd_combine_postchirp(double2 rr, double2 ii, double2 ir, double2 ri,
+                                                        double2 w, int direction, int64_t n) {
+  double yrh, yrl, yih, yil;
+  dd_add(rr.x, rr.y, -ii.x, -ii.y, yrh, yrl);  // rr - ii
+  dd_add(ir.x, ir.y, ri.x, ri.y, yih, yil);    // ir + ri
+  double a1h, a1l, a2h, a2l, ore, oim, tmp;
+  dd_mul_d(yrh, yrl, w.x, a1h, a1l);
+  dd_mul_d(yih, yil, w.y, a2h, a2l);
+  dd_add(a1h, a1l, -a2h, -a2l, ore, tmp);
+  dd_mul_d(yrh, yrl, w.y, a1h, a1l);
+  dd_mul_d(yih, yil, w.x, a2h, a2l);
+  dd_add(a1h, a1l, a2h, a2l, oim, tmp);
+  if (direction > 0) {
+    const double dn = (double)n;
+    ore = __ddiv_rn(ore, dn);
+    oim = __ddiv_rn(-oim, dn);
+  }
+  return make_double2(ore, oim);
+}
+
 // CTA = 64 outputs x 4 real convolutions: thread (cv, jl) forms conv cv's DD sum of
 // output j (Garner + scaled sum in flush order), then the cv = 0 threads combine the four
 // sums and post-chirp.  (The four per-conv chains are independent: one thread per conv
@@ -1720,31 +1751,8 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish(FinishParams P) {
     P.out[b * P.n + j] = o;
     return;
   }
-  double Sh[4], Sl[4];
-#pragma unroll
-  for (int cv = 0; cv < 4; ++cv) {
-    Sh[cv] = s_S[cv][jl].x;
-    Sl[cv] = s_S[cv][jl].y;
-  }
-  double yrh, yrl, yih, yil;
-  dd_add(Sh[0], Sl[0], -Sh[1], -Sl[1], yrh, yrl);  // rr - ii
-  dd_add(Sh[2], Sl[2], Sh[3], Sl[3], yih, yil);    // ir + ri
-  const double2 w = P.chirp[j];
-  double a1h, a1l, a2h, a2l, ore, oim, tmp;
-  dd_mul_d(yrh, yrl, w.x, a1h, a1l);
-  dd_mul_d(yih, yil, w.y, a2h, a2l);
-  dd_add(a1h, a1l, -a2h, -a2l, ore, tmp);
-  dd_mul_d(yrh, yrl, w.y, a1h, a1l);
-  dd_mul_d(yih, yil, w.x, a2h, a2l);
-  dd_add(a1h, a1l, a2h, a2l, oim, tmp);
-  if (P.direction > 0) {
-    const double dn = (double)P.n;
-    ore = __ddiv_rn(ore, dn);
-    oim = __ddiv_rn(-oim, dn);
-  }
-  o.x = ore;
-  o.y = oim;
-  P.out[b * P.n + j] = o;
+  P.out[b * P.n + j] = dd_combine_postchirp(s_S[0][jl], s_S[1][jl], s_S[2][jl], s_S[3][jl], P.chirp[j],
+                                            P.direction, P.n);
 }
 
 // f4, single-pass plans: Garner per group, z 2^-cexp accumulated with TSAdd in flush order
@@ -1853,6 +1861,370 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish_img(FinishParams P) {
   o.y = oim;
   P.out[b * P.n + j] = o;
 }
+
+// ============================================================== one-launch small transform
+// One-pass plans (R = 1, 2^8 <= m = C <= 2^12), default mode (DD, four real convolutions):
+// the whole path of ONE transform -- split (a1, a2), the forward NTTs (a3), pointwise
+// products + NTT-domain accumulation (a4), inverse NTTs (a5), Garner (a6) and the scaled DD
+// sums + post-chirp (a7) -- in ONE launch.  One thread-block cluster of 4 Z CTAs per
+// transform; CTA rank = (q * 2 + a) * Z + z owns prime q, x' part a and every Z-th
+// (conv, group) item of the two convolutions that use part a (as the one-pass row kernel's
+// gridDim.z split).  Every CTA splits the whole transform itself (n <= 2^11 elements: the
+// K + 1 passes need a block reduction each, no cluster barrier), keeps its part's digits,
+// the K forward spectra and its items' residues in shared memory; one cluster barrier
+// publishes the residues and the Garner + DD sums read the partner prime's residues through
+// distributed shared memory.  Every value goes through the operation sequence of the
+// multi-kernel path (k_split_cluster, k_row_fused, k_crt_finish), so the output is bitwise
+// that path's.  (a fused kernel for the latency-bound small sizes.)
+// Latency notes (B200, tools/microbench_fp64.cu): a dependent DADD / DFMA costs ~25 clocks,
+// so the split processes up to 4 elements per thread as interleaved chains, and the prime's
+// twiddles and the part's W rows are bulk-copied (TMA) into shared memory at the start, where
+// they land while the split runs.
+struct SmallParams {
+  const double2* x;      // [nb][n]
+  const double2* chirp;  // [n]
+  double2* out;          // [nb][n]
+  int64_t n;
+  int K, L, alpha, rho, conj, direction;
+  uint32_t p[2], pinv[2];
+  const uint2* tw;          // [2 prime][2 dir][m]
+  const uint32_t* W;        // [2 q][2 b][K][m] Montgomery W m^{-1} 2^32, row_perm(., logC, w_s0)
+  int w_s0;
+  const int32_t* wsplit;    // kw[2], Ew[2][K]
+  FinishParams F;           // Garner constants
+  unsigned long long* mu;   // [nb][2][K]  (written by rank 0, as the split kernels leave them)
+  int32_t* stats;           // [nb][stats_stride]
+  int32_t* sched;           // [nb][4][sched_stride]
+  int Z;                    // CTAs per (prime, part)
+  int slots;                // residue slots per CTA (>= ceil(items / Z))
+  int stage;                // twiddles + W rows staged in shared memory
+  int fault;                // test-only residue corruption (as k_fault_inject)
+};
+constexpr int kSmallLogE = 3;  // 8 elements per thread and round
+#ifndef OZ_SMALL_EPT
+#define OZ_SMALL_EPT 4
+#endif
+constexpr int kSmallEPT = OZ_SMALL_EPT;  // split: elements per thread interleaved
+#ifndef OZ_SMALL_TIMING
+#define OZ_SMALL_TIMING 0  // tools/: per-phase %globaltimer stamps of every CTA (debug builds)
+#endif
+#if OZ_SMALL_TIMING
+__device__ unsigned long long g_small_t[64][16];
+#define SMALL_STAMP(k)                                                               \
+  do {                                                                               \
+    if (threadIdx.x == 0 && blockIdx.y == 0) {                                       \
+      unsigned long long t_;                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+      g_small_t[cl.block_rank()][k] = t_;                                            \
+    }                                                                                \
+  } while (0)
+#else
+#define SMALL_STAMP(k) \
+  do {                 \
+  } while (0)
+#endif
+__host__ __device__ constexpr int small_threads(int logC) { return 1 << (logC - kSmallLogE); }
+// dynamic shared memory (32-bit words), in order:
+//   head: sched [4][SS] | stats | wsplit | digits of part a [K][n]
+//   stage (optional): twiddles of prime q [2 dir][m] uint2 | W rows of part a's convs [2 b][K][m]
+//   union: x' of the split [4][n] doubles | (X spectra [K][m] | 3 exchange buffers | residues)
+__host__ __device__ inline size_t small_head_words(int64_t n, int K, int L) {
+  return ((4 * (size_t)sched_stride(K, L) + stats_stride(K) + 2 + 2 * K + (size_t)K * n) + 3) & ~(size_t)3;
+}
+__host__ __device__ inline size_t small_stage_words(int logC, int K) {
+  const size_t m = (size_t)1 << logC;
+  return 4 * m + 2 * (size_t)K * m;
+}
+__host__ __device__ inline size_t small_union_words(int logC, int64_t n, int K, int slots) {
+  const size_t m = (size_t)1 << logC;
+  const size_t ntt = (size_t)K * m + 3 * (m + (m >> kSmallLogE) + 4) + (size_t)slots * n;
+  const size_t split = 8 * (size_t)n;  // four doubles per element
+  return ntt > split ? ntt : split;
+}
+
+template <int LOGC, bool STAGE>
+__global__ void __launch_bounds__(small_threads(LOGC)) k_small_fused(SmallParams P) {
+  constexpr int NT = small_threads(LOGC);
+  constexpr uint32_t m = 1u << LOGC;
+  constexpr uint32_t padm = (m + (m >> kSmallLogE) + 4) & ~3u;
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ unsigned long long s_red[2][NT / 32];
+  __shared__ unsigned long long s_mu[2 * kMaxK];
+  __shared__ double s_sc[4][kMaxK * kMaxK];
+  __shared__ double2 s_S[4][NT / 4];
+  __shared__ __align__(8) unsigned long long s_bar;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int Z = P.Z;
+  const int z = rank % Z, a = (rank / Z) & 1, q = rank / (2 * Z);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t b = blockIdx.y;
+  const int K = P.K, L = P.L;
+  const int nn = (int)P.n;
+  const int SS = sched_stride(K, L);
+  SMALL_STAMP(0);
+  int32_t* s_sched = reinterpret_cast<int32_t*>(smem);  // [4][SS]
+  int32_t* s_stats = s_sched + 4 * SS;
+  int32_t* s_wsplit = s_stats + stats_stride(K);         // [2 + 2K]
+  int32_t* dig = s_wsplit + 2 + 2 * K;                   // [K][n], part a
+  uint32_t* after_head = smem + small_head_words(P.n, K, L);
+  uint2* s_tw = reinterpret_cast<uint2*>(after_head);    // stage: [2 dir][m]
+  uint32_t* s_W = after_head + 4 * m;                    // stage: [2 b][K][m]
+  uint32_t* U = after_head + (STAGE ? small_stage_words(LOGC, K) : 0);
+  double* xp = reinterpret_cast<double*>(U);              // split: h[2][n], l[2][n]
+  uint32_t* X = U;                                        // [K][m], row_perm(., LOGC, 3)
+  uint32_t* work = X + (size_t)K * m;                     // [3][padm]
+  uint32_t* res = work + 3 * padm;                        // [slots][n]
+  const uint32_t p = P.p[q];
+  const uint2* gTf = P.tw + (size_t)(q * 2 + 0) * m;
+  const uint2* gTi = P.tw + (size_t)(q * 2 + 1) * m;
+  const uint32_t* gW = P.W + (size_t)(q * 2) * K * m;    // [2 b][K][m] of prime q
+
+  // ---- stage the prime's twiddles and W rows (TMA bulk copies; they land during the split)
+  if (STAGE && tid == 0) {
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&s_bar, (uint32_t)(4 * m + 2 * K * m) * 4u);
+    bulk_g2s(s_tw, gTf, m * 8u, &s_bar);
+    bulk_g2s(s_tw + m, gTi, m * 8u, &s_bar);
+    for (int r = 0; r < 2 * K; ++r) bulk_g2s(s_W + (size_t)r * m, gW + (size_t)r * m, m * 4u, &s_bar);
+  }
+  for (int i = tid; i < 4 * SS + stats_stride(K); i += NT) s_sched[i] = 0;  // schedules (alg8_schedule
+                                                                             // expects them zeroed), stats
+  if (tid < 2 + 2 * K) s_wsplit[tid] = __ldg(&P.wsplit[tid]);
+
+  // ---- a1 + a2: split of both parts (the k_split_cluster sequence, one CTA, no DSMEM)
+  SplitParams SP{};
+  SP.x = P.x; SP.chirp = P.chirp; SP.len = P.n; SP.mode = 0; SP.conj = P.conj;
+  SP.K = K; SP.alpha = P.alpha; SP.rho = P.rho; SP.L = L; SP.wsplit = s_wsplit;
+  SP.stats = s_stats; SP.sched = s_sched; SP.shared = 0;
+  int kv[2] = {K, K};
+  int Eprev[2] = {0, 0};
+  bool bad = false;
+  for (int level = 0; level <= K; ++level) {
+    SplitC<false> lc[2];
+#pragma unroll
+    for (int v = 0; v < 2; ++v) lc[v] = split_c<false>(Eprev[v], P.alpha, P.rho);
+    unsigned long long m0 = 0, m1 = 0;
+    for (int j0 = tid; j0 < nn; j0 += kSmallEPT * NT) {
+      double h[kSmallEPT][2], l[kSmallEPT][2];
+#pragma unroll
+      for (int u = 0; u < kSmallEPT; ++u) {
+        const int j = min(j0 + u * NT, nn - 1);  // out-of-range slots redo element n - 1
+        if (level == 0) {
+          load_xprime(SP, b, j, h[u][0], l[u][0], h[u][1], l[u][1]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            h[u][v] = xp[v * nn + j];
+            l[u][v] = xp[(2 + v) * nn + j];
+          }
+        }
+      }
+      if (level > 0) {
+#pragma unroll
+        for (int u = 0; u < kSmallEPT; ++u) {
+          const int j = j0 + u * NT;
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            int32_t D = 0;
+            if (level - 1 < kv[v]) D = split_step(h[u][v], l[u][v], lc[v]);
+            if (v == a && j < nn) dig[(level - 1) * nn + j] = D;
+          }
+        }
+      }
+      if (level == K) continue;
+#pragma unroll
+      for (int u = 0; u < kSmallEPT; ++u) {
+        const int j = j0 + u * NT;
+        if (j >= nn) continue;
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          xp[v * nn + j] = h[u][v];
+          xp[(2 + v) * nn + j] = l[u][v];
+        }
+        const unsigned long long a0 = (unsigned long long)__double_as_longlong(fabs(h[u][0]));
+        const unsigned long long a1 = (unsigned long long)__double_as_longlong(fabs(h[u][1]));
+        m0 = a0 > m0 ? a0 : m0;  // NaN bits exceed +Inf bits: a NaN sticks
+        m1 = a1 > m1 ? a1 : m1;
+      }
+    }
+    if (level == K) break;
+    SMALL_STAMP(8 + 2 * level);
+    m0 = warp_max_u64(m0);
+    m1 = warp_max_u64(m1);
+    if (lane == 0) { s_red[0][warp] = m0; s_red[1][warp] = m1; }
+    __syncthreads();
+    SMALL_STAMP(9 + 2 * level);
+    m0 = m1 = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+      m0 = s_red[0][w] > m0 ? s_red[0][w] : m0;
+      m1 = s_red[1][w] > m1 ? s_red[1][w] : m1;
+    }
+    __syncthreads();  // s_red free for the next level
+    if (tid == 0) { s_mu[level] = m0; s_mu[K + level] = m1; }
+    const unsigned long long mv[2] = {m0, m1};
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const unsigned long long u = mv[v];
+      if (u >= kInfBits) bad = true;
+      Eprev[v] = (u == 0 || u >= kInfBits) ? 0 : ceil_log2_bits(u);
+      if (u == 0 && kv[v] == K) kv[v] = level;
+    }
+    if (bad) {  // as k_split_cluster: later levels keep mu = 0
+      for (int k = level + 1; k < K; ++k)
+        if (tid == 0) { s_mu[k] = 0; s_mu[K + k] = 0; }
+      break;
+    }
+  }
+  SMALL_STAMP(14);
+  __syncthreads();
+  int Ef[2][kMaxK], kvf[2];
+  bad = split_exponents(SP, 0, s_mu, Ef, kvf, true, true);  // stats + 4 schedules -> smem
+  __syncthreads();
+  SMALL_STAMP(15);
+  if (rank == 0) {  // the per-transform records the multi-kernel path leaves in the workspace
+    if (tid < 2 * K) P.mu[b * 2 * K + tid] = s_mu[tid];
+    for (int i = tid; i < stats_stride(K); i += NT) P.stats[b * stats_stride(K) + i] = s_stats[i];
+    for (int i = tid; i < 4 * SS; i += NT) P.sched[b * 4 * SS + i] = s_sched[i];
+  }
+  for (int i = tid; i < 4 * K * K; i += NT) {
+    const int cv = i / (K * K), g = i % (K * K);
+    if (g < s_sched[cv * SS]) s_sc[cv][g] = pow2_exact(-s_sched[cv * SS + 1 + g * (2 + 2 * L)]);
+  }
+  const int ng[4] = {s_sched[0], s_sched[SS], s_sched[2 * SS], s_sched[3 * SS]};
+  SMALL_STAMP(1);
+
+  // ---- a3: the ka forward spectra of part a, prime q (every z recomputes them)
+  if (STAGE) mbar_wait(&s_bar, 0u);
+  const uint2* Tf = STAGE ? s_tw : gTf;
+  const uint2* Ti = STAGE ? s_tw + m : gTi;
+  const uint32_t* Wq = STAGE ? s_W : gW;
+  const int ka = bad ? 0 : kvf[a];
+  uint32_t* const wk3[3] = {work, work + padm, work + 2 * padm};
+  if (ka == 3) {  // the three slices as one NV = 3 pass (shared twiddle loads, 3x ILP)
+    __syncthreads();  // xp reads done
+    sub_ntt_multi<LOGC, false, 1, 3, kSmallLogE, true, false, false, STAGE>(
+        tid, wk3, 0u, 1u, Tf, Tw0{nullptr, 0u, 0u}, p,
+        [&](int v, int, uint32_t e) -> uint32_t { return e < (uint32_t)nn ? lift(dig[v * nn + e], p) : 0u; },
+        [&](int v, int, uint32_t e, uint32_t val) { X[v * m + row_perm(e, LOGC, kSmallLogE)] = val; });
+  } else {
+    for (int s = 0; s < ka; ++s) {
+      __syncthreads();  // xp reads done (s = 0) / exchange buffer free
+      const int32_t* D = dig + s * nn;
+      uint32_t* xs = X + s * m;
+      sub_ntt<LOGC, false, 1, kSmallLogE, true, STAGE>(
+          tid, work, 0u, 1u, Tf, p,
+          [&](int, uint32_t e) -> uint32_t { return e < (uint32_t)nn ? lift(D[e], p) : 0u; },
+          [&](int, uint32_t e, uint32_t v) { xs[row_perm(e, LOGC, kSmallLogE)] = v; });
+    }
+  }
+  SMALL_STAMP(2);
+  // ---- a4 + a5: items (ci, g) = every Z-th of the two convolutions' Alg.8 groups
+  const uint32_t pinv = 0u - P.pinv[q];  // +p^{-1} mod 2^32
+  const int cvs[2] = {a, a == 0 ? 3 : 2};
+  const int nitems = bad ? 0 : ng[cvs[0]] + ng[cvs[1]];
+  constexpr int CNT = RoundT<LOGC, true, 0, kSmallLogE>::cnt;
+  for (int it = z, slot = 0; it < nitems; it += Z, ++slot) {
+    __syncthreads();  // spectra written / exchange buffer free
+    const int ci = it < ng[cvs[0]] ? 0 : 1;
+    const int g = ci ? it - ng[cvs[0]] : it;
+    const int cv = cvs[ci];
+    const int32_t* grp = s_sched + cv * SS + 1 + g * (2 + 2 * L);
+    const int np = grp[1];
+    const uint32_t* Wb = Wq + (size_t)conv_b(cv) * K * m;
+    uint32_t zv[CNT];
+    for (int ip0 = 0; ip0 < np; ip0 += 3) {  // lazy sums of <= 3 products, one REDC each
+      unsigned long long T[CNT];
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) T[i] = 0ull;
+      const int ipe = min(np, ip0 + 3);
+      for (int ip = ip0; ip < ipe; ++ip) {
+        const uint32_t* xr = X + grp[2 + 2 * ip] * m;
+        const uint32_t* wr = Wb + (size_t)grp[3 + 2 * ip] * m;
+#pragma unroll
+        for (int i = 0; i < CNT; ++i) {
+          const uint32_t e = round_elem<LOGC, true, 0, kSmallLogE>(tid, i);
+          T[i] += (unsigned long long)xr[row_perm(e, LOGC, kSmallLogE)] * wr[row_perm(e, LOGC, P.w_s0)];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) {
+        const uint32_t r = redc_lazy3(T[i], p, pinv);
+        zv[i] = ip0 == 0 ? r : add_mod(zv[i], r, p);
+      }
+    }
+    uint32_t* rs = res + (size_t)slot * nn;
+    const bool flip = P.fault && b == 0 && q == 0 && cv == 0 && g == ng[0] - 1;
+    sub_ntt<LOGC, true, 1, kSmallLogE, true, STAGE>(
+        tid, work, 0u, 1u, Ti, p, [&](int i, uint32_t) -> uint32_t { return zv[i]; },
+        [&](int, uint32_t e, uint32_t val) {
+          if (e < (uint32_t)nn) rs[e] = (flip && e == 0) ? val ^ 1u : val;
+        });
+  }
+  SMALL_STAMP(3);
+  cl.sync();  // every CTA's residues visible cluster-wide
+  SMALL_STAMP(4);
+
+  // ---- a6 + a7: thread (cv, jl) sums conv cv's Garner values 2^-cexp in flush order, then
+  // the cv = 0 threads combine the four sums and post-chirp (k_crt_finish's sequence)
+  constexpr int NQ = NT / 4;
+  const int cvt = tid / NQ, jl = tid % NQ;
+  for (int64_t j0 = (int64_t)rank * NQ; j0 < P.n; j0 += (int64_t)4 * Z * NQ) {
+    const int64_t j = j0 + jl;
+    double2 w = make_double2(0.0, 0.0);
+    if (cvt == 0 && j < P.n) w = __ldg(&P.chirp[j]);  // in flight during the DD chain
+    if (j < P.n && !bad) {
+      const int cv = cvt, ca = conv_a(cv), ci = cv >> 1;  // cv 2, 3 are part a's second conv
+      double sh = 0.0, sl = 0.0;
+      for (int g0 = 0; g0 < ng[cv]; g0 += 9) {
+        uint32_t z0[9], z1[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          if (g0 + i < ng[cv]) {
+            const int it = ci ? ng[ca] + g0 + i : g0 + i;
+            const int zr = it % Z, sl_ = it / Z;
+            const uint32_t* r0 = cl.map_shared_rank(res, (0 * 2 + ca) * Z + zr);
+            const uint32_t* r1 = cl.map_shared_rank(res, (1 * 2 + ca) * Z + zr);
+            z0[i] = r0[(size_t)sl_ * nn + j];
+            z1[i] = r1[(size_t)sl_ * nn + j];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          if (g0 + i < ng[cv]) {
+            const long long Zv = garner2(z0[i], z1[i], P.F);
+            double hs, ls;
+            scaled_split(Zv, s_sc[cv][g0 + i], hs, ls);
+            dd_add(sh, sl, hs, ls, sh, sl);
+          }
+        }
+      }
+      s_S[cv][jl] = make_double2(sh, sl);
+    }
+    __syncthreads();
+    if (cvt == 0 && j < P.n) {
+      double2 o;
+      if (bad) {
+        o.x = __longlong_as_double(0x7FF8000000000000ll);
+        o.y = o.x;
+      } else {
+        o = dd_combine_postchirp(s_S[0][jl], s_S[1][jl], s_S[2][jl], s_S[3][jl], w, P.direction, P.n);
+      }
+      P.out[b * P.n + j] = o;
+    }
+    __syncthreads();
+  }
+  SMALL_STAMP(5);
+  cl.sync();  // no CTA exits while another may still read its residues
+  SMALL_STAMP(6);
+}
+#if OZ_SMALL_TIMING
+extern "C" int ozfft_debug_small_times(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_small_t, sizeof(g_small_t));
+}
+#endif
 
 // ============================================================== fused inverse column pass + CRT
 // For R > 1 the last log2(R) DIT stages, Garner's CRT and the scaled DD accumulation
@@ -2612,6 +2984,66 @@ ozfft_status launch_plan_precompute(Plan& pl, void* stream) {
   return s;
 }
 
+#ifndef OZ_SMALL_Z
+#define OZ_SMALL_Z 4  // CTAs per (prime, part) of k_small_fused: clusters of 4 Z CTAs
+#endif
+// k_small_fused for one-pass plans in the default mode; OZFFT_ERR_UNSUPPORTED_LENGTH (no
+// error recorded) when the plan is outside its range, so the caller takes the multi-kernel path.
+static ozfft_status launch_small_fused(const Plan& pl, const ExecArgs& A, int32_t* stats, int32_t* sched,
+                                       unsigned long long* mu, const double2* chirp, const uint2* tw,
+                                       const uint32_t* W, const int32_t* wsplit, cudaStream_t st) {
+  if (!pl.small_fused || pl.logR != 0 || pl.logC < 8 || pl.logC > 12 || pl.image || pl.ts)
+    return OZFFT_ERR_UNSUPPORTED_LENGTH;
+  const int Z = pl.small_z > 0 ? pl.small_z : OZ_SMALL_Z;
+  const int slots = (2 * pl.K * pl.K + Z - 1) / Z;
+  const size_t base = 4 * (small_head_words(pl.n, pl.K, pl.L) + small_union_words(pl.logC, pl.n, pl.K, slots));
+  const size_t staged = base + 4 * small_stage_words(pl.logC, pl.K);
+  const int stage = staged <= 200 * 1024 ? 1 : 0;
+  const size_t smem = stage ? staged : base;
+  if (smem > 200 * 1024) return OZFFT_ERR_UNSUPPORTED_LENGTH;
+  SmallParams P{};
+  P.x = reinterpret_cast<const double2*>(A.in);
+  P.chirp = chirp;
+  P.out = reinterpret_cast<double2*>(A.out);
+  P.n = pl.n; P.K = pl.K; P.L = pl.L; P.alpha = pl.alpha; P.rho = pl.rho;
+  P.conj = A.direction > 0 ? 1 : 0;
+  P.direction = A.direction;
+  P.p[0] = pl.p[0]; P.p[1] = pl.p[1]; P.pinv[0] = pl.pinv[0]; P.pinv[1] = pl.pinv[1];
+  P.tw = tw; P.W = W; P.w_s0 = row_s0(pl.logC, false); P.wsplit = wsplit;
+  fill_crt_consts(pl, P.F);
+  P.mu = mu; P.stats = stats; P.sched = sched;
+  P.Z = Z; P.slots = slots; P.stage = stage;
+  P.fault = pl.fault;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(4 * Z), (unsigned)A.nb);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)(4 * Z);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaSuccess;
+  prof_mark(pl, OZFFT_STAGE_ROW_FUSED, true, st);
+  dispatch_log<8, 12>(pl.logC, [&](auto I) {
+    auto kern = stage ? k_small_fused<I.value, true> : k_small_fused<I.value, false>;
+    cfg.blockDim = dim3((unsigned)small_threads(I.value));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (4 * Z > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaLaunchKernelEx(&cfg, kern, P);
+  });
+  prof_mark(pl, OZFFT_STAGE_ROW_FUSED, false, st);
+  count_launches(1);
+  if (e != cudaSuccess) {
+    set_error(std::string("k_small_fused: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+    return OZFFT_ERR_CUDA;
+  }
+  return cuda_check("k_small_fused");
+}
+
 ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (A.nb < 1 || A.ws0 < 0 || A.ws0 + A.nb > pl.chunk) {  // the chunked workspace regions
@@ -2641,6 +3073,10 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   const int32_t* wsplit = reinterpret_cast<const int32_t*>(pl.pers + pl.poff.wsplit);
   const ozfft_taps* taps = A.taps;
 
+  if (A.phase == 0 && !taps && !A.res_out && A.unit_mask == 0xFFu && A.finish) {
+    const ozfft_status fs = launch_small_fused(pl, A, stats, sched, mu, chirp, tw, W, wsplit, st);
+    if (fs != OZFFT_ERR_UNSUPPORTED_LENGTH) return fs;  // else: the multi-kernel path
+  }
   SplitParams SP{};
   SP.x = reinterpret_cast<const double2*>(A.in);
   SP.chirp = chirp;
