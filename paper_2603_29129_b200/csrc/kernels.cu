@@ -1046,8 +1046,11 @@ __device__ __forceinline__ uint32_t digit_image(int32_t dre, int32_t dim, uint2 
 
 // Elements per thread per round (log2) of the row and column sub-transforms: 32 for the
 // one-warp rows of C = 2^10 (two-pass plans) and for columns of R >= 2^9, else 16.
+#ifndef OZ_ROW_LOGE11
+#define OZ_ROW_LOGE11 4  // elements per thread (log2) of the two-pass rows of C = 2^11
+#endif
 __host__ __device__ constexpr int row_loge(int logC, bool two_pass) {
-  return two_pass && logC == 10 ? 5 : 4;
+  return two_pass && logC == 11 ? OZ_ROW_LOGE11 : (two_pass && logC == 10 ? 5 : 4);
 }
 #ifndef OZ_COL_E32_MIN_LOGR
 #define OZ_COL_E32_MIN_LOGR 9
@@ -1347,7 +1350,7 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   if (ka == 0 && !P.fwd_only) return;  // no slices: the schedule has no groups here
   // [K][XS] forward spectra rows (row_perm order); two-pass rows are XS = C + C/16 + 4 words
   // apart (the padded exchange layout of the three-slice forward fits in place, 16B-aligned)
-  constexpr uint32_t XS = TWO_PASS ? C + (C >> 4) + 4 : C;
+  constexpr uint32_t XS = TWO_PASS ? C + (C >> LOGE) + 4 : C;
   uint32_t* Xs = smem;
   // [padC]: inter-round exchange buffer; a CTA barrier before each sub-transform frees it
   // (double buffering, which would drop that barrier, measured slower: more registers)
@@ -1860,6 +1863,69 @@ __global__ void __launch_bounds__(256, 4) k_crt_finish_img(FinishParams P) {
   o.x = ore;
   o.y = oim;
   P.out[b * P.n + j] = o;
+}
+
+// Garner + scaled DD sums in flush order from gathered residues (the unit-sharded single
+// transform after its all-gather; one transform): CTA = (conv, 256 x kCrtDDPer outputs).
+// A dependent DADD costs ~25 clocks on B200, so each thread keeps kCrtDDPer independent DD chains and
+// the next group's residues in flight.  Same per-value sequence as k_col_inv_crt /
+// k_crt_finish (Alg.8 l.974-976); k_finish_dd then combines the four sums and post-chirps.
+#ifndef OZ_CRTDD_PER
+#define OZ_CRTDD_PER 4
+#endif
+constexpr int kCrtDDPer = OZ_CRTDD_PER;  // outputs (independent DD chains) per thread
+__global__ void __launch_bounds__(256) k_crt_dd(FinishParams P, double2* __restrict__ S) {
+  const int cv = blockIdx.y;
+  const int K = P.K, L = P.L;
+  __shared__ double s_sc[kMaxK * kMaxK];
+  const int32_t* srow = P.sched + cv * sched_stride(K, L);
+  const int ng = srow[0];
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) s_sc[g] = pow2_exact(-srow[1 + g * (2 + 2 * L)]);
+  __syncthreads();
+  if (P.stats[2 + 2 * K] & 1) return;  // non-finite transform: k_finish_dd writes NaN
+  const int64_t n = P.n;
+  const int64_t j0 = (int64_t)blockIdx.x * 256 * kCrtDDPer + threadIdx.x;
+  const uint32_t* r0 = P.res + (size_t)(cv * 2 + 0) * P.rg * n;
+  const uint32_t* r1 = P.res + (size_t)(cv * 2 + 1) * P.rg * n;
+  double h[kCrtDDPer], l[kCrtDDPer];
+  uint32_t a0[kCrtDDPer], a1[kCrtDDPer];
+#pragma unroll
+  for (int u = 0; u < kCrtDDPer; ++u) {
+    const int64_t j = j0 + u * 256;
+    h[u] = 0.0;
+    l[u] = 0.0;
+    a0[u] = ng > 0 && j < n ? __ldcs(&r0[j]) : 0u;
+    a1[u] = ng > 0 && j < n ? __ldcs(&r1[j]) : 0u;
+  }
+  for (int g = 0; g < ng; ++g) {
+    uint32_t c0[kCrtDDPer], c1[kCrtDDPer];
+#pragma unroll
+    for (int u = 0; u < kCrtDDPer; ++u) {
+      c0[u] = a0[u];
+      c1[u] = a1[u];
+    }
+    if (g + 1 < ng) {
+#pragma unroll
+      for (int u = 0; u < kCrtDDPer; ++u) {
+        const int64_t j = j0 + u * 256;
+        a0[u] = j < n ? __ldcs(&r0[(int64_t)(g + 1) * n + j]) : 0u;
+        a1[u] = j < n ? __ldcs(&r1[(int64_t)(g + 1) * n + j]) : 0u;
+      }
+    }
+    const double sc = s_sc[g];
+#pragma unroll
+    for (int u = 0; u < kCrtDDPer; ++u) {
+      const long long Z = garner2(c0[u], c1[u], P);
+      double hs, ls;
+      scaled_split(Z, sc, hs, ls);
+      dd_add(h[u], l[u], hs, ls, h[u], l[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kCrtDDPer; ++u) {
+    const int64_t j = j0 + u * 256;
+    if (j < n) S[cv * n + j] = make_double2(h[u], l[u]);
+  }
 }
 
 // ============================================================== one-launch small transform
@@ -2721,6 +2787,11 @@ static ozfft_status launch_split(const Plan& pl, SplitParams SP, int64_t nb, cud
   const int threads = 256;
   int64_t blocks_per = (SP.len + threads * OZ_SPLIT_EPT - 1) / (threads * OZ_SPLIT_EPT);
   if (blocks_per < 1) blocks_per = 1;
+  if (blocks_per * nb < 4 * sm_count()) {  // small batches: fill the GPU (grid-stride kernels)
+    const int64_t want = (4 * sm_count() + nb - 1) / nb, most = (SP.len + threads - 1) / threads;
+    blocks_per = want < most ? want : most;
+    if (blocks_per < 1) blocks_per = 1;
+  }
   if (blocks_per > 65535) blocks_per = 65535;
   dim3 grid((unsigned)blocks_per, (unsigned)nb);
 #if OZ_SPLIT_CLUSTER
@@ -2803,7 +2874,7 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   const size_t C = 1ull << pl.logC;
   const int rle = row_loge(pl.logC, pl.logR > 0);
   const size_t padC = C + (C >> rle) + 1;
-  const size_t XS = pl.logR > 0 ? C + (C >> 4) + 4 : C;  // X row stride (k_row_fused)
+  const size_t XS = pl.logR > 0 ? C + (C >> rle) + 4 : C;  // X row stride (k_row_fused)
   c.row_smem = ((size_t)pl.K * XS + padC + 2 * pl.K * pl.K * (1 + 2 * pl.L)) * sizeof(uint32_t);
   c.row_threads = pl.logC >= rle ? (1 << (pl.logC - rle)) : 1;  // exactly Tv: every thread active
   return c;
@@ -3355,12 +3426,20 @@ ozfft_status launch_finish_from_residues(const Plan& pl, const uint32_t* res, in
   dim3 grid((unsigned)((pl.n + 255) / 256), 1);
   const dim3 grid4((unsigned)((pl.n + kFinishCols - 1) / kFinishCols), 1);
   prof_mark(pl, OZFFT_STAGE_CRT_FINISH, true, st);
-  if (pl.ts)
+  int nl = 1;
+  if (pl.ts) {
     k_crt_finish_ts<<<grid, 256, 0, st>>>(FP);
-  else
+  } else if (pl.logR > 0) {  // long transforms: 8 DD chains per thread, then the combine
+    double2* S = reinterpret_cast<double2*>(pl.ws + pl.woff.S);
+    const dim3 gdd((unsigned)((pl.n + 256 * kCrtDDPer - 1) / (256 * kCrtDDPer)), 4);
+    k_crt_dd<<<gdd, 256, 0, st>>>(FP, S);
+    k_finish_dd<<<grid, 256, 0, st>>>(S, FP.stats, pl.K, FP.chirp, FP.out, pl.n, direction, 0, 0);
+    nl = 2;
+  } else {
     k_crt_finish<<<grid4, 256, 0, st>>>(FP);
+  }
   prof_mark(pl, OZFFT_STAGE_CRT_FINISH, false, st);
-  count_launches(1);
+  count_launches(nl);
   return cuda_check("k_crt_finish (shard)");
 }
 

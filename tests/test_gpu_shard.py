@@ -59,3 +59,28 @@ def test_shard_schedule_with_gaps():
         out = torch.empty(n, dtype=torch.complex128, device="cuda")
         plan.shard_finish(res, g, out)
         assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("world", [1, 8])
+def test_shard_c3_size_and_nonfinite(world):
+    """The single-transform variant at the c3 length (n = 2^18: the finish from gathered
+    residues runs k_crt_dd + k_finish_dd) equals the batched execute bit for bit; a
+    non-finite input gives NaN through the same path."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_29129_b200 as oz
+    n = 1 << 18
+    x = torch.from_numpy(workloads.draw("uniform", 2, 1, n)).cuda()
+    plan = oz.Plan(n, 1)
+    ref = plan.forward(x)[0]
+    res = torch.zeros(plan.shard_residue_bytes() // 4, dtype=torch.int32, device="cuda")
+    out = torch.empty(n, dtype=torch.complex128, device="cuda")
+    for r in range(world):
+        g = plan.shard_partial(x, r, world, res)
+    plan.shard_finish(res, g, out)
+    assert torch.equal(out, ref)
+    x[0, 12345] = float("nan")
+    for r in range(world):
+        g = plan.shard_partial(x, r, world, res)
+    plan.shard_finish(res, g, out)
+    assert torch.isnan(out.real).all() and torch.isnan(out.imag).all()
