@@ -300,6 +300,9 @@ constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
 #ifndef OZ_SPLIT_EPT
 #define OZ_SPLIT_EPT 8  // elements per thread of k_split_max / k_split_digits
 #endif
+#ifndef OZ_SPLIT_ILP
+#define OZ_SPLIT_ILP 2  // k_split_max / k_split_digits: elements per thread interleaved
+#endif
 #ifndef OZ_SPLIT_CL_EPT
 #define OZ_SPLIT_CL_EPT 1  // elements per thread per iteration of k_split_cluster
 #endif
@@ -407,28 +410,51 @@ __global__ void __launch_bounds__(256) k_split_max(SplitParams P, int level) {
   }
   __syncthreads();
   unsigned long long m0 = 0, m1 = 0;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P.len;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    unsigned long long a0, a1;
+  // OZ_SPLIT_ILP elements per thread and iteration as independent chains (a dependent DADD
+  // costs ~25 clocks on B200); out-of-range slots redo the thread's first element
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < P.len; j0 += OZ_SPLIT_ILP * stride) {
+    unsigned long long a0[OZ_SPLIT_ILP], a1[OZ_SPLIT_ILP];
     if constexpr (TS) {  // f4: TS words, mu over r0
-      TSv r[2];
-      load_xprime_ts(P, b, j, r[0], r[1]);
+      TSv r[OZ_SPLIT_ILP][2];
+#pragma unroll
+      for (int u = 0; u < OZ_SPLIT_ILP; ++u) {
+        const int64_t j = j0 + u * stride < P.len ? j0 + u * stride : j0;
+        load_xprime_ts(P, b, j, r[u][0], r[u][1]);
+      }
 #pragma unroll
       for (int v = 0; v < 2; ++v)
-        for (int k = 0; k < lv[v]; ++k) (void)split_step_ts(r[v], s_c[v][k]);
-      a0 = ts_key(r[0]);
-      a1 = ts_key(r[1]);
+        for (int k = 0; k < lv[v]; ++k)
+#pragma unroll
+          for (int u = 0; u < OZ_SPLIT_ILP; ++u) (void)split_step_ts(r[u][v], s_c[v][k]);
+#pragma unroll
+      for (int u = 0; u < OZ_SPLIT_ILP; ++u) {
+        a0[u] = ts_key(r[u][0]);
+        a1[u] = ts_key(r[u][1]);
+      }
     } else {
-      double h[2], l[2];
-      load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
+      double h[OZ_SPLIT_ILP][2], l[OZ_SPLIT_ILP][2];
+#pragma unroll
+      for (int u = 0; u < OZ_SPLIT_ILP; ++u) {
+        const int64_t j = j0 + u * stride < P.len ? j0 + u * stride : j0;
+        load_xprime(P, b, j, h[u][0], l[u][0], h[u][1], l[u][1]);
+      }
 #pragma unroll
       for (int v = 0; v < 2; ++v)  // a level with mu == 0 ended this part's split (Alg.6 l.780)
-        for (int k = 0; k < lv[v]; ++k) (void)split_step(h[v], l[v], s_c[v][k]);
-      a0 = (unsigned long long)__double_as_longlong(fabs(h[0]));
-      a1 = (unsigned long long)__double_as_longlong(fabs(h[1]));
+        for (int k = 0; k < lv[v]; ++k)
+#pragma unroll
+          for (int u = 0; u < OZ_SPLIT_ILP; ++u) (void)split_step(h[u][v], l[u][v], s_c[v][k]);
+#pragma unroll
+      for (int u = 0; u < OZ_SPLIT_ILP; ++u) {
+        a0[u] = (unsigned long long)__double_as_longlong(fabs(h[u][0]));
+        a1[u] = (unsigned long long)__double_as_longlong(fabs(h[u][1]));
+      }
     }
-    m0 = a0 > m0 ? a0 : m0;  // NaN bits exceed +Inf bits: a NaN sticks
-    m1 = a1 > m1 ? a1 : m1;
+#pragma unroll
+    for (int u = 0; u < OZ_SPLIT_ILP; ++u) {
+      m0 = a0[u] > m0 ? a0[u] : m0;  // NaN bits exceed +Inf bits: a NaN sticks
+      m1 = a1[u] > m1 ? a1[u] : m1;
+    }
   }
   __shared__ unsigned long long red[2][8];
   m0 = warp_max_u64(m0);
@@ -543,31 +569,43 @@ __global__ void __launch_bounds__(256) k_split_digits(SplitParams P) {
     s_c[v][k] = split_c<TS>(k < P.K ? E[v][k] : 0, P.alpha, P.rho);
   }
   __syncthreads();
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P.len;
-       j += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < P.len; j0 += OZ_SPLIT_ILP * stride) {
     if constexpr (TS) {
-      TSv r[2];
-      load_xprime_ts(P, b, j, r[0], r[1]);
+      TSv r[OZ_SPLIT_ILP][2];
+#pragma unroll
+      for (int u = 0; u < OZ_SPLIT_ILP; ++u) {
+        const int64_t j = j0 + u * stride < P.len ? j0 + u * stride : j0;
+        load_xprime_ts(P, b, j, r[u][0], r[u][1]);
+      }
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j;
-        for (int k = 0; k < P.K; ++k) {
-          int32_t D = 0;
-          if (k < kv[v]) D = split_step_ts(r[v], s_c[v][k]);
-          dv[k * P.len] = D;
-        }
+        int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j0;
+        for (int k = 0; k < P.K; ++k)
+#pragma unroll
+          for (int u = 0; u < OZ_SPLIT_ILP; ++u) {
+            int32_t D = 0;
+            if (k < kv[v]) D = split_step_ts(r[u][v], s_c[v][k]);
+            if (j0 + u * stride < P.len) dv[k * P.len + u * stride] = D;
+          }
       }
     } else {
-      double h[2], l[2];
-      load_xprime(P, b, j, h[0], l[0], h[1], l[1]);
+      double h[OZ_SPLIT_ILP][2], l[OZ_SPLIT_ILP][2];
+#pragma unroll
+      for (int u = 0; u < OZ_SPLIT_ILP; ++u) {
+        const int64_t j = j0 + u * stride < P.len ? j0 + u * stride : j0;
+        load_xprime(P, b, j, h[u][0], l[u][0], h[u][1], l[u][1]);
+      }
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j;
-        for (int k = 0; k < P.K; ++k) {
-          int32_t D = 0;
-          if (k < kv[v]) D = split_step(h[v], l[v], s_c[v][k]);
-          dv[k * P.len] = D;
-        }
+        int32_t* dv = P.digits + ((b * 2 + v) * P.K) * P.len + j0;
+        for (int k = 0; k < P.K; ++k)
+#pragma unroll
+          for (int u = 0; u < OZ_SPLIT_ILP; ++u) {
+            int32_t D = 0;
+            if (k < kv[v]) D = split_step(h[u][v], l[u][v], s_c[v][k]);
+            if (j0 + u * stride < P.len) dv[k * P.len + u * stride] = D;
+          }
       }
     }
   }
