@@ -1328,7 +1328,7 @@ struct RowCfg {
   static constexpr int E = 1 << LOGE;
   static constexpr int threads = LOGC >= LOGE ? (1 << (LOGC - LOGE)) : 1;
 #ifndef OZ_ROW_MINB
-#define OZ_ROW_MINB 5  // 96 registers, 5 CTAs/SM (6 at 80 registers: c3 1074 vs 1065 us)
+#define OZ_ROW_MINB 6  // 80 registers, 6 CTAs/SM (with the 16-byte W/X quads: c3 1031 vs 1037 us at 96 / 5)
 #endif
   static constexpr int min_blocks = LOGC == 11 ? OZ_ROW_MINB : (LOGC == 10 && TWO_PASS ? 12 : 1);
   // stages of the first DIT round (= last DIF round): its groups are contiguous blocks
@@ -1336,20 +1336,57 @@ struct RowCfg {
 };
 
 // Row-local storage order used for the X rows in shared memory and for the cached W
-// spectra: element e of a row (internal bit-reversed order) lives at
-// (e mod 2^S0) * (C / 2^S0) + e / 2^S0, so that in the first DIT round (groups of 2^S0
-// contiguous elements, one group per thread) a warp touches consecutive words.
-__host__ __device__ __forceinline__ uint32_t row_perm(uint32_t e, int logC, int S0) {
+// spectra.  In the first DIT round thread t holds the 2^S0 contiguous elements
+// e = t 2^S0 + i (internal bit-reversed order).  OZ_ROW_VEC: element e lives at
+// (i / 4) (C 4 / 2^S0) + 4 t + (i mod 4), so a thread's registers 4k .. 4k+3 are one 16-byte
+// word and a warp's 16-byte loads / stores of quad k cover 512 contiguous bytes (coalesced
+// LDG.128, conflict-free LDS/STS.128: a quarter of the W / X load instructions of the
+// pointwise stage).  Without it: (e mod 2^S0) (C / 2^S0) + e / 2^S0 (32-bit words, a warp
+// touches consecutive words per register).
+#ifndef OZ_ROW_VEC
+#define OZ_ROW_VEC 1
+#endif
+__host__ __device__ __forceinline__ uint32_t row_perm_lin(uint32_t e, int logC, int S0) {
   return ((e & ((1u << S0) - 1)) << (logC - S0)) + (e >> S0);
 }
+__host__ __device__ __forceinline__ uint32_t row_perm(uint32_t e, int logC, int S0) {
+#if OZ_ROW_VEC
+  if (S0 >= 2) {
+    const uint32_t i = e & ((1u << S0) - 1), t = e >> S0;
+    return ((i >> 2) << (logC - S0 + 2)) + (t << 2) + (i & 3);
+  }
+#endif
+  return row_perm_lin(e, logC, S0);
+}
 
-// row_perm of the element held in register i by thread tv in the first DIT round (element
-// g*2^S0 + k, g = tv + u*Tv, i = u*2^S0 + k): tv + compile-time offset.
+// row_perm of the element held in register i (< 2^S0) by thread tv in the first DIT round
+// (element tv 2^S0 + i): a compile-time offset plus a function of tv.
 template <int LOGC, bool TWO_PASS>
 __device__ __forceinline__ uint32_t row_slot(int tv, int i) {
   constexpr int S0 = RowCfg<LOGC, TWO_PASS>::S0;
   constexpr int Tv = RowCfg<LOGC, TWO_PASS>::threads;
+#if OZ_ROW_VEC
+  if constexpr (S0 >= 2)
+    return ((uint32_t)(i >> 2) << (LOGC - S0 + 2)) + ((uint32_t)tv << 2) + (uint32_t)(i & 3);
+#endif
   return (uint32_t)tv + ((uint32_t)(i & ((1 << S0) - 1)) << (LOGC - S0)) + (uint32_t)(i >> S0) * Tv;
+}
+// 16-byte quads of row_slot: registers 4k .. 4k+3 of thread tv start at row_quad(tv, k)
+template <int LOGC, bool TWO_PASS>
+__device__ __forceinline__ uint32_t row_quad(int tv, int k) {
+  constexpr int S0 = RowCfg<LOGC, TWO_PASS>::S0;
+  return ((uint32_t)k << (LOGC - S0 + 2)) + ((uint32_t)tv << 2);
+}
+template <int LOGC, bool TWO_PASS>
+__host__ __device__ constexpr bool row_vec() {
+  return OZ_ROW_VEC && RowCfg<LOGC, TWO_PASS>::S0 >= 2;
+}
+__device__ __forceinline__ uint4 ldg_stream4(const uint32_t* p) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p));
+  return v;
 }
 
 template <int LOGC, bool TWO_PASS>
@@ -1472,9 +1509,17 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
           });
       __syncthreads();  // every last-round read done before X overwrites the rows
 #pragma unroll
-      for (int v = 0; v < 3; ++v)
+      for (int v = 0; v < 3; ++v) {
+        if constexpr (row_vec<LOGC, TWO_PASS>()) {
 #pragma unroll
-        for (int i = 0; i < CNT0; ++i) Xs[v * XS + row_slot<LOGC, TWO_PASS>(tv, i)] = xv[v][i];
+          for (int k = 0; k < CNT0 / 4; ++k)
+            *reinterpret_cast<uint4*>(Xs + v * XS + row_quad<LOGC, TWO_PASS>(tv, k)) =
+                make_uint4(xv[v][4 * k], xv[v][4 * k + 1], xv[v][4 * k + 2], xv[v][4 * k + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < CNT0; ++i) Xs[v * XS + row_slot<LOGC, TWO_PASS>(tv, i)] = xv[v][i];
+        }
+      }
       s_begin = 3;
     }
   }
@@ -1535,12 +1580,36 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
   // pointwise products for this thread's round-0 elements: 64-bit lazy sums of up to 3
   // products X * W~ (W~ = W m^{-1} 2^32, sums < 3 p^2 < 2^64), one Montgomery reduction each
   auto wld = [&](const uint32_t* w) -> uint32_t { return ldg_stream(w); };
+  // this thread's CNT words of a W row / an X row (16-byte quads with OZ_ROW_VEC)
+  auto ld_wrow = [&](const uint32_t* wr, uint32_t (&w)[E]) {
+    if constexpr (row_vec<LOGC, TWO_PASS>()) {
+#pragma unroll
+      for (int k = 0; k < CNT / 4; ++k) {
+        const uint4 v = ldg_stream4(wr + row_quad<LOGC, TWO_PASS>(tv, k));
+        w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) w[i] = wld(&wr[row_slot<LOGC, TWO_PASS>(tv, i)]);
+    }
+  };
+  auto ld_xrow = [&](const uint32_t* xr, uint32_t (&x)[E]) {
+    if constexpr (row_vec<LOGC, TWO_PASS>()) {
+#pragma unroll
+      for (int k = 0; k < CNT / 4; ++k) {
+        const uint4 v = *reinterpret_cast<const uint4*>(xr + row_quad<LOGC, TWO_PASS>(tv, k));
+        x[4 * k] = v.x; x[4 * k + 1] = v.y; x[4 * k + 2] = v.z; x[4 * k + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) x[i] = xr[row_slot<LOGC, TWO_PASS>(tv, i)];
+    }
+  };
   auto load_w0 = [&](int ci, int g, uint32_t (&w)[E]) {  // W row of an item's first pair
     const int cv = ci ? cv1 : cv0;
     const uint32_t* wr0 = P.W + (size_t)(q * 2 + (P.image ? a : conv_b(cv))) * K * m + rowoff +
                           tab[(ci * G + g) * tstride + 2];
-#pragma unroll
-    for (int i = 0; i < CNT; ++i) w[i] = wld(&wr0[row_slot<LOGC, TWO_PASS>(tv, i)]);
+    ld_wrow(wr0, w);
   };
   auto pointwise = [&](int ci, int g, uint32_t (&z)[E]) {
     const int cv = ci ? cv1 : cv0;
@@ -1550,31 +1619,23 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
     if (np <= 3) {  // (L <= 3 always): the W loads of two pairs in flight ahead of the
                     // products (one L2 latency per group instead of one per pair; loading the
                     // next item's W during this item's NTT measured slower -- registers)
-      uint32_t w0[E], w1[E];
+      uint32_t w0[E], w1[E], xv[E];
       load_w0(ci, g, w0);
-      if (np > 1) {
-        const uint32_t* wr1 = Wb + tg[4];
-#pragma unroll
-        for (int i = 0; i < CNT; ++i) w1[i] = wld(&wr1[row_slot<LOGC, TWO_PASS>(tv, i)]);
-      }
+      if (np > 1) ld_wrow(Wb + tg[4], w1);
       unsigned long long T[E];
-      const uint32_t* x0 = Xs + tg[1];
+      ld_xrow(Xs + tg[1], xv);
 #pragma unroll
-      for (int i = 0; i < CNT; ++i) T[i] = (unsigned long long)x0[row_slot<LOGC, TWO_PASS>(tv, i)] * w0[i];
-      if (np > 2) {
-        const uint32_t* wr2 = Wb + tg[6];
-#pragma unroll
-        for (int i = 0; i < CNT; ++i) w0[i] = wld(&wr2[row_slot<LOGC, TWO_PASS>(tv, i)]);
-      }
+      for (int i = 0; i < CNT; ++i) T[i] = (unsigned long long)xv[i] * w0[i];
+      if (np > 2) ld_wrow(Wb + tg[6], w0);
       if (np > 1) {
-        const uint32_t* x1 = Xs + tg[3];
+        ld_xrow(Xs + tg[3], xv);
 #pragma unroll
-        for (int i = 0; i < CNT; ++i) T[i] += (unsigned long long)x1[row_slot<LOGC, TWO_PASS>(tv, i)] * w1[i];
+        for (int i = 0; i < CNT; ++i) T[i] += (unsigned long long)xv[i] * w1[i];
       }
       if (np > 2) {
-        const uint32_t* x2 = Xs + tg[5];
+        ld_xrow(Xs + tg[5], xv);
 #pragma unroll
-        for (int i = 0; i < CNT; ++i) T[i] += (unsigned long long)x2[row_slot<LOGC, TWO_PASS>(tv, i)] * w0[i];
+        for (int i = 0; i < CNT; ++i) T[i] += (unsigned long long)xv[i] * w0[i];
       }
       if (np == 3) {
 #pragma unroll
@@ -2076,7 +2137,7 @@ __global__ void __launch_bounds__(small_threads(LOGC)) k_small_fused(SmallParams
   uint32_t* s_W = after_head + 4 * m;                    // stage: [2 b][K][m]
   uint32_t* U = after_head + (STAGE ? small_stage_words(LOGC, K) : 0);
   double* xp = reinterpret_cast<double*>(U);              // split: h[2][n], l[2][n]
-  uint32_t* X = U;                                        // [K][m], row_perm(., LOGC, 3)
+  uint32_t* X = U;                                        // [K][m], row_perm_lin(., LOGC, 3)
   uint32_t* work = X + (size_t)K * m;                     // [3][padm]
   uint32_t* res = work + 3 * padm;                        // [slots][n]
   const uint32_t p = P.p[q];
@@ -2212,7 +2273,7 @@ __global__ void __launch_bounds__(small_threads(LOGC)) k_small_fused(SmallParams
     sub_ntt_multi<LOGC, false, 1, 3, kSmallLogE, true, false, false, STAGE>(
         tid, wk3, 0u, 1u, Tf, Tw0{nullptr, 0u, 0u}, p,
         [&](int v, int, uint32_t e) -> uint32_t { return e < (uint32_t)nn ? lift(dig[v * nn + e], p) : 0u; },
-        [&](int v, int, uint32_t e, uint32_t val) { X[v * m + row_perm(e, LOGC, kSmallLogE)] = val; });
+        [&](int v, int, uint32_t e, uint32_t val) { X[v * m + row_perm_lin(e, LOGC, kSmallLogE)] = val; });
   } else {
     for (int s = 0; s < ka; ++s) {
       __syncthreads();  // xp reads done (s = 0) / exchange buffer free
@@ -2221,7 +2282,7 @@ __global__ void __launch_bounds__(small_threads(LOGC)) k_small_fused(SmallParams
       sub_ntt<LOGC, false, 1, kSmallLogE, true, STAGE>(
           tid, work, 0u, 1u, Tf, p,
           [&](int, uint32_t e) -> uint32_t { return e < (uint32_t)nn ? lift(D[e], p) : 0u; },
-          [&](int, uint32_t e, uint32_t v) { xs[row_perm(e, LOGC, kSmallLogE)] = v; });
+          [&](int, uint32_t e, uint32_t v) { xs[row_perm_lin(e, LOGC, kSmallLogE)] = v; });
     }
   }
   SMALL_STAMP(2);
@@ -2250,7 +2311,7 @@ __global__ void __launch_bounds__(small_threads(LOGC)) k_small_fused(SmallParams
 #pragma unroll
         for (int i = 0; i < CNT; ++i) {
           const uint32_t e = round_elem<LOGC, true, 0, kSmallLogE>(tid, i);
-          T[i] += (unsigned long long)xr[row_perm(e, LOGC, kSmallLogE)] * wr[row_perm(e, LOGC, P.w_s0)];
+          T[i] += (unsigned long long)xr[row_perm_lin(e, LOGC, kSmallLogE)] * wr[row_perm(e, LOGC, P.w_s0)];
         }
       }
 #pragma unroll
