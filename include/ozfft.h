@@ -243,6 +243,34 @@ ozfft_status ozfft_shard_partial(const ozfft_plan* plan, int shard, int nshards,
 ozfft_status ozfft_shard_finish(const ozfft_plan* plan, const void* residues_all, int32_t groups,
                                 void* out, int direction, void* stream);
 
+/* ---- the same exchange fused into the producing kernel (peer memory) ---------------
+ * BASELINE.json north_star (single transform: primes / slice pairs sharded, the residues
+ * gathered before CRT) with the gather done by the kernel that computes the residues: the
+ * inverse-NTT epilogue (k_col_inv; one-pass plans: the row kernel) stores every residue of
+ * this rank's units into the exchange buffer of EVERY rank, over NVLink peer memory, so
+ * the transfer overlaps the NTT tile by tile and no collective runs afterwards.
+ * `residues_by_rank[r]` (r < nshards) is rank r's exchange buffer ([8][g][n] uint32, the
+ * capacity of ozfft_shard_residue_bytes(plan, 0)) as a device pointer valid in this
+ * process: its own buffer for r == shard, a CUDA IPC mapping (ozfft_ipc_open_handle) or a
+ * peer-accessible allocation for the others.  Same split, schedule read and *groups as
+ * ozfft_shard_partial.  Completion: a rank may call ozfft_shard_finish on its own buffer
+ * once every rank's ozfft_shard_partial_p2p has completed on its stream (the caller's
+ * barrier, e.g. stream synchronize + a process-group barrier, or a device-side
+ * collective enqueued after it).  nshards <= 8 and must divide 8.
+ * Errors: SHARD, NOT_BOUND, INVALID_ARGUMENT, CUDA. */
+ozfft_status ozfft_shard_partial_p2p(const ozfft_plan* plan, int shard, int nshards, const void* in,
+                                     int direction, void* const* residues_by_rank, int32_t* groups,
+                                     void* stream);
+/* CUDA IPC for those buffers: the 64-byte handle of the device allocation that contains
+ * `dev_ptr` (cudaIpcGetMemHandle) and the byte offset of `dev_ptr` inside it (a caching
+ * allocator's tensor need not start its allocation); the mapping of another process's
+ * (handle, offset) in this process -- *dev_ptr = mapped base + offset (cudaIpcOpenMemHandle,
+ * lazy peer access) -- and its release (the pointer and offset ozfft_ipc_open_handle gave).
+ * Errors: INVALID_ARGUMENT, CUDA. */
+ozfft_status ozfft_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
+ozfft_status ozfft_ipc_open_handle(const void* handle64, uint64_t offset, void** dev_ptr);
+ozfft_status ozfft_ipc_close(void* dev_ptr, uint64_t offset);
+
 /* ---- profiling (tracing) -----------------------------------------------------------
  * Per-stage CUDA-event timers.  While enabled, every execute records an event pair
  * around each stage kernel on the execute stream (no host synchronization).

@@ -70,7 +70,8 @@ EXPORTS = ["ozfft_plan_create", "ozfft_plan_get_info", "ozfft_plan_bind", "ozfft
            "ozfft_shard_residue_bytes", "ozfft_shard_partial", "ozfft_shard_finish",
            "ozfft_plan_destroy", "ozfft_status_string", "ozfft_last_error_string",
            "ozfft_version", "ozfft_profile_enable", "ozfft_profile_read", "ozfft_kernel_launches",
-           "ozfft_host_subbatches"]
+           "ozfft_host_subbatches", "ozfft_shard_partial_p2p", "ozfft_ipc_get_handle",
+           "ozfft_ipc_open_handle", "ozfft_ipc_close"]
 
 STAGES = ["split_max", "split_digits", "col_fwd", "row_fused", "col_inv", "crt_finish"]
 
@@ -98,6 +99,10 @@ def load_library() -> C.CDLL:
     L.ozfft_shard_residue_bytes.restype = u64
     L.ozfft_shard_partial.argtypes = [vp, i32, i32, vp, i32, vp, C.POINTER(C.c_int32), vp]
     L.ozfft_shard_finish.argtypes = [vp, vp, C.c_int32, vp, i32, vp]
+    L.ozfft_shard_partial_p2p.argtypes = [vp, i32, i32, vp, i32, C.POINTER(vp), C.POINTER(C.c_int32), vp]
+    L.ozfft_ipc_get_handle.argtypes = [vp, vp, C.POINTER(u64)]
+    L.ozfft_ipc_open_handle.argtypes = [vp, u64, C.POINTER(vp)]
+    L.ozfft_ipc_close.argtypes = [vp, u64]
     L.ozfft_plan_destroy.argtypes = [vp]
     L.ozfft_profile_enable.argtypes = [vp, i32]
     L.ozfft_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), vp]
@@ -108,6 +113,8 @@ def load_library() -> C.CDLL:
     for f in ("ozfft_plan_create", "ozfft_plan_get_info", "ozfft_plan_bind", "ozfft_execute",
               "ozfft_execute_host", "ozfft_execute_taps", "ozfft_last_stats",
               "ozfft_shard_partial", "ozfft_shard_finish", "ozfft_plan_destroy",
+              "ozfft_shard_partial_p2p", "ozfft_ipc_get_handle", "ozfft_ipc_open_handle",
+              "ozfft_ipc_close",
               "ozfft_profile_enable", "ozfft_profile_read"):
         getattr(L, f).restype = C.c_int
     L.ozfft_status_string.argtypes = [C.c_int]
@@ -127,6 +134,32 @@ def _check(status: int):
 
 def version() -> str:
     return load_library().ozfft_version().decode()
+
+
+def ipc_handle(t: torch.Tensor) -> bytes:
+    """CUDA IPC handle of a tensor's device memory: 64 handle bytes + the 8-byte offset of the
+    tensor inside its allocation (a caching allocator's tensor need not start it)."""
+    buf = C.create_string_buffer(64)
+    off = C.c_uint64(0)
+    with torch.cuda.device(t.device):
+        _check(load_library().ozfft_ipc_get_handle(t.data_ptr(), buf, C.byref(off)))
+    return buf.raw + int(off.value).to_bytes(8, "little")
+
+
+def ipc_open(handle: bytes, device=None) -> int:
+    """Map another process's tensor (ipc_handle) into this process: its device pointer."""
+    ptr = C.c_void_p(0)
+    off = int.from_bytes(handle[64:72], "little")
+    with torch.cuda.device(_normalize_device(device)):
+        _check(load_library().ozfft_ipc_open_handle(C.create_string_buffer(handle[:64], 64), off, C.byref(ptr)))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int, handle: bytes, device=None):
+    """Release a mapping made by ipc_open(handle)."""
+    off = int.from_bytes(handle[64:72], "little")
+    with torch.cuda.device(_normalize_device(device)):
+        _check(load_library().ozfft_ipc_close(C.c_void_p(ptr), off))
 
 
 def kernel_launches() -> int:
@@ -307,6 +340,19 @@ class Plan:
             _check(self._lib.ozfft_shard_partial(self._h, shard, nshards, x.data_ptr(), direction,
                                                  residues.data_ptr(), C.byref(g),
                                                  _stream_ptr(stream, self.device)))
+        return int(g.value)
+
+    def shard_partial_p2p(self, x: torch.Tensor, shard: int, nshards: int, buffers: list,
+                          direction: int = -1, stream=None) -> int:
+        """shard_partial with the exchange fused into the producing kernels: this shard's
+        residues are stored into every rank's buffer; buffers[r] = rank r's exchange buffer as
+        a device pointer valid here (int, e.g. from ipc_open) or a tensor (include/ozfft.h)."""
+        ptrs = (C.c_void_p * nshards)(*[b.data_ptr() if isinstance(b, torch.Tensor) else int(b)
+                                        for b in buffers])
+        g = C.c_int32(0)
+        with torch.cuda.device(self.device):
+            _check(self._lib.ozfft_shard_partial_p2p(self._h, shard, nshards, x.data_ptr(), direction,
+                                                     ptrs, C.byref(g), _stream_ptr(stream, self.device)))
         return int(g.value)
 
     def shard_finish(self, residues: torch.Tensor, groups: int, out: torch.Tensor, direction: int = -1,

@@ -692,8 +692,9 @@ uint64_t ozfft_shard_residue_bytes(const ozfft_plan* pl, int32_t groups) {
   return (uint64_t)8 * g * pl->n * 4;
 }
 
-ozfft_status ozfft_shard_partial(const ozfft_plan* pl, int shard, int nshards, const void* in,
-                                 int direction, void* residues, int32_t* groups, void* stream) {
+static ozfft_status shard_partial_impl(const ozfft_plan* pl, int shard, int nshards, const void* in,
+                                       int direction, void* residues, void* const* peers,
+                                       int32_t* groups, void* stream) {
   ozfft_status s = check_exec(pl, in, residues, direction);
   if (s) return s;
   if (!groups) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null groups pointer");
@@ -736,9 +737,80 @@ ozfft_status ozfft_shard_partial(const ozfft_plan* pl, int shard, int nshards, c
   // buffer (an in-place all-gather then completes it on every rank)
   a.res_out = reinterpret_cast<uint32_t*>(residues);
   a.res_groups = g;
+  if (peers) {  // peer-memory exchange: the producing kernels store into every rank's buffer
+    a.npeers = nshards;
+    for (int r = 0; r < nshards; ++r) a.res_peers[r] = reinterpret_cast<uint32_t*>(peers[r]);
+  }
   s = launch_execute(*pl, a, stream);
   const_cast<ozfft_plan*>(pl)->last_batch = 1;
   return s;
+}
+
+ozfft_status ozfft_shard_partial(const ozfft_plan* pl, int shard, int nshards, const void* in,
+                                 int direction, void* residues, int32_t* groups, void* stream) {
+  return shard_partial_impl(pl, shard, nshards, in, direction, residues, nullptr, groups, stream);
+}
+
+ozfft_status ozfft_shard_partial_p2p(const ozfft_plan* pl, int shard, int nshards, const void* in,
+                                     int direction, void* const* residues_by_rank, int32_t* groups,
+                                     void* stream) {
+  if (!residues_by_rank) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null residues_by_rank");
+  if (nshards < 1 || nshards > 8 || shard < 0 || shard >= nshards)
+    return fail(OZFFT_ERR_SHARD, "nshards must divide 8 and 0 <= shard < nshards");
+  for (int r = 0; r < nshards; ++r)
+    if (!residues_by_rank[r]) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null rank buffer");
+  return shard_partial_impl(pl, shard, nshards, in, direction, residues_by_rank[shard], residues_by_rank,
+                            groups, stream);
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (no link-time libcuda)
+static ozfft_status alloc_base(const void* dev_ptr, uintptr_t* base) {
+  typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return fail(OZFFT_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+    fn = reinterpret_cast<GetRange>(f);
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+    return fail(OZFFT_ERR_INVALID_ARGUMENT, "pointer is not in a device allocation");
+  *base = (uintptr_t)b;
+  return OZFFT_OK;
+}
+
+ozfft_status ozfft_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset) {
+  if (!dev_ptr || !handle64 || !offset) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle is 64 bytes");
+  uintptr_t base = 0;
+  ozfft_status s = alloc_base(dev_ptr, &base);
+  if (s) return s;
+  cudaIpcMemHandle_t h;
+  s = check_cuda(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+  if (s) return s;
+  std::memcpy(handle64, &h, sizeof(h));
+  *offset = (uint64_t)((uintptr_t)dev_ptr - base);
+  return OZFFT_OK;
+}
+
+ozfft_status ozfft_ipc_open_handle(const void* handle64, uint64_t offset, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  void* base = nullptr;
+  const ozfft_status s =
+      check_cuda(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  if (!s) *dev_ptr = static_cast<char*>(base) + offset;
+  return s;
+}
+
+ozfft_status ozfft_ipc_close(void* dev_ptr, uint64_t offset) {
+  if (!dev_ptr) return fail(OZFFT_ERR_INVALID_ARGUMENT, "null argument");
+  return check_cuda(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset), "cudaIpcCloseMemHandle");
 }
 
 ozfft_status ozfft_shard_finish(const ozfft_plan* pl, const void* residues_all, int32_t groups,

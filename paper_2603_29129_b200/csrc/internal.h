@@ -143,6 +143,8 @@ struct ExecArgs {
                        // (ws0 + nb <= chunk); disjoint slots may run on concurrent streams
   uint32_t* res_out = nullptr;  // unit-sharded transform: residues written here, [unit][res_groups][n]
   int res_groups = 0;
+  uint32_t* res_peers[8] = {};  // ... and also into these buffers (peer memory), if npeers > 0
+  int npeers = 0;
   int phase = 0;       // 0: whole path; 1: split only (stats, schedules); 2: everything after the split
 };
 ozfft_status launch_plan_precompute(Plan& pl, void* stream);

@@ -1071,6 +1071,8 @@ struct ColParams {
   const int32_t* stats;   // [nb][stats_stride]
   const int32_t* sched;   // [nb][4][sched_stride]
   uint32_t unit_mask;
+  uint32_t* res_peers[8];  // unit-sharded transform, peer-memory exchange: residues also stored
+  int npeers;              // into these buffers (same offsets as res)
   int image;              // f2: the forward vectors are the digit images D_re +- iota D_im
   uint2 io[2][2];         // [q][image] Shoup pair of iota_q (image 0) or p_q - iota_q (1)
 };
@@ -1264,13 +1266,22 @@ __global__ void __launch_bounds__(256) k_col_inv(ColParams P) {
     for (int i = 0; i < E; ++i) cur[i] = nxt[i];
     if (g + 1 < ng) fetch(g + 1);
     if (g > 0) __syncthreads();  // smem tile free
-    uint32_t* out = P.res + (((b * 4 + cv) * 2 + q) * P.rg + g) * P.n + col;
+    const int64_t ooff = (((b * 4 + cv) * 2 + q) * P.rg + g) * P.n + col;
+    uint32_t* out = P.res + ooff;
     sub_ntt<LOGR, true, Cb, LOGE>(
         tv, smem + c, col, C, T, p, [&](int i, uint32_t) -> uint32_t { return cur[i]; },
         [&](int, uint32_t e, uint32_t val) {
-          if (e * C < lim) out[e * C] = val;
+          if (e * C < lim) {
+            out[e * C] = val;
+            // peer-memory exchange: the same residue into every other rank's buffer
+            for (int r = 0; r < P.npeers; ++r)
+              if (P.res_peers[r] != P.res) P.res_peers[r][ooff + (int64_t)e * C] = val;
+          }
         });
   }
+  // peer stores visible system-wide before anything this rank signals afterwards (the
+  // barrier / collective the caller orders after the kernel)
+  if (P.npeers > 0) __threadfence_system();
 }
 
 // ============================================================== fused row kernel
@@ -1292,6 +1303,8 @@ struct RowParams {
   const int32_t* stats;
   const int32_t* sched;
   uint32_t unit_mask;
+  uint32_t* res_peers[8];  // as ColParams (one-pass plans write residues in the row kernel)
+  int npeers;
   int fwd_only;           // 1: write the forward spectra (internal order) to Xout, stop
   uint32_t* Xout;         // fwd_only or tap: [nb][2 q][2 a][K][m]
   uint32_t* Zout;         // tap: [nb][2 q][4][K*K][m] (internal order, W m^{-1} scaled)
@@ -1699,9 +1712,15 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
           return z[i];
         },
         [&](int, uint32_t e, uint32_t val) {
-          if (e < nlim) op[e] = val;
+          if (e < nlim) {
+            op[e] = val;
+            if constexpr (!TWO_PASS)  // peer-memory exchange (unit-sharded single transform)
+              for (int r = 0; r < P.npeers; ++r)
+                if (P.res_peers[r] != P.res) P.res_peers[r][(op - P.res) + e] = val;
+          }
         });
   }
+  if (!TWO_PASS && P.npeers > 0) __threadfence_system();  // as k_col_inv
 }
 
 // ============================================================== CRT + recombination
@@ -3281,6 +3300,8 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.tw = tw; CP.digits = SP.digits; CP.in_len = n; CP.Y = Y; CP.stats = stats;
     CP.sched = sched; CP.G = Gb; CP.res = res; CP.rg = rg; CP.n = n; CP.unit_mask = A.unit_mask;
     CP.image = pl.image;
+    CP.npeers = A.npeers;
+    for (int r = 0; r < 8; ++r) CP.res_peers[r] = A.res_peers[r];
     fill_iota(pl, CP.io);
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 4;
     prof_mark(pl, OZFFT_STAGE_COL_FWD, true, st);
@@ -3295,6 +3316,8 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
   RP.p[0] = pl.p[0]; RP.p[1] = pl.p[1]; RP.tw = tw; RP.digits = SP.digits; RP.in_len = n;
   RP.Y = Y; RP.W = W; RP.pinv[0] = pl.pinv[0]; RP.pinv[1] = pl.pinv[1]; RP.G = Gb; RP.res = res; RP.rg = rg; RP.n = n; RP.stats = stats; RP.sched = sched;
   RP.unit_mask = A.unit_mask; RP.fwd_only = 0; RP.Xout = Xtap; RP.Zout = Ztap;
+  RP.npeers = A.npeers;
+  for (int r = 0; r < 8; ++r) RP.res_peers[r] = A.res_peers[r];
   RP.image = pl.image;
   fill_iota(pl, RP.io);
   {
@@ -3379,6 +3402,8 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     CP.nb = nb; CP.K = K; CP.L = L; CP.p[0] = pl.p[0]; CP.p[1] = pl.p[1];
     CP.tw = tw; CP.stats = stats; CP.sched = sched; CP.G = Gb; CP.res = res; CP.rg = rg; CP.n = n;
     CP.unit_mask = A.unit_mask;
+    CP.npeers = A.npeers;
+    for (int r = 0; r < 8; ++r) CP.res_peers[r] = A.res_peers[r];
     const int64_t nblk = (1ll << (pl.logC - c.logCb)) * nb * 8;
     prof_mark(pl, OZFFT_STAGE_COL_INV, true, st);
     launch_col_inv(pl.logR, pl.logC, (unsigned)nblk, c, st, CP);
