@@ -214,8 +214,29 @@ def run_single(args, cfg, rank, world, local_rank):
     out = torch.empty(n, dtype=torch.complex128, device=dev)
     ag = []  # (start, end) events around the all-gather of each timed step
     gsz = [0]
+    p2p = getattr(args, "p2p", False)
+    peers = [residues.data_ptr()]
+    if p2p and world > 1:  # every rank's exchange buffer mapped into this process (CUDA IPC)
+        handles = [None] * world
+        dist.all_gather_object(handles, oz.ipc_handle(residues))
+        peers = [residues.data_ptr() if r == rank else oz.ipc_open(handles[r], dev) for r in range(world)]
+    token = torch.zeros(1, device=dev)
 
     def step(record=False):
+        if p2p:
+            # the producing kernels store every residue into every rank's buffer; a one-word
+            # all-reduce on the stream is the device-side barrier before the finish
+            g = plan.shard_partial_p2p(x, rank, world, peers)
+            gsz[0] = g
+            if world > 1:
+                if record:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                dist.all_reduce(token)
+                if record:
+                    e1.record(stream)
+                    ag.append((e0, e1))
+            return plan.shard_finish(residues, g, out)
         g = plan.shard_partial(x, rank, world, residues)
         gsz[0] = g
         if world > 1:
@@ -256,7 +277,14 @@ def run_single(args, cfg, rank, world, local_rank):
         nbytes = plan.shard_residue_bytes(gsz[0])
         ag_per = ag_ms / args.steps
         busbw = (nbytes * (world - 1) / world) / (ag_per * 1e-3) / 1e9 if ag_per > 0 else None
-        allgather = {"ms_per_step": ag_per, "bytes": nbytes, "groups": gsz[0],
+        if p2p:
+            allgather = {"ms_per_step": ag_per, "bytes": nbytes, "groups": gsz[0],
+                         "note": "peer-memory exchange fused into the inverse-NTT epilogue (stores "
+                                 "into every rank's buffer through CUDA IPC mappings); ms_per_step "
+                                 "is the one-word all-reduce used as the barrier after it"}
+        else:
+            allgather = None
+        allgather = allgather or {"ms_per_step": ag_per, "bytes": nbytes, "groups": gsz[0],
                      "busbw_GBs": busbw,
                      "frac_of_peer_copy_770GBs": busbw / 770.0 if busbw else None,
                      "note": "in-place NCCL all_gather_into_tensor of the inverse-NTT residues "
@@ -268,8 +296,10 @@ def run_single(args, cfg, rank, world, local_rank):
                 "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u32", "data": "synthetic",
                 "config": {"workload": f"single-transform variant of {cfg.name}: transform 0, n={n}, "
-                                       f"units (prime, conv) split over {world} rank(s), one NCCL "
-                                       "all-gather of the residues before CRT",
+                                       f"units (prime, conv) split over {world} rank(s), "
+                                       + ("residues stored into every rank's buffer by the producing "
+                                          "kernels (peer memory)" if p2p else
+                                          "one NCCL all-gather of the residues") + " before CRT",
                            "n": n, "m": plan.m, "parallelism": f"unit-sharded x{world}",
                            "residue_bytes_gathered": nbytes if world > 1 else 0},
                 "gpu_launches": int(oz.kernel_launches() - launches0),
@@ -613,6 +643,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--conv", default="padded", choices=["padded", "cyclic"],
                     help="Bluestein length: m >= 2n-1 (north star) or m = n (P:238-241)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="--mode single: the residue exchange fused into the producing kernels "
+                         "(peer-memory stores through CUDA IPC mappings) instead of an NCCL all-gather")
     ap.add_argument("--mode", default="batch", choices=["batch", "single"],
                     help="batch: the configured batch sharded over the ranks (the headline); "
                          "single: one transform sharded over the ranks by (prime, conv) units "
