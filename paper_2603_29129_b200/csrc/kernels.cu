@@ -1118,6 +1118,10 @@ __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32
 #ifndef OZ_CI_SNAKE_MAX
 #define OZ_CI_SNAKE_MAX 7
 #endif
+#ifndef OZ_CI_DB
+#define OZ_CI_DB 0  // k_col_inv_crt: double-buffered exchange tile (measured slower: c3 873 vs 763 us,
+                    // the larger shared-memory carveout leaves less L1 for the column twiddles)
+#endif
 #ifndef OZ_CI_T0S
 #define OZ_CI_T0S 8  // k_col_inv_crt: step-1 round column twiddles staged in shared memory
 #endif  // for log2 R >= this (c3 803 -> 769 us; shorter columns lose: c4 658 -> 715, c2 132 -> 215,
@@ -2478,7 +2482,11 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
     s_sc[g] = scalbn(1.0, -s_ce[g]);
   }
   constexpr uint32_t TILE = ((1u << LOGR) + (1u << LOGR) / E + 1) * Cb;
-  double2* Sacc = reinterpret_cast<double2*>(smem + ((TILE + 3) & ~3u));  // [NH][THREADS], 16B-aligned
+  constexpr uint32_t TILEW = (TILE + 3) & ~3u;
+  // OZ_CI_DB: two exchange tiles used alternately, so a tile's exchange writes never meet
+  // the previous tile's reads and the per-tile "tile free" barrier goes (the extra 17 KB
+  // keep 3 CTAs per SM: registers bound the occupancy)
+  double2* Sacc = reinterpret_cast<double2*>(smem + (OZ_CI_DB ? 2 : 1) * TILEW);  // [NH][THREADS]
 #pragma unroll
   for (int i = 0; i < NH; ++i) Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
   // OZ_CI_T0S: for long columns, the step-1 round's column twiddles of both primes (the same
@@ -2513,18 +2521,19 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
 #pragma unroll
     for (int i = 0; i < E; ++i) cur[i] = nxt[i];
     if (t + 1 < 2 * ng) fetch(t + 1);
-    if (t > 0) __syncthreads();  // smem tile free
+    if (!OZ_CI_DB && t > 0) __syncthreads();  // smem tile free
+    uint32_t* const tb = smem + (OZ_CI_DB ? (uint32_t)(t & 1) * TILEW : 0u);
     const uint32_t p = q ? P.F.p1 : P.F.p0;
     const uint2* T = P.tw + (size_t)(q * 2 + 1) * m;
     uint32_t rr[NH];
     if constexpr (kT0S)
-      sub_ntt_t0<LOGR, true, Cb, LOGE>(tv, smem + c, col, C, T, Tw0{tw0 + q * (Cb << S1), (uint32_t)c, (uint32_t)Cb}, p,
+      sub_ntt_t0<LOGR, true, Cb, LOGE>(tv, tb + c, col, C, T, Tw0{tw0 + q * (Cb << S1), (uint32_t)c, (uint32_t)Cb}, p,
                               [&](int i, uint32_t) -> uint32_t { return cur[i]; },
                               [&](int i, uint32_t, uint32_t val) {
                                 if (needed(i)) rr[hslot(i)] = val;  // rows >= R/2 never needed
                               });
     else
-      sub_ntt<LOGR, true, Cb, LOGE>(tv, smem + c, col, C, T, p,
+      sub_ntt<LOGR, true, Cb, LOGE>(tv, tb + c, col, C, T, p,
                               [&](int i, uint32_t) -> uint32_t { return cur[i]; },
                               [&](int i, uint32_t, uint32_t val) {
                                 if (needed(i)) rr[hslot(i)] = val;  // rows >= R/2 never needed
@@ -3355,7 +3364,8 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     const size_t tile = ((1ull << pl.logR) + ((1ull << pl.logR) >> cle) + 1) * (1ull << lcb);
     const bool prune = 2 * n <= m;  // padded plans; cyclic plans (m = n) need every row
     const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / (prune ? 2 : 1);
-    const size_t smem = ((tile + 3) & ~(size_t)3) * 4 + (size_t)nh * threads * 16 * (pl.image ? 2 : 1) +
+    const size_t smem = ((tile + 3) & ~(size_t)3) * 4 * (!pl.image && OZ_CI_DB ? 2 : 1) +
+                        (size_t)nh * threads * 16 * (pl.image ? 2 : 1) +
                         (!pl.image && OZ_CI_T0S && pl.logR >= OZ_CI_T0S
                              ? (size_t)2 * ((size_t)1 << col_s1(pl.logR)) * ((size_t)1 << lcb) * 8 : 0);
     const int64_t nblk = (1ll << (pl.logC - lcb)) * nb * (pl.image ? 1 : 4);
