@@ -1118,6 +1118,11 @@ __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32
 #ifndef OZ_CI_SNAKE_MAX
 #define OZ_CI_SNAKE_MAX 7
 #endif
+#ifndef OZ_CI_RACC
+#define OZ_CI_RACC 0  // k_col_inv_crt: DD accumulators in registers (<= 8 slots per thread); measured
+                      // slower: c3 821 us at 127 registers / 2 CTAs, 931 at 80 / 3 (spills), vs 763
+#endif
+__host__ __device__ constexpr bool ci_racc(int nh) { return OZ_CI_RACC && nh <= 8; }
 #ifndef OZ_CI_DB
 #define OZ_CI_DB 0  // k_col_inv_crt: double-buffered exchange tile (measured slower: c3 873 vs 763 us,
                     // the larger shared-memory carveout leaves less L1 for the column twiddles)
@@ -2487,14 +2492,23 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   // the previous tile's reads and the per-tile "tile free" barrier goes (the extra 17 KB
   // keep 3 CTAs per SM: registers bound the occupancy)
   double2* Sacc = reinterpret_cast<double2*>(smem + (OZ_CI_DB ? 2 : 1) * TILEW);  // [NH][THREADS]
+  // OZ_CI_RACC: the DD accumulators in registers instead of shared memory (frees 32 KB per
+  // CTA for L1, where the column twiddles live)
+  constexpr bool kRacc = ci_racc(NH);
+  double2 racc[kRacc ? NH : 1];
 #pragma unroll
-  for (int i = 0; i < NH; ++i) Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
+  for (int i = 0; i < NH; ++i) {
+    if constexpr (kRacc)
+      racc[i] = make_double2(0.0, 0.0);
+    else
+      Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
+  }
   // OZ_CI_T0S: for long columns, the step-1 round's column twiddles of both primes (the same
   // for every group of the CTA) are staged in shared memory once, after the accumulators (ncu
   // at c3: the first product of each tile waited on these L2 loads, 13 % of the samples)
   constexpr int S1 = col_s1(LOGR);
   constexpr bool kT0S = OZ_CI_T0S != 0 && LOGR >= OZ_CI_T0S;
-  [[maybe_unused]] uint2* tw0 = reinterpret_cast<uint2*>(Sacc + NH * THREADS);  // [2 q][2^S1][Cb]
+  [[maybe_unused]] uint2* tw0 = reinterpret_cast<uint2*>(Sacc + (kRacc ? 0 : NH * THREADS));  // [2 q][2^S1][Cb]
   if constexpr (kT0S) {
     for (int q = 0; q < 2; ++q)
       stage_col_tw0<S1, Cb>(tw0 + q * (Cb << S1), P.tw + (size_t)(q * 2 + 1) * m, C, cb << LOGCB);
@@ -2577,7 +2591,10 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
           if (h0 + j < NH) {
             const int h = h0 + j;
             Z[j] = q ? garner2(r0[h], rr[h], P.F) : garner2(rr[h], r0[h], P.F);
-            acc[j] = Sacc[h * THREADS + tid];
+            if constexpr (kRacc)
+              acc[j] = racc[h];
+            else
+              acc[j] = Sacc[h * THREADS + tid];
           }
 #pragma unroll
         for (int j = 0; j < NB; ++j)
@@ -2592,7 +2609,12 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
           }
 #pragma unroll
         for (int j = 0; j < NB; ++j)
-          if (h0 + j < NH) Sacc[(h0 + j) * THREADS + tid] = acc[j];
+          if (h0 + j < NH) {
+            if constexpr (kRacc)
+              racc[h0 + j] = acc[j];
+            else
+              Sacc[(h0 + j) * THREADS + tid] = acc[j];
+          }
       }
     }
   }
@@ -2601,7 +2623,12 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   for (int i = 0; i < CNTL; ++i) {
     if (!needed(i)) continue;
     const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, i);
-    if (e * C < lim) So[e * C] = Sacc[hslot(i) * THREADS + tid];
+    if (e * C < lim) {
+      if constexpr (kRacc)
+        So[e * C] = racc[hslot(i)];
+      else
+        So[e * C] = Sacc[hslot(i) * THREADS + tid];
+    }
   }
 }
 
@@ -3365,7 +3392,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     const bool prune = 2 * n <= m;  // padded plans; cyclic plans (m = n) need every row
     const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / (prune ? 2 : 1);
     const size_t smem = ((tile + 3) & ~(size_t)3) * 4 * (!pl.image && OZ_CI_DB ? 2 : 1) +
-                        (size_t)nh * threads * 16 * (pl.image ? 2 : 1) +
+                        (!pl.image && ci_racc(nh) ? 0 : (size_t)nh * threads * 16 * (pl.image ? 2 : 1)) +
                         (!pl.image && OZ_CI_T0S && pl.logR >= OZ_CI_T0S
                              ? (size_t)2 * ((size_t)1 << col_s1(pl.logR)) * ((size_t)1 << lcb) * 8 : 0);
     const int64_t nblk = (1ll << (pl.logC - lcb)) * nb * (pl.image ? 1 : 4);
