@@ -2094,6 +2094,9 @@ struct SmallParams {
   int fault;                // test-only residue corruption (as k_fault_inject)
 };
 constexpr int kSmallLogE = 3;  // 8 elements per thread and round
+#ifndef OZ_SMALL_FWD3
+#define OZ_SMALL_FWD3 1  // k_small_fused: the three forward spectra as one NV = 3 pass
+#endif
 #ifndef OZ_SMALL_EPT
 #define OZ_SMALL_EPT 4
 #endif
@@ -2296,7 +2299,7 @@ __global__ void __launch_bounds__(small_threads(LOGC)) k_small_fused(SmallParams
   const uint32_t* Wq = STAGE ? s_W : gW;
   const int ka = bad ? 0 : kvf[a];
   uint32_t* const wk3[3] = {work, work + padm, work + 2 * padm};
-  if (ka == 3) {  // the three slices as one NV = 3 pass (shared twiddle loads, 3x ILP)
+  if (OZ_SMALL_FWD3 && ka == 3) {  // the three slices as one NV = 3 pass (shared twiddle loads, 3x ILP)
     __syncthreads();  // xp reads done
     sub_ntt_multi<LOGC, false, 1, 3, kSmallLogE, true, false, false, STAGE>(
         tid, wk3, 0u, 1u, Tf, Tw0{nullptr, 0u, 0u}, p,
