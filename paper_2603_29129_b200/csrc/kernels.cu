@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <type_traits>
 
@@ -2937,6 +2938,9 @@ static int sm_count() {
   }
   return v;
 }
+#ifndef OZ_ROW_Z_WAVES
+#define OZ_ROW_Z_WAVES 0  // two-pass rows: item split when the grid has fewer waves than this
+#endif
 #ifndef OZ_ROW_ZMAX
 #define OZ_ROW_ZMAX 18  // most CTAs one (transform, part, prime) row of a one-pass plan uses
 #endif
@@ -3366,6 +3370,21 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
       int64_t z = ctas < sm_count() ? sm_count() / ctas : 1;
       z = z > 2 * K * K ? 2 * K * K : (z < 1 ? 1 : z);
       grid.z = (unsigned)(z > OZ_ROW_ZMAX ? OZ_ROW_ZMAX : z);
+    } else {
+      // small batches of two-pass plans: split each row's (conv, group) items over z CTAs
+      // (each recomputes the row's forward spectra) so that the grid fills more waves
+      static const int zknob = [] {
+        const char* t = std::getenv("OZFFT_ROW_Z");  // tuning knob (tools/)
+        return t ? std::atoi(t) : 0;
+      }();
+      int64_t z = 1;
+      if (zknob > 0) {
+        z = zknob;
+      } else {
+        const int64_t ctas = nb * (4ll << pl.logR);
+        while (z < 2 && ctas * z < (int64_t)OZ_ROW_Z_WAVES * sm_count() * OZ_ROW_MINB) z *= 2;
+      }
+      grid.z = (unsigned)(z > 2 * K * K ? 2 * K * K : z);
     }
     prof_mark(pl, OZFFT_STAGE_ROW_FUSED, true, st);
     launch_row(pl.logC, pl.logR, grid, c, st, RP);
