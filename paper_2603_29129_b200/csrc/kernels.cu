@@ -820,7 +820,10 @@ __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_
   }
 }
 // DIT stages h = gstep .. gstep*2^(S-1): v' = v * Tinv[h + (pos mod h)]; (u + v', u - v')
-template <int S, int NV, int E, bool UNIT = false, bool SMEM_T = false>
+// CANON0: the group's inputs are canonical (< p; the first round of an inverse row item reads
+// the pointwise REDC outputs), so the w^0 = 1 butterflies of the first stage skip the
+// canonicalising min of v (it only guards the lazy < 2p values of later stages)
+template <int S, int NV, int E, bool UNIT = false, bool SMEM_T = false, bool CANON0 = false>
 __device__ __forceinline__ void dit_group(uint32_t (&x)[NV][E], int off, uint32_t rmod,
                                           uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
   if constexpr (UNIT) {
@@ -841,7 +844,7 @@ __device__ __forceinline__ void dit_group(uint32_t (&x)[NV][E], int off, uint32_
       for (int v = 0; v < NV; ++v) {
         const uint32_t a = x[v][off + k];  // always canonical: it was a "u" of this stage
         const uint32_t vin = x[v][off + k + d];  // may be lazy (< 2p)
-        const uint32_t b = one ? min(vin, vin - p) : mul_shoup(vin, w, p);
+        const uint32_t b = one ? ((CANON0 && st == 0) ? vin : min(vin, vin - p)) : mul_shoup(vin, w, p);
         if (st + 1 < S && (k & (2 * d))) {
           // both outputs are the "v" operand of the next stage, whose Shoup product
           // accepts any 32-bit input: keep them in [0, 2p), skip the subtractions
@@ -951,7 +954,8 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
       else
         dif_group<RT::S, NV, E, false, true, zhi>(x, u * (1 << RT::S), t0.gb, t0.gs, t0.T, p);
     } else if constexpr (INV) {
-      dit_group<RT::S, NV, E, unit, TGEN>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+      // round 0 reads load_first's values: canonical for every UNIT (row) caller
+      dit_group<RT::S, NV, E, unit, TGEN, unit && R == 0>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     } else {
       dif_group<RT::S, NV, E, unit, TGEN, zhi>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     }
