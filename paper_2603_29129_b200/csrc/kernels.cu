@@ -823,7 +823,9 @@ __device__ __forceinline__ void dif_group(uint32_t (&x)[NV][E], int off, uint32_
 // CANON0: the group's inputs are canonical (< p; the first round of an inverse row item reads
 // the pointwise REDC outputs), so the w^0 = 1 butterflies of the first stage skip the
 // canonicalising min of v (it only guards the lazy < 2p values of later stages)
-template <int S, int NV, int E, bool UNIT = false, bool SMEM_T = false, bool CANON0 = false>
+// LZ: the last stage leaves its outputs lazy (< 2p): only for outputs that are consumed as
+// the v-operand of a Shoup product (two-pass rows of odd index, see k_row_fused)
+template <int S, int NV, int E, bool UNIT = false, bool SMEM_T = false, bool CANON0 = false, bool LZ = false>
 __device__ __forceinline__ void dit_group(uint32_t (&x)[NV][E], int off, uint32_t rmod,
                                           uint32_t gstep, const uint2* __restrict__ T, uint32_t p) {
   if constexpr (UNIT) {
@@ -845,7 +847,7 @@ __device__ __forceinline__ void dit_group(uint32_t (&x)[NV][E], int off, uint32_
         const uint32_t a = x[v][off + k];  // always canonical: it was a "u" of this stage
         const uint32_t vin = x[v][off + k + d];  // may be lazy (< 2p)
         const uint32_t b = one ? ((CANON0 && st == 0) ? vin : min(vin, vin - p)) : mul_shoup(vin, w, p);
-        if (st + 1 < S && (k & (2 * d))) {
+        if ((st + 1 < S && (k & (2 * d))) || (LZ && st + 1 == S)) {
           // both outputs are the "v" operand of the next stage, whose Shoup product
           // accepts any 32-bit input: keep them in [0, 2p), skip the subtractions
           x[v][off + k] = a + b;
@@ -925,7 +927,7 @@ struct Tw0 {
 };
 
 template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, bool ZHI,
-          bool TGEN, class LoadF, class StoreF>
+          bool TGEN, bool LZ, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int tv,
                                               uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
@@ -955,7 +957,8 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
         dif_group<RT::S, NV, E, false, true, zhi>(x, u * (1 << RT::S), t0.gb, t0.gs, t0.T, p);
     } else if constexpr (INV) {
       // round 0 reads load_first's values: canonical for every UNIT (row) caller
-      dit_group<RT::S, NV, E, unit, TGEN, unit && R == 0>(x, u * (1 << RT::S), rmod, step * gs, T, p);
+      dit_group<RT::S, NV, E, unit, TGEN, unit && R == 0, LZ && R == RT::nr - 1>(x, u * (1 << RT::S), rmod,
+                                                                            step * gs, T, p);
     } else {
       dif_group<RT::S, NV, E, unit, TGEN, zhi>(x, u * (1 << RT::S), rmod, step * gs, T, p);
     }
@@ -978,16 +981,16 @@ __device__ __forceinline__ void sub_ntt_round(uint32_t (&x)[NV][1 << LOGE], int 
 }
 
 template <int LOGN, bool INV, int R, int CB, int NV, int LOGE, bool UNIT, bool T0S, bool ZHI,
-          bool TGEN, class LoadF, class StoreF>
+          bool TGEN, bool LZ, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int tv,
                                                uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                                uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
                                                uint32_t p, LoadF& load_first, StoreF& store_last) {
   if constexpr (R < RoundT<LOGN, INV, 0, LOGE>::nr) {
-    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE, UNIT, T0S, ZHI, TGEN>(x, tv, sm, gb_mod, gs, T, t0, p,
-                                                               load_first, store_last);
-    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE, UNIT, T0S, ZHI, TGEN>(x, tv, sm, gb_mod, gs, T, t0, p,
-                                                                    load_first, store_last);
+    sub_ntt_round<LOGN, INV, R, CB, NV, LOGE, UNIT, T0S, ZHI, TGEN, LZ>(x, tv, sm, gb_mod, gs, T, t0, p,
+                                                                   load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, R + 1, CB, NV, LOGE, UNIT, T0S, ZHI, TGEN, LZ>(x, tv, sm, gb_mod, gs, T, t0, p,
+                                                                        load_first, store_last);
   }
 }
 
@@ -1002,7 +1005,7 @@ __device__ __forceinline__ void sub_ntt_rounds(uint32_t (&x)[NV][1 << LOGE], int
 // consumes the final values.  The buffers must be free for writes on entry.  UNIT: the
 // caller passes gb_mod == 0 and gs == 1 (rows), enabling the compile-time step-1 round.
 template <int LOGN, bool INV, int CB, int NV, int LOGE = 4, bool UNIT = false, bool T0S = false,
-          bool ZHI = false, bool TGEN = false, class LoadF, class StoreF>
+          bool ZHI = false, bool TGEN = false, bool LZ = false, class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV], uint32_t gb_mod,
                                               uint32_t gs, const uint2* __restrict__ T, Tw0 t0,
                                               uint32_t p, LoadF&& load_first, StoreF&& store_last) {
@@ -1012,20 +1015,20 @@ __device__ __forceinline__ void sub_ntt_multi(int tv, uint32_t* const (&sm)[NV],
       for (int v = 0; v < NV; ++v) store_last(v, 0, 0u, load_first(v, 0, 0u));
   } else {
     uint32_t x[NV][1 << LOGE];
-    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE, UNIT, T0S, ZHI, TGEN>(x, tv, sm, gb_mod, gs, T, t0, p,
-                                                                load_first, store_last);
+    sub_ntt_rounds<LOGN, INV, 0, CB, NV, LOGE, UNIT, T0S, ZHI, TGEN, LZ>(x, tv, sm, gb_mod, gs, T, t0, p,
+                                                                    load_first, store_last);
   }
 }
 
 // Single-vector form: load_first(i, e), store_last(i, e, val).  TGEN: T may point to shared
 // memory (generic loads instead of the read-only global path).
-template <int LOGN, bool INV, int CB, int LOGE = 4, bool UNIT = false, bool TGEN = false, class LoadF,
-          class StoreF>
+template <int LOGN, bool INV, int CB, int LOGE = 4, bool UNIT = false, bool TGEN = false, bool LZ = false,
+          class LoadF, class StoreF>
 __device__ __forceinline__ void sub_ntt(int tv, uint32_t* __restrict__ sm, uint32_t gb_mod,
                                         uint32_t gs, const uint2* __restrict__ T, uint32_t p,
                                         LoadF&& load_first, StoreF&& store_last) {
   uint32_t* const sms[1] = {sm};
-  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, UNIT, false, false, TGEN>(
+  sub_ntt_multi<LOGN, INV, CB, 1, LOGE, UNIT, false, false, TGEN, LZ>(
       tv, sms, gb_mod, gs, T, Tw0{nullptr, 0u, 0u}, p,
       [&](int, int i, uint32_t e) { return load_first(i, e); },
       [&](int, int i, uint32_t e, uint32_t v) { store_last(i, e, v); });
@@ -1327,6 +1330,10 @@ struct RowParams {
   uint2 io[2][2];         // [q][image] Shoup pair of iota_q / p_q - iota_q
 };
 
+#ifndef OZ_ROW_LAZYG
+#define OZ_ROW_LAZYG 0  // two-pass rows of odd index store G lazily (< 2p), see k_row_fused; off:
+                        // the second inverse instance costs more (c3 row 1102 vs 1026 us) than it saves
+#endif
 #ifndef OZ_ROW_QMAJOR
 #define OZ_ROW_QMAJOR 1
 #endif
@@ -1719,20 +1726,29 @@ __global__ void __launch_bounds__(RowCfg<LOGC, TWO_PASS>::threads, RowCfg<LOGC, 
     pointwise(ci0, g0, z);
     uint32_t* const zt = ztap_ptr(ci0, g0);
     uint32_t* const op = out_ptr(ci0, g0);
-    sub_ntt<LOGC, true, 1, LOGE, true>(
-        tv, wk, 0u, 1u, Ti, p,
-        [&](int i, uint32_t e) -> uint32_t {
-          if (zt) zt[e] = z[i];
-          return z[i];
-        },
-        [&](int, uint32_t e, uint32_t val) {
-          if (e < nlim) {
-            op[e] = val;
-            if constexpr (!TWO_PASS)  // peer-memory exchange (unit-sharded single transform)
-              for (int r = 0; r < P.npeers; ++r)
-                if (P.res_peers[r] != P.res) P.res_peers[r][(op - P.res) + e] = val;
-          }
-        });
+    auto inverse = [&](auto lz) {
+      sub_ntt<LOGC, true, 1, LOGE, true, false, decltype(lz)::value>(
+          tv, wk, 0u, 1u, Ti, p,
+          [&](int i, uint32_t e) -> uint32_t {
+            if (zt) zt[e] = z[i];
+            return z[i];
+          },
+          [&](int, uint32_t e, uint32_t val) {
+            if (e < nlim) {
+              op[e] = val;
+              if constexpr (!TWO_PASS)  // peer-memory exchange (unit-sharded single transform)
+                for (int r = 0; r < P.npeers; ++r)
+                  if (P.res_peers[r] != P.res) P.res_peers[r][(op - P.res) + e] = val;
+            }
+          });
+    };
+    // Two-pass plans: G row `row` of an odd index is, in every column kernel, the v-operand of
+    // the first DIT stage (rows 2i, 2i + 1), i.e. the input of a Shoup product, which accepts
+    // any 32-bit value -- so odd rows leave the last stage's outputs lazy (< 2p).
+    if (TWO_PASS && OZ_ROW_LAZYG && (row & 1u))
+      inverse(std::integral_constant<bool, true>{});
+    else
+      inverse(std::integral_constant<bool, false>{});
   }
   if (!TWO_PASS && P.npeers > 0) __threadfence_system();  // as k_col_inv
 }
