@@ -1131,6 +1131,11 @@ __host__ __device__ constexpr int col_loge(int logR) { return logR >= OZ_COL_E32
                       // slower: c3 821 us at 127 registers / 2 CTAs, 931 at 80 / 3 (spills), vs 763
 #endif
 __host__ __device__ constexpr bool ci_racc(int nh) { return OZ_CI_RACC && nh <= 8; }
+#ifndef OZ_CI_GACC
+#define OZ_CI_GACC 0  // k_col_inv_crt: DD accumulators read-modify-written in place in the output S
+#endif                // (L2-resident, .cg) instead of 32 KB of shared memory per CTA: more L1 for the
+                      // column twiddles
+__host__ __device__ constexpr bool ci_gacc(int nh) { return OZ_CI_GACC && !ci_racc(nh); }
 #ifndef OZ_CI_DB
 #define OZ_CI_DB 0  // k_col_inv_crt: double-buffered exchange tile (measured slower: c3 873 vs 763 us,
                     // the larger shared-memory carveout leaves less L1 for the column twiddles)
@@ -2519,20 +2524,25 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   // OZ_CI_RACC: the DD accumulators in registers instead of shared memory (frees 32 KB per
   // CTA for L1, where the column twiddles live)
   constexpr bool kRacc = ci_racc(NH);
+  constexpr bool kGacc = ci_gacc(NH);
   double2 racc[kRacc ? NH : 1];
 #pragma unroll
   for (int i = 0; i < NH; ++i) {
     if constexpr (kRacc)
       racc[i] = make_double2(0.0, 0.0);
-    else
+    else if constexpr (!kGacc)
       Sacc[i * THREADS + tid] = make_double2(0.0, 0.0);
   }
+  // OZ_CI_GACC: slot h of this thread is output row hrow(h) of its column
+  auto islot = [](int h) {
+    return PRUNE ? ((h >> (SL - 1)) << SL) + (h & ((1 << (SL - 1)) - 1)) : h;
+  };
   // OZ_CI_T0S: for long columns, the step-1 round's column twiddles of both primes (the same
   // for every group of the CTA) are staged in shared memory once, after the accumulators (ncu
   // at c3: the first product of each tile waited on these L2 loads, 13 % of the samples)
   constexpr int S1 = col_s1(LOGR);
   constexpr bool kT0S = OZ_CI_T0S != 0 && LOGR >= OZ_CI_T0S;
-  [[maybe_unused]] uint2* tw0 = reinterpret_cast<uint2*>(Sacc + (kRacc ? 0 : NH * THREADS));  // [2 q][2^S1][Cb]
+  [[maybe_unused]] uint2* tw0 = reinterpret_cast<uint2*>(Sacc + (kRacc || kGacc ? 0 : NH * THREADS));  // [2 q][2^S1][Cb]
   if constexpr (kT0S) {
     for (int q = 0; q < 2; ++q)
       stage_col_tw0<S1, Cb>(tw0 + q * (Cb << S1), P.tw + (size_t)(q * 2 + 1) * m, C, cb << LOGCB);
@@ -2553,6 +2563,7 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   if (ng > 0) fetch(0);
   __syncthreads();  // s_sc ready
   uint32_t r0[NH];  // the group's first tile's residues
+  double2* const So = P.S + (b * 4 + cv) * P.n + col;
   for (int t = 0; t < 2 * ng; ++t) {
     const int g = t >> 1, q = tile_q(t);
     uint32_t cur[E];
@@ -2615,10 +2626,14 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
           if (h0 + j < NH) {
             const int h = h0 + j;
             Z[j] = q ? garner2(r0[h], rr[h], P.F) : garner2(rr[h], r0[h], P.F);
-            if constexpr (kRacc)
+            if constexpr (kRacc) {
               acc[j] = racc[h];
-            else
+            } else if constexpr (kGacc) {
+              const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, islot(h));
+              acc[j] = (g > 0 && e * C < lim) ? __ldcg(&So[e * C]) : make_double2(0.0, 0.0);
+            } else {
               acc[j] = Sacc[h * THREADS + tid];
+            }
           }
 #pragma unroll
         for (int j = 0; j < NB; ++j)
@@ -2634,15 +2649,19 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
 #pragma unroll
         for (int j = 0; j < NB; ++j)
           if (h0 + j < NH) {
-            if constexpr (kRacc)
+            if constexpr (kRacc) {
               racc[h0 + j] = acc[j];
-            else
+            } else if constexpr (kGacc) {
+              const uint32_t e = round_elem<LOGR, true, NR - 1, LOGE>(tv, islot(h0 + j));
+              if (e * C < lim) __stcg(&So[e * C], acc[j]);
+            } else {
               Sacc[(h0 + j) * THREADS + tid] = acc[j];
+            }
           }
       }
     }
   }
-  double2* So = P.S + (b * 4 + cv) * P.n + col;
+  if (kGacc && ng > 0) return;  // the sums are already in place
 #pragma unroll
   for (int i = 0; i < CNTL; ++i) {
     if (!needed(i)) continue;
@@ -2650,6 +2669,8 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
     if (e * C < lim) {
       if constexpr (kRacc)
         So[e * C] = racc[hslot(i)];
+      else if constexpr (kGacc)
+        So[e * C] = make_double2(0.0, 0.0);  // no groups: the zero sum
       else
         So[e * C] = Sacc[hslot(i) * THREADS + tid];
     }
@@ -3434,7 +3455,7 @@ ozfft_status launch_execute(const Plan& pl, const ExecArgs& A, void* stream) {
     const bool prune = 2 * n <= m;  // padded plans; cyclic plans (m = n) need every row
     const int nh = (pl.logR >= cle ? (1 << cle) : (1 << pl.logR)) / (prune ? 2 : 1);
     const size_t smem = ((tile + 3) & ~(size_t)3) * 4 * (!pl.image && OZ_CI_DB ? 2 : 1) +
-                        (!pl.image && ci_racc(nh) ? 0 : (size_t)nh * threads * 16 * (pl.image ? 2 : 1)) +
+                        (!pl.image && (ci_racc(nh) || ci_gacc(nh)) ? 0 : (size_t)nh * threads * 16 * (pl.image ? 2 : 1)) +
                         (!pl.image && OZ_CI_T0S && pl.logR >= OZ_CI_T0S
                              ? (size_t)2 * ((size_t)1 << col_s1(pl.logR)) * ((size_t)1 << lcb) * 8 : 0);
     const int64_t nblk = (1ll << (pl.logC - lcb)) * nb * (pl.image ? 1 : 4);
