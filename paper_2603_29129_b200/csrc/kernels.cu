@@ -1150,6 +1150,11 @@ __host__ __device__ constexpr bool ci_gacc(int nh) { return OZ_CI_GACC && !ci_ra
 #ifndef OZ_CF_MINB
 #define OZ_CF_MINB 5
 #endif
+#ifndef OZ_CF_QLOOP
+#define OZ_CF_QLOOP 0  // k_col_fwd (real mode): one CTA does both primes of its (part, column block);
+                       // measured slower (c3 col_fwd 180.5 vs 175.8 us, c2 44.2 vs 37.3 us): half as
+                       // many CTAs, and the first tile load is already hidden behind the twiddle staging
+#endif
 template <int LOGR>
 struct ColCfg {
   static constexpr int min_blocks_fwd = col_loge(LOGR) == 5 ? 1 : OZ_CF_MINB;
@@ -1190,31 +1195,44 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(C
   constexpr uint32_t ncb = 1u << (LOGC - LOGCB);
   constexpr int CNT = RoundT<LOGR, false, 0, LOGE>::cnt;
   const uint32_t cb = blockIdx.x % ncb;
-  uint32_t v = blockIdx.x / ncb;  // (b * 2 + q) * 2 + a
+  // OZ_CF_QLOOP (real mode): one CTA per (transform, part, column block) transforms the part's
+  // slices for BOTH primes in turn -- 2 ka tiles per CTA instead of ka, so only one tile load
+  // in 2 ka (not one in ka) has nothing to overlap with; the raw digits are prefetched and
+  // lifted (ruling 5) when the tile starts.  Otherwise v = (b * 2 + q) * 2 + a.
+  constexpr bool QL = OZ_CF_QLOOP && !IMG;
+  uint32_t v = blockIdx.x / ncb;
   const int a = (int)(v & 1); v >>= 1;
-  const int q = (int)(v & 1); v >>= 1;
+  int q0 = 0;
+  if constexpr (!QL) { q0 = (int)(v & 1); v >>= 1; }
   const int64_t b = v;
   const int32_t* st = P.stats + b * stats_stride(P.K);
   const int ka = st[a];  // 0 if the transform is non-finite
   // unit (cv, q) needs part a if conv_a(cv) == a
-  const uint32_t need = a == 0 ? ((1u << (0 * 2 + q)) | (1u << (3 * 2 + q)))
-                               : ((1u << (1 * 2 + q)) | (1u << (2 * 2 + q)));
-  if (ka == 0 || !(P.unit_mask & need)) return;
+  auto need = [&](int q) {
+    return a == 0 ? ((1u << (0 * 2 + q)) | (1u << (3 * 2 + q))) : ((1u << (1 * 2 + q)) | (1u << (2 * 2 + q)));
+  };
+  int nq = 1;
+  if constexpr (QL) {
+    const bool n0 = (P.unit_mask & need(0)) != 0, n1 = (P.unit_mask & need(1)) != 0;
+    if (!n0 && !n1) return;
+    q0 = n0 ? 0 : 1;
+    nq = n0 && n1 ? 2 : 1;
+  } else {
+    if (!(P.unit_mask & need(q0))) return;
+  }
+  if (ka == 0) return;
   const int c = threadIdx.x & (Cb - 1);
   const int tv = threadIdx.x >> LOGCB;
-  const uint32_t p = q ? P.p[1] : P.p[0];
   const uint32_t col = (cb << LOGCB) + c;
-  const uint2* T = P.tw + (size_t)(q * 2 + 0) * m;
   const uint32_t lim = P.in_len > col ? (uint32_t)(P.in_len - col) : 0u;  // e*C < lim <=> i < in_len
   constexpr int S1 = col_s1(LOGR);
   constexpr uint32_t TILEW = (((1u << LOGR) + (1u << LOGR) / E + 1) * Cb + 1) & ~1u;  // 8-byte aligned
-  uint2* tw0 = reinterpret_cast<uint2*>(smem + TILEW);  // [2^S1][Cb] step-1 twiddles
-  stage_col_tw0<S1, Cb>(tw0, T, C, cb << LOGCB);
-  __syncthreads();
-  uint32_t nxt[E];
-  [[maybe_unused]] const uint2 io = P.io[q][a];
-  auto fetch = [&](int s) {
+  uint2* tw0 = reinterpret_cast<uint2*>(smem + TILEW);  // [nq][2^S1][Cb] step-1 twiddles
+  uint32_t nxt[E];  // IMG: residues of the image; real mode: raw digits (lifted at use)
+  auto fetch = [&](int s, int q) {
     if constexpr (IMG) {  // image a of slice s from both parts' digits (f2; P.image)
+      const uint2 io = P.io[q][a];
+      const uint32_t p = q ? P.p[1] : P.p[0];
       const int32_t* Dr = P.digits + ((b * 2 + 0) * P.K + s) * P.in_len + col;
       const int32_t* Di = P.digits + ((b * 2 + 1) * P.K + s) * P.in_len + col;
 #pragma unroll
@@ -1227,20 +1245,27 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_fwd) k_col_fwd(C
 #pragma unroll
       for (int i = 0; i < CNT; ++i) {
         const uint32_t e = round_elem<LOGR, false, 0, LOGE>(tv, i);
-        nxt[i] = e * C < lim ? lift(__ldg(&D[e * C]), p) : 0u;
+        nxt[i] = e * C < lim ? (uint32_t)__ldg(&D[e * C]) : 0u;
       }
     }
   };
-  fetch(0);
-  for (int s = 0; s < ka; ++s) {
+  fetch(0, q0);  // in flight while the twiddles are staged
+  for (int k = 0; k < nq; ++k)
+    stage_col_tw0<S1, Cb>(tw0 + k * (Cb << S1), P.tw + (size_t)((q0 + k) * 2 + 0) * m, C, cb << LOGCB);
+  __syncthreads();
+  const int nit = nq * ka;
+  for (int it = 0; it < nit; ++it) {
+    const int k = it >= ka ? 1 : 0, s = it - k * ka, q = q0 + k;
+    const uint32_t p = q ? P.p[1] : P.p[0];
+    const uint2* T = P.tw + (size_t)(q * 2 + 0) * m;
     uint32_t cur[E];
 #pragma unroll
-    for (int i = 0; i < E; ++i) cur[i] = nxt[i];
-    if (s + 1 < ka) fetch(s + 1);
-    if (s > 0) __syncthreads();  // smem tile free
+    for (int i = 0; i < E; ++i) cur[i] = IMG ? nxt[i] : lift((int32_t)nxt[i], p);
+    if (it + 1 < nit) fetch(it + 1 >= ka ? it + 1 - ka : it + 1, it + 1 >= ka ? q0 + 1 : q0);
+    if (it > 0) __syncthreads();  // smem tile free
     uint32_t* out = P.Y + (((b * 2 + q) * 2 + a) * P.K + s) * (int64_t)m + col;
     sub_ntt_t0<LOGR, false, Cb, LOGE, ZHI>(
-        tv, smem + c, col, C, T, Tw0{tw0, (uint32_t)c, (uint32_t)Cb}, p,
+        tv, smem + c, col, C, T, Tw0{tw0 + k * (Cb << S1), (uint32_t)c, (uint32_t)Cb}, p,
         [&](int i, uint32_t) -> uint32_t { return cur[i]; },
         [&](int, uint32_t e, uint32_t val) { out[e * C] = val; });
   }
@@ -3071,7 +3096,8 @@ static NttLaunch ntt_launch_cfg(const Plan& pl) {
   NttLaunch c;
   c.logCb = col_logCb(pl.logR, pl.logC);
   c.col_smem = col_smem(pl.logR, c.logCb);
-  c.col_fwd_smem = ((c.col_smem + 7) & ~(size_t)7) + ((size_t)1 << col_s1(pl.logR)) * ((size_t)1 << c.logCb) * 8;
+  c.col_fwd_smem = ((c.col_smem + 7) & ~(size_t)7) +
+                   (OZ_CF_QLOOP && !pl.image ? 2 : 1) * ((size_t)1 << col_s1(pl.logR)) * ((size_t)1 << c.logCb) * 8;
   c.col_threads = col_threads(pl.logR, c.logCb);
   const size_t C = 1ull << pl.logC;
   const int rle = row_loge(pl.logC, pl.logR > 0);
@@ -3119,6 +3145,7 @@ bool decomposition_supported(int logR, int logC) {
 
 static void launch_col_fwd(int logR, int logC, unsigned nblk, const NttLaunch& c, cudaStream_t st,
                            const ColParams& CP, bool zhi = false) {
+  if (OZ_CF_QLOOP && !CP.image) nblk /= 2;  // both primes in one CTA
   dispatch_rc(logR, logC, [&](auto I, auto J) {
     if (CP.image && zhi) {
       set_smem(k_col_fwd<I.value, J.value, true, true>, c.col_fwd_smem);
