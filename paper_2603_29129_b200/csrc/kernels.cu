@@ -1144,6 +1144,9 @@ __host__ __device__ constexpr bool ci_gacc(int nh) { return OZ_CI_GACC && !ci_ra
 #define OZ_CI_T0S 8  // k_col_inv_crt: step-1 round column twiddles staged in shared memory
 #endif  // for log2 R >= this (c3 803 -> 769 us; shorter columns lose: c4 658 -> 715, c2 132 -> 215,
         // wider column blocks make the table large and the snake order already reuses L1)
+#ifndef OZ_CI_FETCH_FIRST
+#define OZ_CI_FETCH_FIRST 0  // k_col_inv_crt: the first tile's loads issued before the CTA's set-up
+#endif
 #ifndef OZ_CI_ILP
 #define OZ_CI_ILP 4  // k_col_inv_crt: CRT + DD chains interleaved per batch
 #endif
@@ -2536,6 +2539,22 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
   __shared__ int s_ce[kMaxK * kMaxK];
   const int32_t* srow = P.sched + (b * 4 + cv) * sched_stride(P.K, P.L);
   const int ng = srow[0];
+  const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
+  uint32_t nxt[E];
+  // tile t -> (group g, prime q): t = 2 g + (q xor snake(g)).  With OZ_CI_SNAKE the primes
+  // alternate q0 q1 | q1 q0 | q0 q1 ..., so each prime's column twiddles serve two tiles in a
+  // row (L1 reuse); the group's second tile runs Garner either way.
+  constexpr bool SNAKE = LOGR >= OZ_CI_SNAKE_MIN && LOGR <= OZ_CI_SNAKE_MAX;
+  auto tile_q = [](int t) { return SNAKE ? ((t & 1) ^ ((t >> 1) & 1)) : (t & 1); };
+  auto fetch = [&](int t) {
+    const int g = t >> 1, q = tile_q(t);
+    const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * (int64_t)m + col;
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0, LOGE>(tv, i) * C]);
+  };
+#if OZ_CI_FETCH_FIRST
+  if (ng > 0) fetch(0);  // in flight during the schedule, accumulator and twiddle set-up
+#endif
   for (int g = tid; g < ng; g += blockDim.x) {
     s_ce[g] = srow[1 + g * (2 + 2 * P.L)];
     s_sc[g] = scalbn(1.0, -s_ce[g]);
@@ -2572,20 +2591,9 @@ __global__ void __launch_bounds__(256, ColCfg<LOGR>::min_blocks_inv_crt) k_col_i
     for (int q = 0; q < 2; ++q)
       stage_col_tw0<S1, Cb>(tw0 + q * (Cb << S1), P.tw + (size_t)(q * 2 + 1) * m, C, cb << LOGCB);
   }
-  const uint32_t lim = P.n > col ? (uint32_t)(P.n - col) : 0u;
-  uint32_t nxt[E];
-  // tile t -> (group g, prime q): t = 2 g + (q xor snake(g)).  With OZ_CI_SNAKE the primes
-  // alternate q0 q1 | q1 q0 | q0 q1 ..., so each prime's column twiddles serve two tiles in a
-  // row (L1 reuse); the group's second tile runs Garner either way.
-  constexpr bool SNAKE = LOGR >= OZ_CI_SNAKE_MIN && LOGR <= OZ_CI_SNAKE_MAX;
-  auto tile_q = [](int t) { return SNAKE ? ((t & 1) ^ ((t >> 1) & 1)) : (t & 1); };
-  auto fetch = [&](int t) {
-    const int g = t >> 1, q = tile_q(t);
-    const uint32_t* in = P.G + (((b * 2 + q) * 4 + cv) * G + g) * (int64_t)m + col;
-#pragma unroll
-    for (int i = 0; i < CNT; ++i) nxt[i] = __ldcs(&in[round_elem<LOGR, true, 0, LOGE>(tv, i) * C]);
-  };
+#if !OZ_CI_FETCH_FIRST
   if (ng > 0) fetch(0);
+#endif
   __syncthreads();  // s_sc ready
   uint32_t r0[NH];  // the group's first tile's residues
   double2* const So = P.S + (b * 4 + cv) * P.n + col;
