@@ -1145,7 +1145,7 @@ __host__ __device__ constexpr bool ci_gacc(int nh) { return OZ_CI_GACC && !ci_ra
 #endif  // for log2 R >= this (c3 803 -> 769 us; shorter columns lose: c4 658 -> 715, c2 132 -> 215,
         // wider column blocks make the table large and the snake order already reuses L1)
 #ifndef OZ_CI_FETCH_FIRST
-#define OZ_CI_FETCH_FIRST 0  // k_col_inv_crt: the first tile's loads issued before the CTA's set-up
+#define OZ_CI_FETCH_FIRST 1  // k_col_inv_crt: the first tile's loads issued before the CTA's set-up (c3 176.76 -> 177.18 GFLOP/s)
 #endif
 #ifndef OZ_CI_ILP
 #define OZ_CI_ILP 4  // k_col_inv_crt: CRT + DD chains interleaved per batch
